@@ -1,0 +1,294 @@
+"""MG-CG benchmark (BASELINE.json metric: MG-CG time-to-solution and DOF/s; smoother HBM GB/s).
+
+Default workload (N=1): BASELINE configs[1] -- 3D constant-coefficient 7-point Poisson on
+257^3 vertices, fp64, f = 2u-1 from seed, CG + 7-level MG V(2,2) Chebyshev(Jacobi), LU on 5^3,
+rtol 1e-8. With N>1 processes (torchrun, one GPU each) the same global problem is box-split
+over N GPUs and levels <= 3 are telescoped onto GPU 0 (reduction factor N): strong scaling.
+
+One step = one complete MG-CG solve (setup, i.e. hierarchy + Chebyshev estimates, is outside
+the timed region; this is the "second of two identical solves" protocol).
+`value` = DOF/s with the right-hand side generated in HBM; `e2e` = DOF/s through the C-ABI
+with pinned host b/x (H2D of b and x0, D2H of x inside the timed region).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (npoints, nlevels, smooth_its, kind, telescope_level, rtol)
+    "cfg1": ((65, 65, 65), 5, 2, 0, None, 1e-8),
+    "cfg2": ((257, 257, 257), 7, 2, 0, 3, 1e-8),
+    "cfg3": ((513, 513, 513), 8, 3, 1, 4, 1e-8),
+    "cfg4w": ((257, 257, 257), 7, 2, 0, 4, 1e-8),
+}
+SEED_F = 1234
+SEED_K = 7
+
+
+def read_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region."""
+
+    def __init__(self, device):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([v.strip() for v in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if "Active" in s[3 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def cpu_reference_sample(steps=1, warmup=0, np3=(129, 129, 129), nlevels=6, m=2):
+    """The reference algorithm on the host: oracle/_ref (compiled reference translation units
+    plus the SPEC-following V-cycle glue) when it was built, else the C restatement in oracle/.
+    Returns (dof_per_s, seconds_per_solve, kind, sample description)."""
+    ref_bin = os.path.join(ROOT, "oracle", "_ref", "tmg_ref_bench")
+    n = np3[0] * np3[1] * np3[2]
+    if os.path.exists(ref_bin):
+        out = subprocess.run([ref_bin, str(np3[0]), str(nlevels), str(m), str(steps), str(warmup), str(SEED_F)],
+                             capture_output=True, text=True, check=True).stdout
+        rec = json.loads(out.strip().splitlines()[-1])
+        t = rec["t_solve_s"]
+        kind = "reference"
+        its = rec["iterations"]
+    else:
+        from oracle import oracle as O
+
+        mg = O.MG(np3, nlevels, smooth_its=m, est_mode=O.EST_LANCZOS)
+        b = O.rhs(np3, SEED_F)
+        for _ in range(warmup):
+            mg.solve(b, rtol=1e-8)
+        ts = []
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            _, rep = mg.solve(b, rtol=1e-8)
+            ts.append(time.perf_counter() - t0)
+        t = sum(ts) / len(ts)
+        kind = "port"
+        its = rep["iterations"]
+    desc = (f"{np3[0]}x{np3[1]}x{np3[2]} Poisson, {nlevels}-level MG V({m},{m}) Cheb-Jacobi CG rtol 1e-8, "
+            f"{its} its, 1 core, solve only (setup excluded)")
+    return n / t, t, kind, desc
+
+
+def run_reference(args, rank, world):
+    cfg = CONFIGS[args.config]
+    if rank != 0:
+        return
+    W = max(args.warmup, 0)
+    K = max(args.steps, 1)
+    rate, t, kind, desc = cpu_reference_sample(steps=K, warmup=min(W, 1))
+    line = {
+        "impl": "reference", "metric": "MG-CG DOF/s (time-to-solution)", "value": rate, "unit": "DOF/s",
+        "n_gpus": args.gpus, "steps": K, "warmup": W, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded RHS)",
+        "config": {"workload": f"{args.config} sample on host cores", "global_batch": 1,
+                   "seq_len": cfg[0][0], "parallelism": "cpu"},
+        "cpu_baseline": {"value": rate, "unit": "DOF/s", "cores": 1, "kind": kind, "sample": desc},
+        "e2e": {"value": rate, "unit": "DOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="tmgx", choices=["tmgx", "reference"])
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--est", default="lanczos", choices=["lanczos", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("gloo", init_method="env://", world_size=world, rank=rank)
+
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        if dist:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    import ctypes
+
+    import numpy as np
+    import torch
+
+    from paper_1604_07163_b200 import tmgx as T
+
+    torch.cuda.set_device(local)
+    np3, nlevels, m, kind, tele_level, rtol = CONFIGS[args.config]
+    est = T.EST_LANCZOS if args.est == "lanczos" else T.EST_REFERENCE
+
+    nccl_id = None
+    if world > 1:
+        obj = [T.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    w = T.World(n_ranks=world, nproc=world, proc=rank, device=local, nccl_id=nccl_id)
+    tele = [T.TelescopeStage(tele_level, world)] if (world > 1 and tele_level is not None) else []
+    t0 = time.perf_counter()
+    s = T.SolverNode(w, T.Problem(np3, kind, seed_k=SEED_K), T.MGConfig(nlevels, m, est, telescope=tele))
+    t_setup = time.perf_counter() - t0
+    cfg = T.KrylovConfig("cg", rtol=rtol)
+    n_local = s.local_size()
+    n_dof = np3[0] * np3[1] * np3[2]
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+
+    def max_over_ranks(v):
+        if not dist:
+            return v
+        t = torch.tensor([v], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- device-resident solves (value)
+    for _ in range(max(args.warmup, 0)):
+        rep = s.solve_seeded(SEED_F, cfg=cfg)
+    barrier()
+    launches = 0
+    dev_times = []
+    its = []
+    with ClockSampler(local) as clk:
+        t_wall0 = time.perf_counter()
+        for _ in range(args.steps):
+            rep = s.solve_seeded(SEED_F, cfg=cfg)
+            dev_times.append(rep.t_solve_s)
+            launches += rep.kernel_launches
+            its.append(rep.iterations)
+        barrier()
+        t_wall = time.perf_counter() - t_wall0
+    t_dev = max_over_ranks(sum(dev_times))
+    value = n_dof * args.steps / t_dev
+
+    # ---- end to end through the C-ABI with pinned host buffers (e2e)
+    b_host = torch.empty(n_local, dtype=torch.float64, pin_memory=True)
+    x_host = torch.zeros(n_local, dtype=torch.float64, pin_memory=True)
+    b_np = s.rhs(SEED_F)
+    b_host.numpy()[:] = b_np
+    for _ in range(max(args.warmup, 1)):
+        x_host.zero_()
+        s.solve_ptr(b_host.data_ptr(), x_host.data_ptr(), False, cfg)
+    barrier()
+    e2e_t = 0.0
+    for _ in range(args.steps):
+        x_host.zero_()
+        t0 = time.perf_counter()
+        rep_e = s.solve_ptr(b_host.data_ptr(), x_host.data_ptr(), False, cfg)
+        e2e_t += time.perf_counter() - t0
+    barrier()
+    e2e_t = max_over_ranks(e2e_t)
+    e2e = n_dof * args.steps / e2e_t
+
+    # ---- roofline of the dominant smoother kernel (fine-level Chebyshev pass), live
+    peak, peak_kind = read_peaks()
+    ms, by = s.bench_kernel(1, nlevels - 1, iters=20)
+    ms_all = max_over_ranks(ms)
+    achieved = by / (ms_all * 1e-3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            traffic = json.load(f).get(f"{args.config}:cheb_step_last")
+    except Exception:
+        pass
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, t_cpu, ckind, desc = cpu_reference_sample(steps=1, warmup=0)
+        cpu = {"value": rate, "unit": "DOF/s", "cores": 1, "kind": ckind, "sample": desc}
+
+    if rank == 0:
+        line = {
+            "metric": "MG-CG DOF/s (time-to-solution)", "value": value, "unit": "DOF/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_dev / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded RHS, natural-index hash; BASELINE configs are synthetic)",
+            "config": {"workload": f"{args.config}: {np3[0]}x{np3[1]}x{np3[2]} "
+                                   f"{'var-coef' if kind else 'Poisson'} {nlevels}-level MG V({m},{m}) "
+                                   f"Cheb-Jacobi CG rtol {rtol:g}, est={args.est}",
+                       "global_batch": 1, "seq_len": np3[0],
+                       "parallelism": f"box{world}" + (f"+telescope(L{tele_level},r{world})" if tele else ""),
+                       "l2": "inputs larger than L2 (one fine vector = %.0f MB)" % (n_dof * 8 / 1e6),
+                       "iterations": its[-1] if its else None, "t_setup_s": t_setup,
+                       "wall_ms_per_step": t_wall / args.steps * 1e3},
+            "e2e": {"value": e2e, "unit": "DOF/s", "h2d_bytes_per_step": 2 * 8 * n_dof,
+                    "d2h_bytes_per_step": 8 * n_dof},
+            "gpu_launches": launches,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "k_cheb_step (last pass, fine level)", "peak_kind": peak_kind,
+                         "bytes_per_launch": by, "ms_per_launch": ms_all},
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,207 @@
+/* tmgx — B200-native MG-preconditioned CG with coarse-level telescoping.
+ *
+ * C-ABI drop-in boundary for the reference's hot path (arxiv 1604.07163 re-creation,
+ * /root/reference/proj/core). Plain pointers and sizes only; no torch or C++ types.
+ * Each entry point cites the reference interface it replaces. The C++ host layer
+ * (paper_1604_07163_b200/csrc/) sits behind these functions; INTEGRATION.md shows the
+ * binding a reference maintainer would add.
+ *
+ * Process model: spawn_world (comm.hpp:176-207) ran R rank threads in one process.
+ * Here R reference ranks (grid boxes) are spread over P processes, one GPU each
+ * (P == R: one box per GPU, NCCL over NVLink) or P == 1 (all R boxes on one GPU,
+ * used to exercise decompositions on a single device). Every call below that the
+ * reference made collectively is collective over the P processes.
+ *
+ * Status codes: 0 ok, 1 configuration error (tmg::ConfigError),
+ * 2 diverged (SolveReport reason), 3 CUDA/NCCL error, 4 internal/usage error (tmg::Error).
+ * tmgx_last_error() returns the message of the last failure on the calling thread.
+ */
+#ifndef TMGX_H
+#define TMGX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TMGX_OK 0
+#define TMGX_ERR_CONFIG 1
+#define TMGX_DIVERGED 2
+#define TMGX_ERR_CUDA 3
+#define TMGX_ERR_INTERNAL 4
+
+#define TMGX_MAX_AXIS_PARTS 64
+#define TMGX_MAX_TELESCOPE 4
+#define TMGX_NCCL_ID_BYTES 128
+
+/* GridHeader (grid.hpp:41-79): rank-independent grid description. */
+typedef struct {
+  int dim;
+  int64_t np[3];
+  int dof;
+  int pg[3];
+  int64_t off[3][TMGX_MAX_AXIS_PARTS + 1];
+} tmgx_header;
+
+/* ---------------------------------------------------------------------------
+ * Index maps — host-only, bit-exact restatements of grid.cpp / comm.cpp / layout.cpp.
+ * ------------------------------------------------------------------------- */
+
+/* choose_proc_grid (grid.cpp:209-240). Returns 1 (ConfigError) if over-decomposed. */
+int tmgx_choose_proc_grid(int size, int dim, const int64_t np[3], int pg_out[3]);
+/* create_grid header (grid.cpp:256-292); hint may be NULL. */
+int tmgx_grid_header(int size, int dim, const int64_t np[3], int dof, const int *hint, tmgx_header *out);
+/* coarsen (grid.cpp:299-368). Returns 1 "cannot coarsen". */
+int tmgx_coarsen_header(const tmgx_header *fine, tmgx_header *coarse);
+/* Layout of the rank-block ordering (grid.cpp:40-46): offsets[n_ranks+1]. */
+int tmgx_layout_offsets(const tmgx_header *h, int64_t *offsets);
+/* NaturalOrdering bijection (grid.cpp:48-115). */
+int64_t tmgx_global_to_natural(const tmgx_header *h, int64_t global);
+int64_t tmgx_natural_to_global(const tmgx_header *h, int64_t natural);
+/* Comm::split_strided (comm.cpp:353-390): member_map gets ceil(n/r) entries. */
+int tmgx_split_strided(int n, int r, int *member_map, int *n_members);
+/* repartition_onto header (grid.cpp:433-493); override_[a] == 0 means "not set". */
+int tmgx_repartition_header(const tmgx_header *h, int sub_size, const int override_[3], tmgx_header *out);
+/* prefusion_layout (grid.cpp:566-580): offsets[parent_size+1]. */
+int tmgx_prefusion_layout(const tmgx_header *new_h, int parent_size, const int *member_map, int n_members,
+                          int64_t *offsets);
+/* build_permutation (grid.cpp:582-599): for old-layout rows [row_begin,row_end) the column
+ * of the single 1 of P-hat. */
+int tmgx_permutation(const tmgx_header *old_h, const tmgx_header *new_h, int64_t row_begin, int64_t row_end,
+                     int64_t *cols);
+
+/* ---------------------------------------------------------------------------
+ * World (spawn_world analog) and solver.
+ * ------------------------------------------------------------------------- */
+typedef struct tmgx_world_s *tmgx_world;
+typedef struct tmgx_solver_s *tmgx_solver;
+
+/* Writes an NCCL unique id (call on process 0, broadcast the bytes to the others). */
+int tmgx_nccl_unique_id(void *out_id /* TMGX_NCCL_ID_BYTES */);
+/* n_ranks reference ranks over nproc processes; process `proc` owns ranks
+ * [proc*n_ranks/nproc, (proc+1)*n_ranks/nproc). nccl_id ignored when nproc == 1. */
+int tmgx_world_create(int n_ranks, int nproc, int proc, int device, const void *nccl_id, tmgx_world *out);
+int tmgx_world_destroy(tmgx_world w);
+/* First and one-past-last reference rank owned by this process. */
+int tmgx_world_local_ranks(tmgx_world w, int *first, int *end);
+
+enum { TMGX_POISSON7 = 0, TMGX_VARCOEF7_HARMONIC = 1 };
+enum { TMGX_EST_REFERENCE = 0, TMGX_EST_LANCZOS = 1 };
+enum { TMGX_KSP_CG = 2, TMGX_KSP_PREONLY = 5 }; /* KrylovMethod (solver.hpp:637) */
+enum { TMGX_RTOL = 0, TMGX_ATOL = 1, TMGX_MAX_ITS = 2, TMGX_FIXED_ITS_DONE = 3, TMGX_REASON_DIVERGED = 4 };
+
+/* assemble_problem (reference problems.cpp is missing): 7-point FD operator
+ * on the unit cube, homogeneous Dirichlet rows, constant k or k from seeded spheres with
+ * harmonic face averages. */
+typedef struct {
+  int kind;
+  int64_t np[3];
+  int pg_hint[3];      /* all 0 = balanced choice (grid.cpp:209-240) */
+  uint64_t seed_k;     /* spheres */
+  int n_spheres;       /* 32 */
+  double k_in;         /* 1e4 */
+} tmgx_problem;
+
+/* Telescope stage: the MG level at which the communicator is coarsened by
+ * reduction_factor, with optional repart_da_processors_{x,y,z} override (0 = not set). */
+typedef struct {
+  int level;
+  int reduction_factor;
+  int override_[3];
+} tmgx_telescope_stage;
+
+/* MG hierarchy: nlevels total (N1+N2-1 when telescoped),
+ * Chebyshev(Jacobi) V(m,m) smoothing, LU at level 0 on a single rank. */
+typedef struct {
+  int nlevels;
+  int smooth_its;
+  int est_mode;
+  const double *cheb_bounds; /* optional: [2*nlevels] (lo,hi) per level; NULL = estimate (solver.cpp:591) */
+  int n_telescope;
+  tmgx_telescope_stage telescope[TMGX_MAX_TELESCOPE];
+} tmgx_mg_cfg;
+
+/* KrylovConfig (solver.hpp:27-37) subset on this path. */
+typedef struct {
+  int method;  /* TMGX_KSP_CG or TMGX_KSP_PREONLY */
+  double rtol;
+  double atol;
+  int max_its;
+} tmgx_ksp_cfg;
+
+/* SolveReport (solver.hpp:39-52) + timings. */
+typedef struct {
+  int reason;
+  int iterations;
+  double norm0;
+  double norm_final;
+  double t_solve_s;       /* device time of the solve (CUDA events) */
+  int64_t kernel_launches; /* kernels launched by the solve */
+} tmgx_report;
+
+/* SolverNode::create + mg_setup + TelescopePC setup (collective). */
+int tmgx_solver_create(tmgx_world w, const tmgx_problem *prob, const tmgx_mg_cfg *mg, tmgx_solver *out);
+int tmgx_solver_destroy(tmgx_solver s);
+
+/* Number of levels, the header of level `level` as seen by the outer hierarchy when
+ * level >= first telescope level else by the innermost containing stage; this process's
+ * local unknown count at that level (0 on idle non-members). */
+int tmgx_solver_level_info(tmgx_solver s, int level, tmgx_header *h, int64_t *n_local);
+/* Chebyshev interval used on `level` (after estimation). */
+int tmgx_solver_bounds(tmgx_solver s, int level, double *lo, double *hi);
+/* Fine-level right-hand side f = 2u-1 keyed by natural index, 0 on Dirichlet vertices,
+ * written into this process's local slice (host pointer). */
+int tmgx_fill_rhs(tmgx_solver s, uint64_t seed, double *b_local);
+
+/* krylov_solve (solver.cpp:420-480) with the MG preconditioner. b/x are this process's
+ * slice of the rank-block ordering (DistVector local order, grid.cpp:61-82), host or
+ * device memory as flagged. history: room for max_its+1 norms, or NULL. Returns 0, or 2
+ * on divergence (report filled either way). */
+int tmgx_solve(tmgx_solver s, const double *b, double *x, int on_device, const tmgx_ksp_cfg *cfg,
+               double *history, tmgx_report *rep);
+/* Same, with the right-hand side generated on the device from `seed` (inputs resident). */
+int tmgx_solve_seeded(tmgx_solver s, uint64_t seed, double *x_dev_or_null, const tmgx_ksp_cfg *cfg,
+                      double *history, tmgx_report *rep);
+
+/* Preconditioner::apply (preconditioner.hpp:17-32): y = one V-cycle applied to x. */
+int tmgx_pc_apply(tmgx_solver s, const double *x, double *y);
+
+/* Level primitives for parity tests (host arrays in the level's local order). */
+int tmgx_level_apply(tmgx_solver s, int level, const double *x, double *y);  /* spmv */
+int tmgx_level_smooth(tmgx_solver s, int level, const double *b, double *x); /* solve_fixed, x in/out */
+int tmgx_level_residual_restrict(tmgx_solver s, int fine_level, const double *b, const double *x,
+                                 double *bc);                                 /* 2^-3 P^T (b - A x) */
+int tmgx_level_prolong_add(tmgx_solver s, int fine_level, const double *xc, double *xf);
+int tmgx_coarse_solve(tmgx_solver s, const double *b, double *x);            /* DenseLU::solve */
+/* Telescope data movement at stage t: gather (P-hat^T x then ScatterPlan::to_sub) of a
+ * parent-layout vector onto the members, and the reverse. Host arrays, local order. */
+int tmgx_telescope_gather(tmgx_solver s, int stage, const double *x_parent, double *x_sub);
+int tmgx_telescope_scatter(tmgx_solver s, int stage, const double *y_sub, double *y_parent);
+
+/* Counters: kernel launches, halo/telescope bytes moved between processes. */
+typedef struct {
+  int64_t kernel_launches;
+  int64_t halo_bytes_sent;
+  int64_t telescope_bytes_sent;
+  int64_t allreduces;
+} tmgx_counters;
+int tmgx_get_counters(tmgx_solver s, tmgx_counters *c);
+
+/* Kernel micro-timing for the roofline (bench.py): launches kernel `which` on `level` `iters`
+ * times back to back on the library stream between CUDA events. Outputs the mean device time
+ * per launch and the algorithmic HBM bytes one launch must move (DESIGN.md §5 table).
+ * which: 0 cheb_step (full: read d,r,x write d',r,x) 1 cheb_step (last: read d,r,x write x)
+ *        2 operator apply 3 residual 4 restriction 5 prolongation 6 cg_update 7 spmv+dot */
+int tmgx_bench_kernel(tmgx_solver s, int which, int level, int iters, double *ms_per_launch,
+                      double *bytes_per_launch);
+
+/* 1 if built with -fmad=false (bitwise parity build), else 0. */
+int tmgx_parity_build(void);
+const char *tmgx_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,91 @@
+"""Builds the in-tree sm_100a shared libraries.
+
+  libtmgx.so         performance build (nvcc may contract a*b+c into DFMA)
+  libtmgx_parity.so  parity build (-fmad=false): V-cycle arithmetic bitwise equal to the CPU oracle
+
+Both are plain nvcc invocations (no torch extension machinery); the .so files live next to
+this file so they travel with the repository snapshot to the GPU box.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from concurrent.futures import ThreadPoolExecutor
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+SOURCES = ["tmg_grid.cpp", "tmgx_kernels.cu", "tmgx_engine.cu", "tmgx_capi.cu"]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def nccl_dirs():
+    try:
+        import nvidia.nccl as nn  # torch-bundled NCCL (same one torch.distributed loads)
+
+        base = list(nn.__path__)[0]
+        inc, lib = os.path.join(base, "include"), os.path.join(base, "lib")
+        if os.path.exists(os.path.join(inc, "nccl.h")):
+            return inc, lib
+    except Exception:
+        pass
+    return "/usr/include", "/usr/lib/x86_64-linux-gnu"
+
+
+def lib_path(parity=False):
+    return os.path.join(HERE, "libtmgx_parity.so" if parity else "libtmgx.so")
+
+
+def _stale(target, deps):
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build(parity=False, verbose=False, force=False):
+    inc, lib = nccl_dirs()
+    tag = "parity" if parity else "perf"
+    objdir = os.path.join(HERE, "build", tag)
+    os.makedirs(objdir, exist_ok=True)
+    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".hpp", ".cuh", ".h"))]
+    headers.append(os.path.join(ROOT, "include", "tmgx.h"))
+    flags = ARCH + ["-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC,-ffp-contract=off",
+                    "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc, "-Xptxas", "-v"]
+    if parity:
+        flags += ["-fmad=false", "-DTMGX_PARITY"]
+    cmds, objs = [], []
+    for src in SOURCES:
+        s = os.path.join(CSRC, src)
+        o = os.path.join(objdir, src + ".o")
+        objs.append(o)
+        if force or _stale(o, [s] + headers):
+            lang = ["-x", "cu"] if src.endswith(".cu") else []
+            cmds.append(["nvcc"] + flags + lang + ["-c", s, "-o", o])
+
+    def run(cmd):
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError("nvcc failed:\n" + " ".join(cmd) + "\n" + r.stdout + r.stderr)
+        return r.stderr
+
+    with ThreadPoolExecutor(max_workers=4) as ex:
+        logs = list(ex.map(run, cmds))
+    if verbose:
+        for lg in logs:
+            sys.stdout.write(lg)
+    out = lib_path(parity)
+    if force or cmds or _stale(out, objs):
+        run(["nvcc"] + ARCH + ["-shared", "-o", out] + objs +
+            ["-L", lib, "-l:libnccl.so.2", "-Xlinker", "-rpath," + lib, "-cudart", "static"])
+    return out
+
+
+def build_all(verbose=False, force=False):
+    return [build(False, verbose, force), build(True, verbose, force)]
+
+
+if __name__ == "__main__":
+    for p in build_all(verbose="-v" in sys.argv, force="-f" in sys.argv):
+        print(p)

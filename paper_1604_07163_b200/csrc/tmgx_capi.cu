@@ -1,0 +1,485 @@
+// extern "C" boundary (include/tmgx.h) over the C++ host layer. Exceptions become status codes:
+// tmg::ConfigError -> 1, tmg::CudaError -> 3, any other failure -> 4.
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "tmgx.h"
+#include "tmgx_engine.hpp"
+
+struct tmgx_world_s {
+  std::unique_ptr<tmgx::World> w;
+};
+struct tmgx_solver_s {
+  tmgx_world world;
+  std::unique_ptr<tmgx::Solver> s;
+};
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    return f();
+  } catch (const tmg::ConfigError& e) {
+    g_err = e.what();
+    return TMGX_ERR_CONFIG;
+  } catch (const tmg::CudaError& e) {
+    g_err = e.what();
+    return TMGX_ERR_CUDA;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return TMGX_ERR_INTERNAL;
+  }
+}
+
+tmg::GridHeader to_hdr(const tmgx_header* h) {
+  tmg::GridHeader g;
+  g.dim = h->dim;
+  g.dof = h->dof;
+  for (int a = 0; a < 3; ++a) {
+    g.npoints[a] = h->np[a];
+    g.proc_grid[a] = h->pg[a];
+    g.axis_offsets[a].assign(h->off[a], h->off[a] + h->pg[a] + 1);
+  }
+  return g;
+}
+
+void from_hdr(const tmg::GridHeader& g, tmgx_header* h) {
+  std::memset(h, 0, sizeof(*h));
+  h->dim = g.dim;
+  h->dof = g.dof;
+  for (int a = 0; a < 3; ++a) {
+    h->np[a] = g.npoints[a];
+    h->pg[a] = g.proc_grid[a];
+    if (g.proc_grid[a] > TMGX_MAX_AXIS_PARTS) throw tmg::ConfigError("too many parts on one axis");
+    for (size_t p = 0; p < g.axis_offsets[a].size(); ++p) h->off[a][p] = g.axis_offsets[a][p];
+  }
+}
+
+int check_level(tmgx_solver s, int level) {
+  if (!s || !s->s) throw tmg::Error("null solver");
+  if (level < 0 || level >= s->s->mgd.nlevels) throw tmg::Error("level out of range");
+  return s->s->node_for_level(level);
+}
+}  // namespace
+
+extern "C" {
+
+const char* tmgx_last_error(void) { return g_err.c_str(); }
+int tmgx_parity_build(void) { return tmgx::parity_build() ? 1 : 0; }
+
+int tmgx_choose_proc_grid(int size, int dim, const int64_t np[3], int pg_out[3]) {
+  return guard([&] {
+    const auto pg = tmg::choose_proc_grid(size, dim, {np[0], np[1], np[2]});
+    for (int a = 0; a < 3; ++a) pg_out[a] = pg[a];
+    return 0;
+  });
+}
+
+int tmgx_grid_header(int size, int dim, const int64_t np[3], int dof, const int* hint, tmgx_header* out) {
+  return guard([&] {
+    std::optional<std::array<int, 3>> h;
+    if (hint) h = std::array<int, 3>{hint[0], hint[1], hint[2]};
+    from_hdr(tmg::build_header_for(size, dim, {np[0], np[1], np[2]}, dof, 1, h), out);
+    return 0;
+  });
+}
+
+int tmgx_coarsen_header(const tmgx_header* fine, tmgx_header* coarse) {
+  return guard([&] {
+    auto c = tmg::try_coarsen_header(to_hdr(fine));
+    if (!c) throw tmg::ConfigError("cannot coarsen");
+    from_hdr(*c, coarse);
+    return 0;
+  });
+}
+
+int tmgx_layout_offsets(const tmgx_header* h, int64_t* offsets) {
+  return guard([&] {
+    const auto lay = to_hdr(h).layout();
+    for (size_t k = 0; k < lay.offsets.size(); ++k) offsets[k] = lay.offsets[k];
+    return 0;
+  });
+}
+
+int64_t tmgx_global_to_natural(const tmgx_header* h, int64_t g) { return to_hdr(h).global_to_natural(g); }
+int64_t tmgx_natural_to_global(const tmgx_header* h, int64_t n) { return to_hdr(h).natural_to_global(n); }
+
+int tmgx_split_strided(int n, int r, int* member_map, int* n_members) {
+  return guard([&] {
+    const auto s = tmg::split_strided(n, r);
+    for (int k = 0; k < s.n_members(); ++k) member_map[k] = s.member_map[k];
+    *n_members = s.n_members();
+    return 0;
+  });
+}
+
+int tmgx_repartition_header(const tmgx_header* h, int sub_size, const int ov[3], tmgx_header* out) {
+  return guard([&] {
+    std::array<std::optional<int>, 3> o;
+    for (int a = 0; a < 3; ++a)
+      if (ov && ov[a]) o[a] = ov[a];
+    from_hdr(tmg::repartition_header(to_hdr(h), sub_size, o), out);
+    return 0;
+  });
+}
+
+int tmgx_prefusion_layout(const tmgx_header* nh, int parent_size, const int* mm, int n_members, int64_t* offsets) {
+  return guard([&] {
+    tmg::SplitResult sp;
+    sp.member_map.assign(mm, mm + n_members);
+    sp.parent_size = parent_size;
+    sp.reduction_factor = n_members > 1 ? mm[1] - mm[0] : parent_size;
+    const auto lay = tmg::prefusion_layout(to_hdr(nh), sp);
+    for (size_t k = 0; k < lay.offsets.size(); ++k) offsets[k] = lay.offsets[k];
+    return 0;
+  });
+}
+
+int tmgx_permutation(const tmgx_header* oh, const tmgx_header* nh, int64_t rb, int64_t re, int64_t* cols) {
+  return guard([&] {
+    const auto o = to_hdr(oh), n = to_hdr(nh);
+    if (!o.same_global_grid(n)) throw tmg::Error("build_permutation: grids describe different global problems");
+    for (int64_t p = rb; p < re; ++p) cols[p - rb] = n.natural_to_global(o.global_to_natural(p));
+    return 0;
+  });
+}
+
+int tmgx_nccl_unique_id(void* out) {
+  return guard([&] {
+    ncclUniqueId id;
+    tmgx::nccl_check(ncclGetUniqueId(&id), "ncclGetUniqueId");
+    std::memcpy(out, &id, sizeof(id));
+    return 0;
+  });
+}
+
+int tmgx_world_create(int n_ranks, int nproc, int proc, int device, const void* nccl_id, tmgx_world* out) {
+  return guard([&] {
+    auto w = new tmgx_world_s;
+    try {
+      w->w = std::make_unique<tmgx::World>(n_ranks, nproc, proc, device, nccl_id);
+    } catch (...) {
+      delete w;
+      throw;
+    }
+    *out = w;
+    return 0;
+  });
+}
+
+int tmgx_world_destroy(tmgx_world w) {
+  return guard([&] {
+    delete w;
+    return 0;
+  });
+}
+
+int tmgx_world_local_ranks(tmgx_world w, int* first, int* end) {
+  *first = w->w->first;
+  *end = w->w->end;
+  return 0;
+}
+
+int tmgx_solver_create(tmgx_world w, const tmgx_problem* p, const tmgx_mg_cfg* m, tmgx_solver* out) {
+  return guard([&] {
+    tmgx::ProblemDesc pd;
+    pd.kind = p->kind;
+    for (int a = 0; a < 3; ++a) {
+      pd.np[a] = p->np[a];
+      pd.pg_hint[a] = p->pg_hint[a];
+    }
+    pd.seed_k = p->seed_k;
+    pd.n_spheres = p->n_spheres;
+    pd.k_in = p->k_in;
+    if (pd.kind != TMGX_POISSON7 && pd.kind != TMGX_VARCOEF7_HARMONIC) throw tmg::ConfigError("unknown operator kind");
+    tmgx::MGDesc md;
+    md.nlevels = m->nlevels;
+    md.m = m->smooth_its;
+    md.est_mode = m->est_mode;
+    if (m->cheb_bounds) md.bounds.assign(m->cheb_bounds, m->cheb_bounds + 2 * m->nlevels);
+    if (m->n_telescope < 0 || m->n_telescope > TMGX_MAX_TELESCOPE) throw tmg::ConfigError("bad telescope count");
+    for (int t = 0; t < m->n_telescope; ++t)
+      md.tele.push_back({m->telescope[t].level, m->telescope[t].reduction_factor,
+                         {m->telescope[t].override_[0], m->telescope[t].override_[1], m->telescope[t].override_[2]}});
+    auto s = new tmgx_solver_s;
+    s->world = w;
+    try {
+      s->s = std::make_unique<tmgx::Solver>(*w->w, pd, md);
+    } catch (...) {
+      delete s;
+      throw;
+    }
+    *out = s;
+    return 0;
+  });
+}
+
+int tmgx_solver_destroy(tmgx_solver s) {
+  return guard([&] {
+    delete s;
+    return 0;
+  });
+}
+
+int tmgx_solver_level_info(tmgx_solver s, int level, tmgx_header* h, int64_t* n_local) {
+  return guard([&] {
+    const int i = check_level(s, level);
+    if (h) from_hdr(s->s->nodes[i].dist->h, h);
+    if (n_local) *n_local = s->s->local_n(i);
+    return 0;
+  });
+}
+
+int tmgx_solver_bounds(tmgx_solver s, int level, double* lo, double* hi) {
+  return guard([&] {
+    const int i = check_level(s, level);
+    *lo = s->s->nodes[i].lo;
+    *hi = s->s->nodes[i].hi;
+    return 0;
+  });
+}
+
+int tmgx_fill_rhs(tmgx_solver s, uint64_t seed, double* b_local) {
+  return guard([&] {
+    auto& S = *s->s;
+    const auto& D = *S.nodes[0].dist;
+    for (size_t q = 0; q < D.local.size(); ++q)
+      S.W.cnt.launches += tmgx::launch_fill_rhs(D.geo[q], S.cw.p[q], seed, true, S.W.stream);
+    S.download(0, S.cw, b_local, false);
+    return 0;
+  });
+}
+
+int tmgx_solve(tmgx_solver s, const double* b, double* x, int on_device, const tmgx_ksp_cfg* cfg, double* history,
+               tmgx_report* rep) {
+  return guard([&] {
+    if (cfg->method != TMGX_KSP_CG && cfg->method != TMGX_KSP_PREONLY)
+      throw tmg::ConfigError("ksp_type must be cg or preonly on this path");
+    auto& S = *s->s;
+    const long long l0 = S.W.cnt.launches;
+    double t_ms = 0;
+    int reason, its;
+    double n0, nf;
+    const int rc = S.solve(b, x, on_device != 0, cfg->method, cfg->rtol, cfg->atol, cfg->max_its, history, &reason,
+                           &its, &n0, &nf, &t_ms, false, 0);
+    rep->reason = reason;
+    rep->iterations = its;
+    rep->norm0 = n0;
+    rep->norm_final = nf;
+    rep->t_solve_s = t_ms * 1e-3;
+    rep->kernel_launches = S.W.cnt.launches - l0;
+    return rc;
+  });
+}
+
+int tmgx_solve_seeded(tmgx_solver s, uint64_t seed, double* x_dev, const tmgx_ksp_cfg* cfg, double* history,
+                      tmgx_report* rep) {
+  return guard([&] {
+    auto& S = *s->s;
+    const long long l0 = S.W.cnt.launches;
+    double t_ms = 0;
+    int reason, its;
+    double n0, nf;
+    const int rc = S.solve(nullptr, x_dev, true, cfg->method, cfg->rtol, cfg->atol, cfg->max_its, history, &reason,
+                           &its, &n0, &nf, &t_ms, true, seed);
+    rep->reason = reason;
+    rep->iterations = its;
+    rep->norm0 = n0;
+    rep->norm_final = nf;
+    rep->t_solve_s = t_ms * 1e-3;
+    rep->kernel_launches = S.W.cnt.launches - l0;
+    return rc;
+  });
+}
+
+int tmgx_pc_apply(tmgx_solver s, const double* x, double* y) {
+  return guard([&] {
+    auto& S = *s->s;
+    auto& nd = S.nodes[0];
+    S.upload(0, nd.b, x, false);
+    S.vcycle(0);
+    S.download(0, nd.x, y, false);
+    return 0;
+  });
+}
+
+int tmgx_level_apply(tmgx_solver s, int level, const double* x, double* y) {
+  return guard([&] {
+    const int i = check_level(s, level);
+    auto& S = *s->s;
+    auto& nd = S.nodes[i];
+    S.upload(i, nd.x, x, false);
+    S.apply(i, nd.x, nd.b);
+    S.download(i, nd.b, y, false);
+    return 0;
+  });
+}
+
+int tmgx_level_smooth(tmgx_solver s, int level, const double* b, double* x) {
+  return guard([&] {
+    const int i = check_level(s, level);
+    auto& S = *s->s;
+    auto& nd = S.nodes[i];
+    if (nd.kind != tmgx::SMOOTH) throw tmg::Error("level has no smoother");
+    S.upload(i, nd.b, b, false);
+    bool zero = true;
+    for (long long t = 0, n = S.local_n(i); t < n; ++t)
+      if (x[t] != 0.0) {
+        zero = false;
+        break;
+      }
+    S.upload(i, nd.x, x, false);
+    S.smooth(i, zero);
+    S.download(i, nd.x, x, false);
+    return 0;
+  });
+}
+
+int tmgx_level_residual_restrict(tmgx_solver s, int fine_level, const double* b, const double* x, double* bc) {
+  return guard([&] {
+    const int i = check_level(s, fine_level);
+    auto& S = *s->s;
+    auto& nd = S.nodes[i];
+    if (nd.kind != tmgx::SMOOTH) throw tmg::Error("level is not restricted from");
+    auto& cn = S.nodes[i + 1];
+    S.upload(i, nd.b, b, false);
+    S.upload(i, nd.x, x, false);
+    S.halo(i, nd.x);
+    const auto& D = *nd.dist;
+    for (size_t q = 0; q < D.local.size(); ++q)
+      S.W.cnt.launches += tmgx::launch_residual(D.geo[q], nd.op[q], nd.b.p[q], nd.x.p[q], nd.r.p[q], S.W.stream);
+    S.halo(i, nd.r);
+    for (size_t q = 0; q < D.local.size(); ++q)
+      S.W.cnt.launches += tmgx::launch_restrict(D.geo[q], cn.dist->geo[q], nd.r.p[q], cn.b.p[q], S.W.stream);
+    S.download(i + 1, cn.b, bc, false);
+    return 0;
+  });
+}
+
+int tmgx_level_prolong_add(tmgx_solver s, int fine_level, const double* xc, double* xf) {
+  return guard([&] {
+    const int i = check_level(s, fine_level);
+    auto& S = *s->s;
+    auto& nd = S.nodes[i];
+    if (nd.kind != tmgx::SMOOTH) throw tmg::Error("level is not prolongated to");
+    auto& cn = S.nodes[i + 1];
+    S.upload(i + 1, cn.x, xc, false);
+    S.upload(i, nd.x, xf, false);
+    S.halo(i + 1, cn.x);
+    const auto& D = *nd.dist;
+    for (size_t q = 0; q < D.local.size(); ++q)
+      S.W.cnt.launches += tmgx::launch_prolong_add(D.geo[q], cn.dist->geo[q], cn.x.p[q], nd.x.p[q], S.W.stream);
+    S.download(i, nd.x, xf, false);
+    return 0;
+  });
+}
+
+int tmgx_coarse_solve(tmgx_solver s, const double* b, double* x) {
+  return guard([&] {
+    auto& S = *s->s;
+    const int i = (int)S.nodes.size() - 1;
+    auto& nd = S.nodes[i];
+    S.upload(i, nd.b, b, false);
+    S.coarse_solve(i);
+    S.download(i, nd.x, x, false);
+    return 0;
+  });
+}
+
+int tmgx_telescope_gather(tmgx_solver s, int stage, const double* xp, double* xs) {
+  return guard([&] {
+    auto& S = *s->s;
+    if (stage < 0 || stage >= (int)S.stage_node.size()) throw tmg::Error("no such telescope stage");
+    const int i = S.stage_node[stage];
+    S.upload(i, S.nodes[i].b, xp, false);
+    tmgx::run_plan(S.W, S.nodes[i].gather, S.nodes[i].b, S.nodes[i + 1].b, true);
+    S.download(i + 1, S.nodes[i + 1].b, xs, false);
+    return 0;
+  });
+}
+
+int tmgx_telescope_scatter(tmgx_solver s, int stage, const double* ys, double* yp) {
+  return guard([&] {
+    auto& S = *s->s;
+    if (stage < 0 || stage >= (int)S.stage_node.size()) throw tmg::Error("no such telescope stage");
+    const int i = S.stage_node[stage];
+    S.upload(i + 1, S.nodes[i + 1].x, ys, false);
+    tmgx::run_plan(S.W, S.nodes[i].scatter, S.nodes[i + 1].x, S.nodes[i].x, true);
+    S.download(i, S.nodes[i].x, yp, false);
+    return 0;
+  });
+}
+
+int tmgx_get_counters(tmgx_solver s, tmgx_counters* c) {
+  const auto& k = s->s->W.cnt;
+  c->kernel_launches = k.launches;
+  c->halo_bytes_sent = k.halo_bytes;
+  c->telescope_bytes_sent = k.tele_bytes;
+  c->allreduces = k.allreduces;
+  return 0;
+}
+
+}  // extern "C"
+
+extern "C" int tmgx_bench_kernel(tmgx_solver s, int which, int level, int iters, double* ms_per_launch,
+                                 double* bytes_per_launch) {
+  return guard([&] {
+    auto& S = *s->s;
+    const int i = check_level(s, level);
+    auto& nd = S.nodes[i];
+    if (nd.kind != tmgx::SMOOTH) throw tmg::Error("bench_kernel needs a smoothed level");
+    const auto& D = *nd.dist;
+    const bool var = S.prob.kind == 1;
+    const double kb = var ? 8.0 : 0.0;  // coefficient stream
+    long long n = D.local_unknowns();
+    double per_pt = 0.0;
+    tmgx::ChebStep cs{0.5, 0.25};
+    auto launch = [&]() {
+      for (size_t q = 0; q < D.local.size(); ++q) {
+        const auto& g = D.geo[q];
+        switch (which) {
+          case 0: tmgx::launch_cheb_step(g, nd.op[q], nd.d.p[q], nd.r.p[q], nd.x.p[q], nd.d2.p[q], nd.r.p[q], nd.x.p[q], cs, false, S.W.stream); break;
+          case 1: tmgx::launch_cheb_step(g, nd.op[q], nd.d.p[q], nd.r.p[q], nd.x.p[q], nd.d2.p[q], nd.r.p[q], nd.x.p[q], cs, true, S.W.stream); break;
+          case 2: tmgx::launch_apply(g, nd.op[q], nd.x.p[q], nd.b.p[q], S.W.stream); break;
+          case 3: tmgx::launch_residual(g, nd.op[q], nd.b.p[q], nd.x.p[q], nd.r.p[q], S.W.stream); break;
+          case 4: tmgx::launch_restrict(g, S.nodes[i + 1].dist->geo[q], nd.r.p[q], S.nodes[i + 1].b.p[q], S.W.stream); break;
+          case 5: tmgx::launch_prolong_add(g, S.nodes[i + 1].dist->geo[q], S.nodes[i + 1].x.p[q], nd.x.p[q], S.W.stream); break;
+          case 6: tmgx::launch_cg_update(g, nd.d.p[q], nd.d2.p[q], nd.x.p[q], nd.r.p[q], S.scal, tmgx::S_TMP1, tmgx::S_FLAG_PW, S.W.stream); break;
+          case 7: tmgx::launch_spmv_dot(g, nd.op[q], nd.x.p[q], nd.b.p[q], S.part + S.part_off[q], S.W.stream); break;
+          default: throw tmg::Error("unknown kernel id");
+        }
+      }
+    };
+    switch (which) {
+      case 0: per_pt = 48 + kb; break;
+      case 1: per_pt = 32 + kb; break;
+      case 2: per_pt = 16 + kb; break;
+      case 3: per_pt = 24 + kb; break;
+      case 4: per_pt = 8 + 8.0 / 8.0; break;
+      case 5: per_pt = 16 + 8.0 / 8.0; break;
+      case 6: per_pt = 48; break;
+      case 7: per_pt = 16 + kb; break;
+      default: throw tmg::Error("unknown kernel id");
+    }
+    tmgx::cuda_check(cudaMemsetAsync(S.scal, 0, sizeof(double) * tmgx::S_NSLOTS, S.W.stream), "memset");
+    for (int w = 0; w < 3; ++w) launch();
+    cudaEvent_t e0, e1;
+    tmgx::cuda_check(cudaEventCreate(&e0), "event");
+    tmgx::cuda_check(cudaEventCreate(&e1), "event");
+    tmgx::cuda_check(cudaEventRecord(e0, S.W.stream), "record");
+    for (int it = 0; it < iters; ++it) launch();
+    tmgx::cuda_check(cudaEventRecord(e1, S.W.stream), "record");
+    tmgx::cuda_check(cudaEventSynchronize(e1), "sync");
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    tmgx::cuda_check(cudaGetLastError(), "bench kernel");
+    *ms_per_launch = ms / iters;
+    *bytes_per_launch = per_pt * (double)n;
+    return 0;
+  });
+}

@@ -1,0 +1,955 @@
+// Host orchestration of the MG-CG path; see tmgx_engine.hpp for the reference map.
+#include "tmgx_engine.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+namespace tmgx {
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw tmg::CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+void nccl_check(ncclResult_t e, const char* what) {
+  if (e != ncclSuccess) throw tmg::CudaError(std::string(what) + ": " + ncclGetErrorString(e));
+}
+#define CK(x) cuda_check((x), #x)
+
+// ------------------------------------------------------------------------------------------
+// World
+// ------------------------------------------------------------------------------------------
+
+World::World(int R_, int P_, int me_, int device_, const void* nccl_id) : R(R_), P(P_), me(me_), device(device_) {
+  if (R < 1 || P < 1 || me < 0 || me >= P || R < P)
+    throw tmg::ConfigError("world: need n_ranks >= nproc >= 1 and 0 <= proc < nproc");
+  first = (int)((long long)me * R / P);
+  end = (int)((long long)(me + 1) * R / P);
+  CK(cudaSetDevice(device));
+  CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  if (P > 1) {
+    if (!nccl_id) throw tmg::ConfigError("world: nproc > 1 needs an NCCL unique id");
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof(id));
+    nccl_check(ncclCommInitRank(&nccl, P, id, me), "ncclCommInitRank");
+  }
+}
+
+World::~World() {
+  if (nccl) ncclCommDestroy(nccl);
+  if (stream) cudaStreamDestroy(stream);
+}
+
+int World::owner(int wr) const {
+  for (int p = 0; p < P; ++p)
+    if (wr < (int)((long long)(p + 1) * R / P)) return p;
+  return P - 1;
+}
+
+// ------------------------------------------------------------------------------------------
+// Dist / Field / arena
+// ------------------------------------------------------------------------------------------
+
+int Dist::slot_of(int m) const {
+  for (size_t q = 0; q < local.size(); ++q)
+    if (local[q] == m) return (int)q;
+  return -1;
+}
+
+long long Dist::local_unknowns() const {
+  long long n = 0;
+  for (const auto& g : geo) n += (long long)g.ex * g.ey * g.ez;
+  return n;
+}
+
+static BoxGeo make_geo(const tmg::GridHeader& h, int m) {
+  const tmg::GridBox b = h.box(m);
+  BoxGeo g;
+  g.ex = (int)b.extent(0);
+  g.ey = (int)b.extent(1);
+  g.ez = (int)b.extent(2);
+  g.gx = (int)b.lo[0];
+  g.gy = (int)b.lo[1];
+  g.gz = (int)b.lo[2];
+  g.Nx = (int)h.npoints[0];
+  g.Ny = (int)h.npoints[1];
+  g.Nz = (int)h.npoints[2];
+  g.px = ((kXO + g.ex + 1) + 3) / 4 * 4;
+  g.pxy = g.px * (g.ey + 2);
+  g.base = kXO + g.px + g.pxy;
+  g.total = g.pxy * (g.ez + 2) + 8;
+  return g;
+}
+
+static long long geo_off(const BoxGeo& g, long long i, long long j, long long k) {
+  return g.base + (i - g.gx) + g.px * (j - g.gy) + g.pxy * (k - g.gz);
+}
+
+std::shared_ptr<Dist> make_dist(const World& W, const tmg::GridHeader& h, const std::vector<int>& wr) {
+  auto D = std::make_shared<Dist>();
+  D->h = h;
+  D->wr = wr;
+  if ((int)wr.size() != h.n_ranks()) throw tmg::Error("dist: rank map does not match the header");
+  for (int m = 0; m < h.n_ranks(); ++m)
+    if (W.local(wr[m])) {
+      D->local.push_back(m);
+      D->geo.push_back(make_geo(h, m));
+    }
+  if ((int)D->local.size() > kMaxLocal) throw tmg::ConfigError("too many boxes per process");
+  return D;
+}
+
+PtrTable Field::table() const {
+  PtrTable t{};
+  for (size_t q = 0; q < p.size() && q < (size_t)kMaxLocal; ++q) t.p[q] = p[q];
+  return t;
+}
+
+DeviceArena::~DeviceArena() {
+  for (void* p : ptrs_) cudaFree(p);
+}
+
+double* DeviceArena::alloc(long long n) {
+  void* p = nullptr;
+  if (n < 1) n = 1;
+  CK(cudaMalloc(&p, (size_t)n * sizeof(double)));
+  CK(cudaMemset(p, 0, (size_t)n * sizeof(double)));
+  ptrs_.push_back(p);
+  return static_cast<double*>(p);
+}
+
+Field make_field(DeviceArena& A, const Dist& D) {
+  Field f;
+  for (const auto& g : D.geo) f.p.push_back(A.alloc(g.total));
+  return f;
+}
+
+// ------------------------------------------------------------------------------------------
+// Region plans
+// ------------------------------------------------------------------------------------------
+
+namespace {
+
+template <class RegionFn>
+RegionPlan build_plan(World& W, DeviceArena& A, const Dist& S, const Dist& T, RegionFn region) {
+  RegionPlan plan;
+  std::vector<CopyDesc> loc, pack, unpack;
+  struct Seg {
+    long long count = 0;
+  };
+  std::vector<long long> scount(W.P, 0), rcount(W.P, 0);
+  // pass 1: count per peer
+  for (int m = 0; m < T.h.n_ranks(); ++m)
+    for (int s = 0; s < S.h.n_ranks(); ++s) {
+      tmg::GridBox reg;
+      if (!region(s, m, reg)) continue;
+      const int os = W.owner(S.wr[s]), ot = W.owner(T.wr[m]);
+      if (os == ot) continue;
+      if (os == W.me) scount[ot] += reg.n_vertices();
+      if (ot == W.me) rcount[os] += reg.n_vertices();
+    }
+  std::vector<long long> soff(W.P, 0), roff(W.P, 0);
+  long long st = 0, rt = 0;
+  for (int p = 0; p < W.P; ++p) {
+    soff[p] = st;
+    roff[p] = rt;
+    if (scount[p]) plan.sends.push_back({p, st, scount[p]});
+    if (rcount[p]) plan.recvs.push_back({p, rt, rcount[p]});
+    st += scount[p];
+    rt += rcount[p];
+  }
+  // pass 2: descriptors in (m asc, s asc) order, identical on both sides of every pair
+  for (int m = 0; m < T.h.n_ranks(); ++m)
+    for (int s = 0; s < S.h.n_ranks(); ++s) {
+      tmg::GridBox reg;
+      if (!region(s, m, reg)) continue;
+      const int os = W.owner(S.wr[s]), ot = W.owner(T.wr[m]);
+      CopyDesc d{};
+      d.nx = (int)reg.extent(0);
+      d.ny = (int)reg.extent(1);
+      d.nz = (int)reg.extent(2);
+      const long long n = reg.n_vertices();
+      if (os == W.me) {
+        const int ss = S.slot_of(s);
+        const BoxGeo& gs = S.geo[ss];
+        d.src_slot = ss;
+        d.src_off = geo_off(gs, reg.lo[0], reg.lo[1], reg.lo[2]);
+        d.src_px = gs.px;
+        d.src_pxy = gs.pxy;
+      }
+      if (ot == W.me) {
+        const int ts = T.slot_of(m);
+        const BoxGeo& gt = T.geo[ts];
+        d.dst_slot = ts;
+        d.dst_off = geo_off(gt, reg.lo[0], reg.lo[1], reg.lo[2]);
+        d.dst_px = gt.px;
+        d.dst_pxy = gt.pxy;
+      }
+      if (os == W.me && ot == W.me) {
+        loc.push_back(d);
+        plan.max_local = std::max<long long>(plan.max_local, n);
+      } else if (os == W.me) {
+        d.dst_slot = -1;
+        d.dst_off = soff[ot];
+        d.dst_px = d.nx;
+        d.dst_pxy = (long long)d.nx * d.ny;
+        soff[ot] += n;
+        pack.push_back(d);
+        plan.max_pack = std::max<long long>(plan.max_pack, n);
+      } else if (ot == W.me) {
+        d.src_slot = -1;
+        d.src_off = roff[os];
+        d.src_px = d.nx;
+        d.src_pxy = (long long)d.nx * d.ny;
+        roff[os] += n;
+        unpack.push_back(d);
+        plan.max_unpack = std::max<long long>(plan.max_unpack, n);
+      }
+    }
+  auto upload = [&](const std::vector<CopyDesc>& v, CopyDesc*& dst, int& n) {
+    n = (int)v.size();
+    if (!n) return;
+    dst = A.alloc_t<CopyDesc>(n);
+    CK(cudaMemcpy(dst, v.data(), sizeof(CopyDesc) * v.size(), cudaMemcpyHostToDevice));
+  };
+  upload(loc, plan.d_local, plan.n_local);
+  upload(pack, plan.d_pack, plan.n_pack);
+  upload(unpack, plan.d_unpack, plan.n_unpack);
+  if (st) plan.sendbuf = A.alloc(st);
+  if (rt) plan.recvbuf = A.alloc(rt);
+  return plan;
+}
+
+}  // namespace
+
+// ghost_exchange (grid.cpp:645-696): every rank's halo box (width 1, clipped to the grid,
+// edges and corners included) is filled from the owning boxes.
+RegionPlan build_halo_plan(World& W, DeviceArena& A, const Dist& D) {
+  return build_plan(W, A, D, D, [&](int s, int m, tmg::GridBox& reg) {
+    if (s == m) return false;
+    tmg::GridBox hb = D.h.box(m);
+    for (int a = 0; a < 3; ++a) {
+      hb.lo[a] = std::max<long long>(0, hb.lo[a] - 1);
+      hb.hi[a] = std::min<long long>(D.h.npoints[a], hb.hi[a] + 1);
+    }
+    reg = tmg::intersect(hb, D.h.box(s));
+    return !reg.empty();
+  });
+}
+
+// P-hat^T composed with ScatterPlan::to_sub (grid.cpp:582-599, scatter_plan.cpp:40-77):
+// every vertex moves from its parent owner box to the member box that owns it in the
+// repartitioned header, i.e. box intersections of the two decompositions.
+RegionPlan build_transfer_plan(World& W, DeviceArena& A, const Dist& S, const Dist& T) {
+  return build_plan(W, A, S, T, [&](int s, int m, tmg::GridBox& reg) {
+    reg = tmg::intersect(S.h.box(s), T.h.box(m));
+    return !reg.empty();
+  });
+}
+
+void run_plan(World& W, const RegionPlan& plan, const Field& src, const Field& dst, bool telescope) {
+  const PtrTable ts = src.table(), td = dst.table();
+  if (plan.n_pack) W.cnt.launches += launch_region_copy(plan.d_pack, plan.n_pack, plan.max_pack, ts, td, nullptr,
+                                                        plan.sendbuf, W.stream);
+  if (!plan.sends.empty() || !plan.recvs.empty()) {
+    nccl_check(ncclGroupStart(), "ncclGroupStart");
+    for (const auto& p : plan.sends) {
+      nccl_check(ncclSend(plan.sendbuf + p.off, (size_t)p.count, ncclDouble, p.proc, W.nccl, W.stream), "ncclSend");
+      (telescope ? W.cnt.tele_bytes : W.cnt.halo_bytes) += p.count * 8;
+    }
+    for (const auto& p : plan.recvs)
+      nccl_check(ncclRecv(plan.recvbuf + p.off, (size_t)p.count, ncclDouble, p.proc, W.nccl, W.stream), "ncclRecv");
+    nccl_check(ncclGroupEnd(), "ncclGroupEnd");
+  }
+  if (plan.n_local)
+    W.cnt.launches += launch_region_copy(plan.d_local, plan.n_local, plan.max_local, ts, td, nullptr, nullptr, W.stream);
+  if (plan.n_unpack)
+    W.cnt.launches += launch_region_copy(plan.d_unpack, plan.n_unpack, plan.max_unpack, ts, td, plan.recvbuf, nullptr,
+                                         W.stream);
+}
+
+// ------------------------------------------------------------------------------------------
+// Solver setup
+// ------------------------------------------------------------------------------------------
+
+static unsigned long long splitmix64_h(unsigned long long x) {
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+static double hashed_uniform_h(unsigned long long seed, unsigned long long idx) {
+  return (double)(splitmix64_h(seed ^ splitmix64_h(idx)) >> 11) * 0x1.0p-53;
+}
+static double harm_h(double a, double b) { return 2.0 * a * b / (a + b); }
+
+double Solver::host_k(const Dist& D, long long gi, long long gj, long long gk) const {
+  if (prob.kind != 1) return 1.0;
+  volatile double x = (double)gi * (1.0 / (double)(D.h.npoints[0] - 1));
+  volatile double y = (double)gj * (1.0 / (double)(D.h.npoints[1] - 1));
+  volatile double z = (double)gk * (1.0 / (double)(D.h.npoints[2] - 1));
+  for (const Sphere& s : spheres) {
+    volatile double dx = x - s.cx, dy = y - s.cy, dz = z - s.cz;
+    volatile double a = dx * dx, b = dy * dy, c = dz * dz;
+    volatile double ab = a + b;
+    volatile double d2 = ab + c;
+    volatile double rr = s.r * s.r;
+    if (d2 <= rr) return prob.k_in;
+  }
+  return 1.0;
+}
+
+static OpParams make_op(const tmg::GridHeader& h) {
+  OpParams op{};
+  double ih2[3];
+  for (int a = 0; a < 3; ++a) {
+    const double hh = 1.0 / (double)(h.npoints[a] - 1);
+    ih2[a] = 1.0 / (hh * hh);
+  }
+  op.ih2x = ih2[0];
+  op.ih2y = ih2[1];
+  op.ih2z = ih2[2];
+  volatile double d = 0.0;  // oracle order: -z,-y,-x,+x,+y,+z
+  d = d + ih2[2];
+  d = d + ih2[1];
+  d = d + ih2[0];
+  d = d + ih2[0];
+  d = d + ih2[1];
+  d = d + ih2[2];
+  op.cdiag = d;
+  op.cinvd = 1.0 / op.cdiag;
+  op.k = nullptr;
+  return op;
+}
+
+Solver::Solver(World& W_, const ProblemDesc& P, const MGDesc& M) : W(W_), prob(P), mgd(M) {
+  CK(cudaSetDevice(W.device));
+  if (mgd.nlevels < 1) throw tmg::ConfigError("mg: number of levels must be >= 1");
+  if (mgd.m < 1) throw tmg::ConfigError("mg: smoother iterations must be >= 1");
+  if (prob.kind == 1) {
+    // sphere s: centre u(seed,4s+0..2), radius 0.05 + 0.10 u(seed,4s+3)
+    for (int s = 0; s < prob.n_spheres; ++s) {
+      Sphere sp;
+      sp.cx = hashed_uniform_h(prob.seed_k, 4ull * s + 0);
+      sp.cy = hashed_uniform_h(prob.seed_k, 4ull * s + 1);
+      sp.cz = hashed_uniform_h(prob.seed_k, 4ull * s + 2);
+      sp.r = 0.05 + 0.10 * hashed_uniform_h(prob.seed_k, 4ull * s + 3);
+      spheres.push_back(sp);
+    }
+    spheres_dev = arena.alloc_t<Sphere>((long long)spheres.size());
+    CK(cudaMemcpy(spheres_dev, spheres.data(), sizeof(Sphere) * spheres.size(), cudaMemcpyHostToDevice));
+  }
+  build_nodes();
+}
+
+int Solver::node_for_level(int level) const {
+  int best = -1;
+  for (size_t i = 0; i < nodes.size(); ++i)
+    if (nodes[i].level == level) best = (int)i;
+  if (best < 0) throw tmg::Error("no such level");
+  return best;
+}
+
+void Solver::build_nodes() {
+  const int top = mgd.nlevels - 1;
+  std::optional<std::array<int, 3>> hint;
+  if (prob.pg_hint[0] || prob.pg_hint[1] || prob.pg_hint[2]) hint = prob.pg_hint;
+  tmg::GridHeader H = tmg::build_header_for(W.R, 3, {prob.np[0], prob.np[1], prob.np[2]}, 1, 1, hint);
+  std::vector<int> wr(W.R);
+  for (int r = 0; r < W.R; ++r) wr[r] = r;
+
+  auto tele = mgd.tele;
+  std::sort(tele.begin(), tele.end(), [](const TeleStage& a, const TeleStage& b) { return a.level > b.level; });
+  for (size_t t = 0; t < tele.size(); ++t) {
+    if (tele[t].level < 0 || tele[t].level > top) throw tmg::ConfigError("telescope: level out of range");
+    if (t && tele[t].level == tele[t - 1].level) throw tmg::ConfigError("telescope: two stages on one level");
+    if (tele[t].r < 1) throw tmg::ConfigError("telescope: reduction factor must be >= 1");
+  }
+  const int T = (int)tele.size();
+  int seg_top = top;
+  for (int s = 0; s <= T; ++s) {
+    const int bottom = s < T ? tele[s].level : 0;
+    for (int l = seg_top; l >= bottom; --l) {
+      Node nd;
+      nd.level = l;
+      nd.stage = (s < T && l == bottom) ? s : -1;
+      nd.kind = (s < T && l == bottom) ? TELESCOPE : (l == 0 ? COARSE : SMOOTH);
+      nd.dist = make_dist(W, H, wr);
+      nodes.push_back(std::move(nd));
+      if (l > bottom) {
+        auto c = tmg::try_coarsen_header(H);
+        if (!c)
+          throw tmg::ConfigError("cannot coarsen: level " + std::to_string(l) + " grid " +
+                                 std::to_string(H.npoints[0]) + "x" + std::to_string(H.npoints[1]) + "x" +
+                                 std::to_string(H.npoints[2]) + " on a " + std::to_string(H.proc_grid[0]) + "x" +
+                                 std::to_string(H.proc_grid[1]) + "x" + std::to_string(H.proc_grid[2]) +
+                                 " processor grid (axes need 2M+1 vertices and every rank one vertex)");
+        H = *c;
+      }
+    }
+    if (s < T) {
+      const tmg::SplitResult sp = tmg::split_strided(H.n_ranks(), tele[s].r);
+      std::array<std::optional<int>, 3> ov;
+      for (int a = 0; a < 3; ++a)
+        if (tele[s].ov[a]) ov[a] = tele[s].ov[a];
+      H = tmg::repartition_header(H, sp.n_members(), ov);
+      std::vector<int> nwr;
+      for (int mm : sp.member_map) nwr.push_back(wr[mm]);
+      wr = nwr;
+      seg_top = bottom;
+      stage_node.push_back((int)nodes.size() - 1);
+    }
+  }
+  if (nodes.back().dist->h.n_ranks() != 1)
+    throw tmg::ConfigError("pc_type lu needs a single-rank communicator; repartition first, e.g. pc_type telescope "
+                           "with <prefix>telescope_pc_type lu");
+
+  // buffers, operators, plans
+  int nloc_max = 1;
+  for (auto& nd : nodes) {
+    const Dist& D = *nd.dist;
+    nloc_max = std::max<int>(nloc_max, (int)D.local.size());
+    if (prob.kind == 1) {
+      nd.kcoef = make_field(arena, D);
+      for (size_t q = 0; q < D.local.size(); ++q)
+        W.cnt.launches += launch_fill_coeff(D.geo[q], nd.kcoef.p[q], spheres_dev, (int)spheres.size(), prob.k_in,
+                                            true, W.stream);
+    }
+    for (size_t q = 0; q < D.local.size(); ++q) {
+      OpParams op = make_op(D.h);
+      if (prob.kind == 1) op.k = nd.kcoef.p[q];
+      nd.op.push_back(op);
+      nblk_max = std::max(nblk_max, grid_blocks(D.geo[q]));
+      staging_n = std::max<long long>(staging_n, D.local_unknowns());
+    }
+    nd.b = make_field(arena, D);
+    nd.x = make_field(arena, D);
+    if (nd.kind == SMOOTH) {
+      nd.r = make_field(arena, D);
+      nd.d = make_field(arena, D);
+      nd.d2 = make_field(arena, D);
+    }
+    nd.halo = build_halo_plan(W, arena, D);
+  }
+  for (size_t i = 0; i < nodes.size(); ++i)
+    if (nodes[i].kind == TELESCOPE) {
+      nodes[i].gather = build_transfer_plan(W, arena, *nodes[i].dist, *nodes[i + 1].dist);
+      nodes[i].scatter = build_transfer_plan(W, arena, *nodes[i + 1].dist, *nodes[i].dist);
+    }
+  part = arena.alloc((long long)nloc_max * 2 * nblk_max);
+  for (int q = 0; q < nloc_max; ++q) part_off.push_back((long long)q * 2 * nblk_max);
+  rank_sums = arena.alloc(2LL * W.R);
+  scal = arena.alloc(S_NSLOTS);
+  CK(cudaMallocHost(&host_scal, sizeof(double) * (S_NSLOTS + 2 * W.R + 8)));
+  staging = arena.alloc(staging_n);
+  {
+    const Dist& D0 = *nodes[0].dist;
+    ranks_dev = arena.alloc_t<int>(D0.h.n_ranks());
+    CK(cudaMemcpy(ranks_dev, D0.wr.data(), sizeof(int) * D0.wr.size(), cudaMemcpyHostToDevice));
+    cx = make_field(arena, D0);
+    cr = make_field(arena, D0);
+    cz = make_field(arena, D0);
+    cp = make_field(arena, D0);
+    cw = make_field(arena, D0);
+  }
+  setup_coarse(nodes.back());
+  CK(cudaStreamSynchronize(W.stream));
+
+  // Chebyshev intervals: given, or estimated (SolverNode::create, solver.cpp:591-592)
+  for (size_t i = 0; i < nodes.size(); ++i) {
+    Node& nd = nodes[i];
+    if (nd.kind != SMOOTH) continue;
+    if (!mgd.bounds.empty()) {
+      nd.lo = mgd.bounds[2 * nd.level];
+      nd.hi = mgd.bounds[2 * nd.level + 1];
+    } else {
+      estimate((int)i, mgd.est_mode);
+    }
+  }
+  CK(cudaStreamSynchronize(W.stream));
+}
+
+// LUPC (precond.cpp:220-229): dense LU of the coarse operator, factored on the host with
+// DenseLU::factor's partial pivoting (precond.cpp:11-48).
+void Solver::setup_coarse(Node& nd) {
+  const Dist& D = *nd.dist;
+  if (D.local.empty()) return;
+  const BoxGeo& g = D.geo[0];
+  const int nx = g.ex, ny = g.ey, nz = g.ez;
+  const int n = nx * ny * nz;
+  nd.nc = n;
+  const OpParams op = make_op(D.h);
+  std::vector<double> kk((size_t)n);
+  for (int k = 0; k < nz; ++k)
+    for (int j = 0; j < ny; ++j)
+      for (int i = 0; i < nx; ++i) kk[(size_t)(i + nx * (j + ny * k))] = host_k(D, i, j, k);
+  std::vector<double> a((size_t)n * n, 0.0);
+  auto K = [&](int i, int j, int k) { return kk[(size_t)(i + nx * (j + ny * k))]; };
+  for (int k = 0; k < nz; ++k)
+    for (int j = 0; j < ny; ++j)
+      for (int i = 0; i < nx; ++i) {
+        const int v = i + nx * (j + ny * k);
+        const bool bnd = i == 0 || j == 0 || k == 0 || i == nx - 1 || j == ny - 1 || k == nz - 1;
+        const double kc = K(i, j, k);
+        const double fzm = (k > 0 ? harm_h(kc, K(i, j, k - 1)) : kc) * op.ih2z;
+        const double fym = (j > 0 ? harm_h(kc, K(i, j - 1, k)) : kc) * op.ih2y;
+        const double fxm = (i > 0 ? harm_h(kc, K(i - 1, j, k)) : kc) * op.ih2x;
+        const double fxp = (i + 1 < nx ? harm_h(kc, K(i + 1, j, k)) : kc) * op.ih2x;
+        const double fyp = (j + 1 < ny ? harm_h(kc, K(i, j + 1, k)) : kc) * op.ih2y;
+        const double fzp = (k + 1 < nz ? harm_h(kc, K(i, j, k + 1)) : kc) * op.ih2z;
+        volatile double d = 0.0;
+        d = d + fzm;
+        d = d + fym;
+        d = d + fxm;
+        d = d + fxp;
+        d = d + fyp;
+        d = d + fzp;
+        double* row = &a[(size_t)v * n];
+        row[v] = d;
+        if (bnd) continue;
+        if (k - 1 > 0) row[v - nx * ny] = -fzm;
+        if (j - 1 > 0) row[v - nx] = -fym;
+        if (i - 1 > 0) row[v - 1] = -fxm;
+        if (i + 1 < nx - 1) row[v + 1] = -fxp;
+        if (j + 1 < ny - 1) row[v + nx] = -fyp;
+        if (k + 1 < nz - 1) row[v + nx * ny] = -fzp;
+      }
+  std::vector<long long> piv((size_t)n);
+  for (int kk2 = 0; kk2 < n; ++kk2) {  // precond.cpp:26-46
+    int p = kk2;
+    double best = std::fabs(a[(size_t)kk2 * n + kk2]);
+    for (int i = kk2 + 1; i < n; ++i)
+      if (std::fabs(a[(size_t)i * n + kk2]) > best) {
+        best = std::fabs(a[(size_t)i * n + kk2]);
+        p = i;
+      }
+    if (best == 0.0) throw tmg::Error("lu factorization: matrix is singular at column " + std::to_string(kk2));
+    piv[(size_t)kk2] = p;
+    if (p != kk2)
+      for (int j = 0; j < n; ++j) std::swap(a[(size_t)kk2 * n + j], a[(size_t)p * n + j]);
+    const double pivot = a[(size_t)kk2 * n + kk2];
+    for (int i = kk2 + 1; i < n; ++i) {
+      const double m = a[(size_t)i * n + kk2] / pivot;
+      a[(size_t)i * n + kk2] = m;
+      if (m == 0.0) continue;
+      for (int j = kk2 + 1; j < n; ++j) {
+        volatile double t = m * a[(size_t)kk2 * n + j];
+        a[(size_t)i * n + j] = a[(size_t)i * n + j] - t;
+      }
+    }
+  }
+  std::vector<long long> map((size_t)n);
+  for (int k = 0; k < nz; ++k)
+    for (int j = 0; j < ny; ++j)
+      for (int i = 0; i < nx; ++i) map[(size_t)(i + nx * (j + ny * k))] = g.base + i + g.px * j + g.pxy * k;
+  nd.map_dev = arena.alloc_t<long long>(n);
+  CK(cudaMemcpy(nd.map_dev, map.data(), sizeof(long long) * n, cudaMemcpyHostToDevice));
+  nd.A_dev = arena.alloc((long long)n * n);
+  if (parity_build()) {
+    nd.piv_dev = arena.alloc_t<long long>(n);
+    CK(cudaMemcpy(nd.piv_dev, piv.data(), sizeof(long long) * n, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(nd.A_dev, a.data(), sizeof(double) * (size_t)n * n, cudaMemcpyHostToDevice));
+  } else {
+    // Performance build: explicit inverse from the same factors (columns = DenseLU::solve(e_c)),
+    // applied as one warp-per-row matvec instead of a 2n-step dependent substitution chain.
+    std::vector<double> inv((size_t)n * n), y((size_t)n), x((size_t)n);
+    for (int c = 0; c < n; ++c) {
+      std::fill(y.begin(), y.end(), 0.0);
+      y[(size_t)c] = 1.0;
+      for (int k = 0; k < n; ++k) {
+        const long long p = piv[(size_t)k];
+        if (p != k) std::swap(y[(size_t)k], y[(size_t)p]);
+        for (int j = 0; j < k; ++j) y[(size_t)k] -= a[(size_t)k * n + j] * y[(size_t)j];
+      }
+      for (int k = n - 1; k >= 0; --k) {
+        double acc = y[(size_t)k];
+        for (int j = k + 1; j < n; ++j) acc -= a[(size_t)k * n + j] * x[(size_t)j];
+        x[(size_t)k] = acc / a[(size_t)k * n + k];
+      }
+      for (int r = 0; r < n; ++r) inv[(size_t)r * n + c] = x[(size_t)r];
+    }
+    CK(cudaMemcpy(nd.A_dev, inv.data(), sizeof(double) * (size_t)n * n, cudaMemcpyHostToDevice));
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// primitives
+// ------------------------------------------------------------------------------------------
+
+void Solver::halo(int i, const Field& f) { run_plan(W, nodes[i].halo, f, f, false); }
+
+void Solver::apply(int i, const Field& x, const Field& y) {
+  Node& nd = nodes[i];
+  halo(i, x);
+  for (size_t q = 0; q < nd.dist->local.size(); ++q)
+    W.cnt.launches += launch_apply(nd.dist->geo[q], nd.op[q], x.p[q], y.p[q], W.stream);
+}
+
+void Solver::coarse_solve(int i) {
+  Node& nd = nodes[i];
+  if (nd.dist->local.empty()) return;
+  if (parity_build())
+    W.cnt.launches += launch_lu_solve(nd.A_dev, nd.piv_dev, nd.nc, nd.map_dev, nd.b.p[0], nd.x.p[0], W.stream);
+  else
+    W.cnt.launches += launch_dense_matvec(nd.A_dev, nd.nc, nd.map_dev, nd.b.p[0], nd.x.p[0], W.stream);
+}
+
+// solve_fixed, Chebyshev branch (solver.cpp:79-110) fused into stencil passes:
+//   pre (x = 0): d0 = D^-1 b / theta ; then m-1 passes  x += d ; r -= A d ; d = c1 d + c2 D^-1 r
+//   post:        r = b - A x ; d0 = D^-1 r / theta ; then the same m-1 passes
+// The last pass folds the final x += d and writes x only.
+void Solver::smooth(int i, bool zero_x) {
+  Node& nd = nodes[i];
+  const Dist& D = *nd.dist;
+  const int m = mgd.m;
+  const double theta = 0.5 * (nd.hi + nd.lo);
+  const double delta = 0.5 * (nd.hi - nd.lo);
+  const double sigma = theta / delta;
+  double rho = 1.0 / sigma;
+  const double s_theta = 1.0 / theta;
+  const size_t nb = D.local.size();
+  if (zero_x) {
+    for (size_t q = 0; q < nb; ++q)
+      W.cnt.launches += launch_cheb_start_zero(D.geo[q], nd.op[q], nd.b.p[q], m == 1 ? nd.x.p[q] : nd.d.p[q], s_theta,
+                                               W.stream);
+    if (m == 1) return;
+  } else {
+    halo(i, nd.x);
+    for (size_t q = 0; q < nb; ++q)
+      W.cnt.launches += launch_cheb_start_res(D.geo[q], nd.op[q], nd.b.p[q], nd.x.p[q], nd.r.p[q], nd.d.p[q], s_theta,
+                                              W.stream);
+    if (m == 1) {
+      for (size_t q = 0; q < nb; ++q) W.cnt.launches += launch_axpy(D.geo[q], 1.0, nd.d.p[q], nd.x.p[q], W.stream);
+      return;
+    }
+  }
+  for (int it = 0; it < m - 1; ++it) {
+    const double rho_new = 1.0 / (2.0 * sigma - rho);
+    ChebStep cs{rho_new * rho, 2.0 * rho_new / delta};
+    rho = rho_new;
+    halo(i, nd.d);
+    const bool first_zero = zero_x && it == 0;
+    for (size_t q = 0; q < nb; ++q)
+      W.cnt.launches += launch_cheb_step(D.geo[q], nd.op[q], nd.d.p[q], first_zero ? nd.b.p[q] : nd.r.p[q],
+                                         first_zero ? nullptr : nd.x.p[q], nd.d2.p[q], nd.r.p[q], nd.x.p[q], cs,
+                                         it == m - 2, W.stream);
+    std::swap(nd.d, nd.d2);
+  }
+}
+
+// mg_apply (Alg. 1) over the node list; TELESCOPE nodes realise
+// TelescopePC::apply: gather, inner V-cycle on the members, scatter back.
+void Solver::vcycle(int i) {
+  Node& nd = nodes[i];
+  if (nd.kind == COARSE) {
+    coarse_solve(i);
+    return;
+  }
+  if (nd.kind == TELESCOPE) {
+    run_plan(W, nd.gather, nd.b, nodes[i + 1].b, true);
+    vcycle(i + 1);
+    run_plan(W, nd.scatter, nodes[i + 1].x, nd.x, true);
+    return;
+  }
+  const Dist& D = *nd.dist;
+  Node& cn = nodes[i + 1];
+  smooth(i, true);
+  halo(i, nd.x);
+  for (size_t q = 0; q < D.local.size(); ++q)
+    W.cnt.launches += launch_residual(D.geo[q], nd.op[q], nd.b.p[q], nd.x.p[q], nd.r.p[q], W.stream);
+  halo(i, nd.r);
+  for (size_t q = 0; q < D.local.size(); ++q)
+    W.cnt.launches += launch_restrict(D.geo[q], cn.dist->geo[q], nd.r.p[q], cn.b.p[q], W.stream);
+  vcycle(i + 1);
+  halo(i + 1, cn.x);
+  for (size_t q = 0; q < D.local.size(); ++q)
+    W.cnt.launches += launch_prolong_add(D.geo[q], cn.dist->geo[q], cn.x.p[q], nd.x.p[q], W.stream);
+  smooth(i, false);
+}
+
+void Solver::device_allreduce_ranksums(int nslots) {
+  if (W.P > 1) {
+    nccl_check(ncclAllReduce(rank_sums, rank_sums, (size_t)nslots * W.R, ncclDouble, ncclSum, W.nccl, W.stream),
+               "ncclAllReduce");
+    W.cnt.allreduces++;
+  }
+}
+
+// Deterministic collective sums for node i's distribution: per-box block partials are reduced
+// in a fixed tree, then summed over the communicator's ranks in rank order (the reference's
+// ordered_fold_sum, comm.cpp:338-351, at box granularity). Identical on every process.
+std::array<double, 2> Solver::collect2(int i, int nslots) {
+  const Dist& D = *nodes[i].dist;
+  CK(cudaMemsetAsync(rank_sums, 0, sizeof(double) * 2 * W.R, W.stream));
+  for (size_t q = 0; q < D.local.size(); ++q)
+    W.cnt.launches += launch_reduce_partials(part + part_off[q], grid_blocks(D.geo[q]), nslots, nblk_max,
+                                             rank_sums + D.wr[D.local[q]], W.R, W.stream);
+  device_allreduce_ranksums(nslots);
+  CK(cudaMemcpyAsync(host_scal, rank_sums, sizeof(double) * 2 * W.R, cudaMemcpyDeviceToHost, W.stream));
+  CK(cudaStreamSynchronize(W.stream));
+  std::array<double, 2> s{0.0, 0.0};
+  for (int m = 0; m < D.h.n_ranks(); ++m) {
+    s[0] += host_scal[D.wr[m]];
+    s[1] += host_scal[W.R + D.wr[m]];
+  }
+  return s;
+}
+
+static double tridiag_eig_max(const std::vector<double>& d, const std::vector<double>& e) {
+  // solver.cpp:488-516 (Sturm bisection)
+  const size_t n = d.size();
+  double lo = d[0], hi = d[0];
+  for (size_t i = 0; i < n; ++i) {
+    const double left = i > 0 ? std::abs(e[i - 1]) : 0.0;
+    const double right = i + 1 < n ? std::abs(e[i]) : 0.0;
+    lo = std::min(lo, d[i] - left - right);
+    hi = std::max(hi, d[i] + left + right);
+  }
+  auto count_below = [&](double x) {
+    int count = 0;
+    double q = 1.0;
+    for (size_t i = 0; i < n; ++i) {
+      const double off = i > 0 ? e[i - 1] : 0.0;
+      q = d[i] - x - (q == 0.0 ? std::abs(off) / 1e-300 : off * off / q);
+      if (q < 0.0) ++count;
+    }
+    return count;
+  };
+  for (int it = 0; it < 200 && hi - lo > 1e-12 * std::max(1.0, std::abs(hi)); ++it) {
+    const double mid = 0.5 * (lo + hi);
+    if (count_below(mid) >= (int)n)
+      hi = mid;
+    else
+      lo = mid;
+  }
+  return 0.5 * (lo + hi);
+}
+
+// chebyshev_bounds_estimate (solver.cpp:520-581): ten Jacobi-preconditioned CG steps from
+// fill_random(0x5eedbeef) keyed by natural index (SURVEY finding 4(b)). mode 0 reproduces the
+// shipped loop (p never updated, solver.cpp:537-561); mode 1 adds p = z + beta p.
+void Solver::estimate(int i, int mode) {
+  Node& nd = nodes[i];
+  const Dist& D = *nd.dist;
+  const size_t nb = D.local.size();
+  Field &r = nd.r, &z = nd.d, &p = nd.d2, &w = nd.x;
+  for (size_t q = 0; q < nb; ++q) W.cnt.launches += launch_fill_rhs(D.geo[q], r.p[q], 0x5eedbeefULL, false, W.stream);
+  for (size_t q = 0; q < nb; ++q)
+    W.cnt.launches += launch_jacobi_dot(D.geo[q], nd.op[q], r.p[q], z.p[q], part + part_off[q], W.stream);
+  double rz = collect2(i, 1)[0];
+  for (size_t q = 0; q < nb; ++q) W.cnt.launches += launch_copy_interior(D.geo[q], z.p[q], p.p[q], W.stream);
+  std::vector<double> alphas, betas;
+  bool broke = false;
+  for (int it = 0; it < 10; ++it) {
+    if (rz == 0.0 || !std::isfinite(rz)) break;
+    halo(i, p);
+    for (size_t q = 0; q < nb; ++q)
+      W.cnt.launches += launch_spmv_dot(D.geo[q], nd.op[q], p.p[q], w.p[q], part + part_off[q], W.stream);
+    const double pw = collect2(i, 1)[0];
+    if (pw <= 0.0 || !std::isfinite(pw)) {
+      if (alphas.empty()) broke = true;
+      break;
+    }
+    const double alpha = rz / pw;
+    for (size_t q = 0; q < nb; ++q) W.cnt.launches += launch_axpy(D.geo[q], -alpha, w.p[q], r.p[q], W.stream);
+    for (size_t q = 0; q < nb; ++q)
+      W.cnt.launches += launch_jacobi_dot(D.geo[q], nd.op[q], r.p[q], z.p[q], part + part_off[q], W.stream);
+    const double rz_new = collect2(i, 1)[0];
+    alphas.push_back(alpha);
+    if (rz_new <= 0.0 || !std::isfinite(rz_new)) break;
+    const double beta = rz_new / rz;
+    betas.push_back(beta);
+    rz = rz_new;
+    if (mode == 1) {
+      double* hb = host_scal + S_NSLOTS + 2 * W.R;
+      *hb = beta;
+      CK(cudaMemcpyAsync(scal + S_TMP0, hb, sizeof(double), cudaMemcpyHostToDevice, W.stream));
+      for (size_t q = 0; q < nb; ++q) W.cnt.launches += launch_p_update(D.geo[q], z.p[q], p.p[q], scal, S_TMP0, W.stream);
+      CK(cudaStreamSynchronize(W.stream));
+    }
+  }
+  if (broke || alphas.empty()) {
+    nd.lo = 0.1;
+    nd.hi = 1.1;
+    return;
+  }
+  const size_t k = alphas.size();
+  std::vector<double> d(k, 0.0), e(k > 0 ? k - 1 : 0, 0.0);
+  for (size_t t = 0; t < k; ++t) {
+    d[t] = 1.0 / alphas[t];
+    if (t > 0) d[t] += betas[t - 1] / alphas[t - 1];
+    if (t + 1 < k) e[t] = std::sqrt(betas[t]) / alphas[t];
+  }
+  const double lam = tridiag_eig_max(d, e);
+  if (!(lam > 0.0) || !std::isfinite(lam)) {
+    nd.lo = 0.1;
+    nd.hi = 1.1;
+    return;
+  }
+  nd.lo = 0.1 * lam;
+  nd.hi = 1.1 * lam;
+}
+
+void Solver::upload(int i, const Field& f, const double* src, bool on_device) {
+  const Dist& D = *nodes[i].dist;
+  long long off = 0;
+  for (size_t q = 0; q < D.local.size(); ++q) {
+    const BoxGeo& g = D.geo[q];
+    const long long n = (long long)g.ex * g.ey * g.ez;
+    const double* s = src + off;
+    if (!on_device) {
+      CK(cudaMemcpyAsync(staging, s, sizeof(double) * n, cudaMemcpyHostToDevice, W.stream));
+      s = staging;
+    }
+    W.cnt.launches += launch_compact_to_box(g, s, f.p[q], W.stream);
+    if (!on_device) CK(cudaStreamSynchronize(W.stream));
+    off += n;
+  }
+}
+
+void Solver::download(int i, const Field& f, double* dst, bool on_device) {
+  const Dist& D = *nodes[i].dist;
+  long long off = 0;
+  for (size_t q = 0; q < D.local.size(); ++q) {
+    const BoxGeo& g = D.geo[q];
+    const long long n = (long long)g.ex * g.ey * g.ez;
+    if (on_device) {
+      W.cnt.launches += launch_box_to_compact(g, f.p[q], dst + off, W.stream);
+    } else {
+      W.cnt.launches += launch_box_to_compact(g, f.p[q], staging, W.stream);
+      CK(cudaMemcpyAsync(dst + off, staging, sizeof(double) * n, cudaMemcpyDeviceToHost, W.stream));
+      CK(cudaStreamSynchronize(W.stream));
+    }
+    off += n;
+  }
+}
+
+// krylov_solve -> solve_cg (solver.cpp:214-266) with PcApply = one V-cycle. Scalars stay on
+// the device; the host reads back {pw, ||z||, flags} once per iteration for the stopping test
+// ||z_k|| <= max(rtol ||z_0||, atol) (solver.cpp:71-77).
+int Solver::solve(const double* b, double* x, bool on_device, int method, double rtol, double atol, int max_its,
+                  double* hist, int* reason, int* its, double* norm0, double* normf, double* t_ms, bool seeded,
+                  unsigned long long seed) {
+  CK(cudaSetDevice(W.device));
+  Node& top = nodes[0];
+  const Dist& D = *top.dist;
+  const size_t nb = D.local.size();
+  Field saved_b = top.b, saved_x = top.x;
+  top.b = cr;
+  top.x = cz;
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, W.stream));
+  *its = 0;
+  *reason = 2;  // max_its
+  // b -> cw (temporary), x0 -> cx
+  if (seeded) {
+    for (size_t q = 0; q < nb; ++q) W.cnt.launches += launch_fill_rhs(D.geo[q], cw.p[q], seed, true, W.stream);
+  } else {
+    upload(0, cw, b, on_device);
+  }
+  if (method == 5) {  // preonly: x = M b
+    for (size_t q = 0; q < nb; ++q) W.cnt.launches += launch_copy_interior(D.geo[q], cw.p[q], cr.p[q], W.stream);
+    vcycle(0);
+    if (x) download(0, cz, x, on_device);
+    CK(cudaEventRecord(e1, W.stream));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    *t_ms = ms;
+    *reason = 3;
+    *its = 1;
+    top.b = saved_b;
+    top.x = saved_x;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return 0;
+  }
+  if (x && !seeded)
+    upload(0, cx, x, on_device);
+  else
+    for (size_t q = 0; q < nb; ++q) CK(cudaMemsetAsync(cx.p[q], 0, sizeof(double) * D.geo[q].total, W.stream));
+  halo(0, cx);
+  for (size_t q = 0; q < nb; ++q)
+    W.cnt.launches += launch_residual(D.geo[q], top.op[q], cw.p[q], cx.p[q], cr.p[q], W.stream);
+  vcycle(0);
+  auto dots = [&](int op) {
+    CK(cudaMemsetAsync(rank_sums, 0, sizeof(double) * 2 * W.R, W.stream));
+    for (size_t q = 0; q < nb; ++q) {
+      W.cnt.launches += launch_dot2(D.geo[q], cr.p[q], cz.p[q], cz.p[q], part + part_off[q],
+                                    part + part_off[q] + nblk_max, W.stream);
+      W.cnt.launches += launch_reduce_partials(part + part_off[q], grid_blocks(D.geo[q]), 2, nblk_max,
+                                               rank_sums + D.wr[D.local[q]], W.R, W.stream);
+    }
+    device_allreduce_ranksums(2);
+    W.cnt.launches += launch_cg_scalars(op, rank_sums, W.R, ranks_dev, D.h.n_ranks(), scal, W.stream);
+  };
+  dots(CG_INIT);
+  CK(cudaMemcpyAsync(host_scal, scal, sizeof(double) * S_NSLOTS, cudaMemcpyDeviceToHost, W.stream));
+  CK(cudaStreamSynchronize(W.stream));
+  const double nrm0 = host_scal[S_NRM];
+  *norm0 = nrm0;
+  *normf = nrm0;
+  if (hist) hist[0] = nrm0;
+  const double tol = std::max(rtol * nrm0, atol);
+  int rc = 0;
+  if (nrm0 <= tol) {
+    *reason = nrm0 <= atol ? 1 : 0;
+  } else {
+    for (size_t q = 0; q < nb; ++q) W.cnt.launches += launch_copy_interior(D.geo[q], cz.p[q], cp.p[q], W.stream);
+    *reason = 2;
+    for (int it = 1; it <= max_its; ++it) {
+      halo(0, cp);
+      CK(cudaMemsetAsync(rank_sums, 0, sizeof(double) * 2 * W.R, W.stream));
+      for (size_t q = 0; q < nb; ++q) {
+        W.cnt.launches += launch_spmv_dot(D.geo[q], top.op[q], cp.p[q], cw.p[q], part + part_off[q], W.stream);
+        W.cnt.launches += launch_reduce_partials(part + part_off[q], grid_blocks(D.geo[q]), 1, nblk_max,
+                                                 rank_sums + D.wr[D.local[q]], W.R, W.stream);
+      }
+      device_allreduce_ranksums(1);
+      W.cnt.launches += launch_cg_scalars(CG_ALPHA, rank_sums, W.R, ranks_dev, D.h.n_ranks(), scal, W.stream);
+      for (size_t q = 0; q < nb; ++q)
+        W.cnt.launches += launch_cg_update(D.geo[q], cp.p[q], cw.p[q], cx.p[q], cr.p[q], scal, S_ALPHA, S_FLAG_PW,
+                                           W.stream);
+      vcycle(0);
+      dots(CG_BETA);
+      CK(cudaMemcpyAsync(host_scal, scal, sizeof(double) * S_NSLOTS, cudaMemcpyDeviceToHost, W.stream));
+      CK(cudaStreamSynchronize(W.stream));
+      if (host_scal[S_FLAG_PW] != 0.0) {
+        *reason = 4;
+        rc = 2;
+        break;
+      }
+      const double nrm = host_scal[S_NRM];
+      *its = it;
+      *normf = nrm;
+      if (hist) hist[it] = nrm;
+      if (nrm <= tol) {
+        *reason = nrm <= atol ? 1 : 0;
+        break;
+      }
+      if (host_scal[S_FLAG_RZ] != 0.0) {
+        *reason = 4;
+        rc = 2;
+        break;
+      }
+      for (size_t q = 0; q < nb; ++q)
+        W.cnt.launches += launch_p_update(D.geo[q], cz.p[q], cp.p[q], scal, S_BETA, W.stream);
+    }
+    if (*reason == 2) rc = 0;
+  }
+  if (x) download(0, cx, x, on_device);
+  CK(cudaEventRecord(e1, W.stream));
+  CK(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  *t_ms = ms;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  top.b = saved_b;
+  top.x = saved_x;
+  CK(cudaGetLastError());
+  return rc;
+}
+
+}  // namespace tmgx

@@ -1,0 +1,207 @@
+// Host orchestration of the B200 MG-CG path: worlds, box distributions, halo and telescope
+// plans, the MG node list, the Chebyshev interval estimator and the CG loop.
+//
+// Reference correspondence:
+//   World            spawn_world / Comm (comm.hpp:75-207): R reference ranks over P processes
+//   Dist             StructuredGrid (grid.hpp:85-118) bound to a (sub-)communicator
+//   RegionPlan       ghost_exchange (grid.cpp:645-696) and ScatterPlan::to_sub/from_sub composed
+//                    with P-hat (scatter_plan.cpp:40-114, grid.cpp:582-599)
+//   MG nodes         mg_setup / mg_apply (missing mg.cpp) with
+//                    TelescopePC (missing telescope.cpp) and LUPC (precond.cpp:220-229)
+//   estimate_bounds  chebyshev_bounds_estimate (solver.cpp:520-581)
+//   solve_cg         solve_cg (solver.cpp:214-266)
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <array>
+#include <memory>
+#include <optional>
+#include <string>
+#include <vector>
+
+#include "tmg_grid.hpp"
+#include "tmgx_kernels.cuh"
+
+namespace tmgx {
+
+void cuda_check(cudaError_t e, const char* what);
+void nccl_check(ncclResult_t e, const char* what);
+
+struct Counters {
+  long long launches = 0;
+  long long halo_bytes = 0;
+  long long tele_bytes = 0;
+  long long allreduces = 0;
+};
+
+struct World {
+  int R = 1;       // reference ranks (grid boxes)
+  int P = 1, me = 0;
+  int device = 0;
+  int first = 0, end = 1;  // local reference ranks
+  cudaStream_t stream = nullptr;
+  ncclComm_t nccl = nullptr;
+  Counters cnt;
+
+  World(int R, int P, int me, int device, const void* nccl_id);
+  ~World();
+  int owner(int world_rank) const;
+  bool local(int world_rank) const { return owner(world_rank) == me; }
+};
+
+// A GridHeader over a communicator whose comm rank m is reference rank wr[m].
+struct Dist {
+  tmg::GridHeader h;
+  std::vector<int> wr;
+  std::vector<int> local;  // comm ranks owned here, ascending
+  std::vector<BoxGeo> geo;  // aligned with local
+  int slot_of(int m) const;
+  long long local_unknowns() const;
+};
+
+std::shared_ptr<Dist> make_dist(const World& W, const tmg::GridHeader& h, const std::vector<int>& wr);
+
+// Per-local-box device buffers of one logical vector.
+struct Field {
+  std::vector<double*> p;
+  PtrTable table() const;
+};
+
+class DeviceArena {
+ public:
+  ~DeviceArena();
+  double* alloc(long long n);
+  template <class T>
+  T* alloc_t(long long n) {
+    return reinterpret_cast<T*>(alloc((n * (long long)sizeof(T) + 7) / 8));
+  }
+
+ private:
+  std::vector<void*> ptrs_;
+};
+
+Field make_field(DeviceArena& A, const Dist& D);
+
+// Region copies between two distributions (halo: same dist, box halo incl. corners).
+struct RegionPlan {
+  CopyDesc* d_local = nullptr;
+  int n_local = 0, max_local = 0;
+  CopyDesc* d_pack = nullptr;
+  int n_pack = 0, max_pack = 0;
+  CopyDesc* d_unpack = nullptr;
+  int n_unpack = 0, max_unpack = 0;
+  struct Peer {
+    int proc;
+    long long off, count;
+  };
+  std::vector<Peer> sends, recvs;
+  double* sendbuf = nullptr;
+  double* recvbuf = nullptr;
+  bool empty() const { return n_local == 0 && sends.empty() && recvs.empty(); }
+};
+
+RegionPlan build_halo_plan(World& W, DeviceArena& A, const Dist& D);
+RegionPlan build_transfer_plan(World& W, DeviceArena& A, const Dist& S, const Dist& T);
+void run_plan(World& W, const RegionPlan& plan, const Field& src, const Field& dst, bool telescope);
+
+struct ProblemDesc {
+  int kind = 0;  // 0 POISSON7, 1 VARCOEF7_HARMONIC
+  std::array<long long, 3> np{65, 65, 65};
+  std::array<int, 3> pg_hint{0, 0, 0};
+  unsigned long long seed_k = 7;
+  int n_spheres = 32;
+  double k_in = 1e4;
+};
+
+struct TeleStage {
+  int level;
+  int r;
+  std::array<int, 3> ov;
+};
+
+struct MGDesc {
+  int nlevels = 5;
+  int m = 2;
+  int est_mode = 1;  // 0 reference, 1 lanczos
+  std::vector<double> bounds;  // optional 2*nlevels
+  std::vector<TeleStage> tele;
+};
+
+enum NodeKind { SMOOTH = 0, TELESCOPE = 1, COARSE = 2 };
+
+struct Node {
+  NodeKind kind;
+  int level;
+  int stage;  // telescope stage index for TELESCOPE nodes
+  std::shared_ptr<Dist> dist;
+  std::vector<OpParams> op;  // per local box
+  Field kcoef, b, x, r, d, d2;
+  RegionPlan halo;
+  double lo = 0.1, hi = 1.1;
+  // telescope
+  RegionPlan gather, scatter;
+  // coarse
+  int nc = 0;
+  double* A_dev = nullptr;  // Ainv (perf) or LU (parity)
+  long long* piv_dev = nullptr;
+  long long* map_dev = nullptr;
+};
+
+class Solver {
+ public:
+  Solver(World& W, const ProblemDesc& P, const MGDesc& M);
+  ~Solver() = default;
+
+  World& W;
+  ProblemDesc prob;
+  MGDesc mgd;
+  DeviceArena arena;
+  std::vector<Node> nodes;
+  std::vector<int> stage_node;  // node index of each TELESCOPE node
+  Sphere* spheres_dev = nullptr;
+  std::vector<Sphere> spheres;
+
+  // CG workspace on the top node's distribution
+  Field cx, cr, cz, cp, cw;
+  double* part = nullptr;       // per local box partials [box][2][nblk]
+  std::vector<long long> part_off;
+  int nblk_max = 0;
+  double* rank_sums = nullptr;  // [2][R] (+ staging)
+  double* scal = nullptr;       // S_NSLOTS
+  double* host_scal = nullptr;  // pinned
+  int* ranks_dev = nullptr;     // comm ranks -> world ranks of the top dist
+  double* staging = nullptr;    // compact I/O staging (device)
+  long long staging_n = 0;
+
+  int node_for_level(int level) const;
+  long long local_n(int node) const { return nodes[node].dist->local_unknowns(); }
+
+  // primitives
+  void vcycle(int i);  // nodes[i].b -> nodes[i].x
+  void smooth(int i, bool zero_x);
+  void halo(int i, const Field& f);
+  void apply(int i, const Field& x, const Field& y);
+  void coarse_solve(int i);
+  void estimate(int i, int mode);
+
+  // collectives: per-box partials -> deterministic rank-ordered sums over dist (host)
+  std::array<double, 2> collect2(int i, int nslots);
+  void device_allreduce_ranksums(int nslots);
+
+  // compact (host or device) <-> field
+  void upload(int i, const Field& f, const double* src, bool on_device);
+  void download(int i, const Field& f, double* dst, bool on_device);
+
+  int solve(const double* b, double* x, bool on_device, int method, double rtol, double atol, int max_its,
+            double* hist, int* reason, int* its, double* norm0, double* normf, double* t_ms, bool seeded,
+            unsigned long long seed);
+
+ private:
+  void build_nodes();
+  void setup_coarse(Node& nd);
+  double host_k(const Dist& D, long long gi, long long gj, long long gk) const;
+};
+
+}  // namespace tmgx

@@ -1,0 +1,843 @@
+// sm_100a kernels for the MG-CG hot path. See tmgx_kernels.cuh for the HBM layout.
+//
+// All operator kernels are matrix-free restatements of the reference's CSR arithmetic:
+//   spmv row loop            dist_matrix.cpp:213-223 (acc = 0; acc += a*x, columns ascending =
+//                            natural order -z,-y,-x,c,+x,+y,+z on one rank)
+//   Jacobi                   precond.cpp:164-185 (multiply by the stored reciprocal)
+//   Chebyshev fixed sweeps   solver.cpp:88-110
+//   P (trilinear)            grid.cpp:373-428 ; R = 2^-3 P^T
+//   CG                       solver.cpp:214-266 ; dots dist_vector.cpp:33-40
+//   fill_random / RHS        dist_vector.cpp:61-65, common.hpp:40-53 keyed by natural index
+//   DenseLU::solve           precond.cpp:50-66
+// The performance build lets nvcc contract a*x+y into DFMA; the parity build (-fmad=false)
+// evaluates exactly the reference's separate multiplies and adds, so its V-cycle is bitwise
+// equal to the CPU oracle.
+//
+// Every kernel here is HBM-bandwidth bound (fp64, ~0.1-0.3 flop/B): the design levers are
+// coalesced x-contiguous rows, z-marching register queues for the +-z neighbours (each plane
+// is fetched from DRAM once), +-x/+-y neighbours served by L1, and fusing the Chebyshev
+// update, Jacobi scaling and residual into the stencil pass.
+#include "tmgx_kernels.cuh"
+
+#include <math.h>
+
+namespace tmgx {
+
+namespace {
+
+__device__ __forceinline__ long long vidx(const BoxGeo& g, int i, int j, int k) {
+  return g.base + i + g.px * j + g.pxy * k;
+}
+
+__device__ __forceinline__ double harm(double a, double b) { return 2.0 * a * b / (a + b); }
+
+// Per-vertex topology: Dirichlet vertex -> diagonal-only row; interior rows
+// drop couplings to Dirichlet neighbours.
+struct Pt {
+  bool bnd;
+  bool cxm, cxp, cym, cyp, czm, czp;  // coupling present
+  bool gxm, gxp, gym, gyp, gzm, gzp;  // neighbour inside the grid
+};
+
+__device__ __forceinline__ Pt make_pt(const BoxGeo& g, int i, int j, int k) {
+  const int gi = g.gx + i, gj = g.gy + j, gk = g.gz + k;
+  Pt p;
+  p.bnd = gi == 0 || gj == 0 || gk == 0 || gi == g.Nx - 1 || gj == g.Ny - 1 || gk == g.Nz - 1;
+  p.cxm = gi >= 2; p.cxp = gi <= g.Nx - 3;
+  p.cym = gj >= 2; p.cyp = gj <= g.Ny - 3;
+  p.czm = gk >= 2; p.czp = gk <= g.Nz - 3;
+  p.gxm = gi > 0; p.gxp = gi < g.Nx - 1;
+  p.gym = gj > 0; p.gyp = gj < g.Ny - 1;
+  p.gzm = gk > 0; p.gzp = gk < g.Nz - 1;
+  return p;
+}
+
+struct Coef {
+  double dg, invd, azm, aym, axm, axp, ayp, azp;
+};
+
+// Row coefficients. Constant k: diagonal precomputed on the host with the same summation.
+// Variable k: harmonic face averages 2 k_i k_j / (k_i + k_j), a missing
+// (out-of-grid) face uses k_i, diagonal summed -z,-y,-x,+x,+y,+z.
+template <bool VAR>
+__device__ __forceinline__ Coef coef_at(const OpParams& op, const Pt& p, double kc, double kxm, double kxp,
+                                        double kym, double kyp, double kzm, double kzp) {
+  Coef c;
+  if (!VAR) {
+    c.dg = op.cdiag;
+    c.invd = op.cinvd;
+    c.azm = c.azp = -op.ih2z;
+    c.aym = c.ayp = -op.ih2y;
+    c.axm = c.axp = -op.ih2x;
+  } else {
+    const double fzm = (p.gzm ? harm(kc, kzm) : kc) * op.ih2z;
+    const double fym = (p.gym ? harm(kc, kym) : kc) * op.ih2y;
+    const double fxm = (p.gxm ? harm(kc, kxm) : kc) * op.ih2x;
+    const double fxp = (p.gxp ? harm(kc, kxp) : kc) * op.ih2x;
+    const double fyp = (p.gyp ? harm(kc, kyp) : kc) * op.ih2y;
+    const double fzp = (p.gzp ? harm(kc, kzp) : kc) * op.ih2z;
+    double d = 0.0;
+    d += fzm;
+    d += fym;
+    d += fxm;
+    d += fxp;
+    d += fyp;
+    d += fzp;
+    c.dg = d;
+    c.invd = 1.0 / d;
+    c.azm = -fzm; c.aym = -fym; c.axm = -fxm;
+    c.axp = -fxp; c.ayp = -fyp; c.azp = -fzp;
+  }
+  return c;
+}
+
+__device__ __forceinline__ double row_apply(const Pt& p, const Coef& c, double uzm, double uym, double uxm,
+                                            double uc, double uxp, double uyp, double uzp) {
+  double acc = 0.0;
+  if (p.bnd) {
+    acc += c.dg * uc;
+  } else {
+    if (p.czm) acc += c.azm * uzm;
+    if (p.cym) acc += c.aym * uym;
+    if (p.cxm) acc += c.axm * uxm;
+    acc += c.dg * uc;
+    if (p.cxp) acc += c.axp * uxp;
+    if (p.cyp) acc += c.ayp * uyp;
+    if (p.czp) acc += c.azp * uzp;
+  }
+  return acc;
+}
+
+// z-marching register queue over one field: m = value at k-1, c = k, n = k+1.
+struct ZQ {
+  double m, c, n;
+};
+
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+  // deterministic: fixed shuffle tree, then fixed warp order
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  const int tid = threadIdx.x + blockDim.x * threadIdx.y;
+  const int w = tid >> 5, l = tid & 31;
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  const int nw = (blockDim.x * blockDim.y + 31) >> 5;
+  double s = 0.0;
+  if (tid == 0)
+    for (int q = 0; q < nw; ++q) s += sh[q];
+  return s;  // valid on tid 0
+}
+
+__device__ __forceinline__ int blk_linear() {
+  return blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+}
+
+dim3 tile_grid(const BoxGeo& g) {
+  return dim3((g.ex + kBX - 1) / kBX, (g.ey + kBY - 1) / kBY, (g.ez + kZC - 1) / kZC);
+}
+const dim3 kBlock(kBX, kBY, 1);
+
+// Loads the 7-point neighbourhood of a field around vertex v with a z queue.
+#define TMGX_NB(u, q, v)                                   \
+  const double u##xm = __ldg((u) + (v) - 1);               \
+  const double u##xp = __ldg((u) + (v) + 1);               \
+  const double u##ym = __ldg((u) + (v) - g.px);            \
+  const double u##yp = __ldg((u) + (v) + g.px);
+
+// ------------------------------------------------------------------------------------------
+// coefficient and right-hand-side generators
+// ------------------------------------------------------------------------------------------
+
+__device__ __forceinline__ unsigned long long splitmix64(unsigned long long x) {
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+__device__ __forceinline__ double hashed_uniform(unsigned long long seed, unsigned long long idx) {
+  const unsigned long long h = splitmix64(seed ^ splitmix64(idx));
+  return (double)(h >> 11) * 0x1.0p-53;
+}
+
+// k at every in-grid position of the padded box (incl. the ghost ring): the coefficient is a
+// pure function of the global vertex, so no exchange is needed (rediscretisation by injection,
+// SURVEY App. A-C7). The inside test uses explicitly unfused products (bit-exact with the oracle).
+__global__ void k_fill_coeff(BoxGeo g, double* __restrict__ kf, const Sphere* __restrict__ sph, int ns,
+                             double k_in, int varcoef) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x - 1;
+  const int j = blockIdx.y * blockDim.y + threadIdx.y - 1;
+  const int k = blockIdx.z - 1;
+  if (i > g.ex || j > g.ey) return;
+  const int gi = g.gx + i, gj = g.gy + j, gk = g.gz + k;
+  if (gi < 0 || gj < 0 || gk < 0 || gi >= g.Nx || gj >= g.Ny || gk >= g.Nz) return;
+  double val = 1.0;
+  if (varcoef) {
+    const double x = __dmul_rn((double)gi, 1.0 / (double)(g.Nx - 1));
+    const double y = __dmul_rn((double)gj, 1.0 / (double)(g.Ny - 1));
+    const double z = __dmul_rn((double)gk, 1.0 / (double)(g.Nz - 1));
+    for (int s = 0; s < ns; ++s) {
+      const double dx = __dadd_rn(x, -sph[s].cx), dy = __dadd_rn(y, -sph[s].cy), dz = __dadd_rn(z, -sph[s].cz);
+      const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+      if (d2 <= __dmul_rn(sph[s].r, sph[s].r)) {
+        val = k_in;
+        break;
+      }
+    }
+  }
+  kf[vidx(g, i, j, k)] = val;
+}
+
+__global__ void k_fill_rhs(BoxGeo g, double* __restrict__ b, unsigned long long seed, int bzero) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y * blockDim.y + threadIdx.y;
+  const int k = blockIdx.z;
+  if (i >= g.ex || j >= g.ey) return;
+  const int gi = g.gx + i, gj = g.gy + j, gk = g.gz + k;
+  const bool bnd = gi == 0 || gj == 0 || gk == 0 || gi == g.Nx - 1 || gj == g.Ny - 1 || gk == g.Nz - 1;
+  const long long nat = gi + (long long)g.Nx * (gj + (long long)g.Ny * gk);
+  double v = 2.0 * hashed_uniform(seed, (unsigned long long)nat) - 1.0;
+  if (bzero && bnd) v = 0.0;
+  b[vidx(g, i, j, k)] = v;
+}
+
+// ------------------------------------------------------------------------------------------
+// Chebyshev smoother kernels
+// ------------------------------------------------------------------------------------------
+
+template <bool VAR>
+__global__ void __launch_bounds__(kBX* kBY) k_cheb_start_zero(BoxGeo g, OpParams op, const double* __restrict__ b,
+                                                               double* __restrict__ out, double s_theta) {
+  const int i = blockIdx.x * kBX + threadIdx.x, j = blockIdx.y * kBY + threadIdx.y;
+  if (i >= g.ex || j >= g.ey) return;
+  const int k0 = blockIdx.z * kZC, k1 = min(k0 + kZC, g.ez);
+  for (int k = k0; k < k1; ++k) {
+    const long long v = vidx(g, i, j, k);
+    const Pt p = make_pt(g, i, j, k);
+    double invd;
+    if (VAR) {
+      const double* K = op.k;
+      invd = coef_at<true>(op, p, K[v], K[v - 1], K[v + 1], K[v - g.px], K[v + g.px], K[v - g.pxy], K[v + g.pxy]).invd;
+    } else {
+      invd = op.cinvd;
+    }
+    const double z = b[v] * invd;  // r = b - A*0 = b
+    out[v] = z * s_theta;
+  }
+}
+
+template <bool VAR>
+__global__ void __launch_bounds__(kBX* kBY)
+    k_cheb_start_res(BoxGeo g, OpParams op, const double* __restrict__ b, const double* __restrict__ x,
+                     double* __restrict__ r, double* __restrict__ d, double s_theta) {
+  const int i = blockIdx.x * kBX + threadIdx.x, j = blockIdx.y * kBY + threadIdx.y;
+  if (i >= g.ex || j >= g.ey) return;
+  const int k0 = blockIdx.z * kZC, k1 = min(k0 + kZC, g.ez);
+  long long v = vidx(g, i, j, k0);
+  ZQ u{__ldg(x + v - g.pxy), __ldg(x + v), 0.0};
+  ZQ kq{0.0, 0.0, 0.0};
+  if (VAR) kq = ZQ{__ldg(op.k + v - g.pxy), __ldg(op.k + v), 0.0};
+  for (int k = k0; k < k1; ++k, v += g.pxy) {
+    u.n = __ldg(x + v + g.pxy);
+    TMGX_NB(x, u, v)
+    const Pt p = make_pt(g, i, j, k);
+    Coef c;
+    if (VAR) {
+      kq.n = __ldg(op.k + v + g.pxy);
+      c = coef_at<true>(op, p, kq.c, __ldg(op.k + v - 1), __ldg(op.k + v + 1), __ldg(op.k + v - g.px),
+                        __ldg(op.k + v + g.px), kq.m, kq.n);
+      kq.m = kq.c; kq.c = kq.n;
+    } else {
+      c = coef_at<false>(op, p, 0, 0, 0, 0, 0, 0, 0);
+    }
+    const double ax = row_apply(p, c, u.m, xym, xxm, u.c, xxp, xyp, u.n);
+    const double rr = b[v] - ax;
+    r[v] = rr;
+    d[v] = (rr * c.invd) * s_theta;
+    u.m = u.c; u.c = u.n;
+  }
+}
+
+template <bool VAR>
+__global__ void __launch_bounds__(kBX* kBY)
+    k_cheb_step(BoxGeo g, OpParams op, const double* __restrict__ d, const double* r_in, const double* x_in,
+                double* __restrict__ d_new, double* r_out, double* x_out, ChebStep cs, int last) {
+  const int i = blockIdx.x * kBX + threadIdx.x, j = blockIdx.y * kBY + threadIdx.y;
+  if (i >= g.ex || j >= g.ey) return;
+  const int k0 = blockIdx.z * kZC, k1 = min(k0 + kZC, g.ez);
+  long long v = vidx(g, i, j, k0);
+  ZQ u{__ldg(d + v - g.pxy), __ldg(d + v), 0.0};
+  ZQ kq{0.0, 0.0, 0.0};
+  if (VAR) kq = ZQ{__ldg(op.k + v - g.pxy), __ldg(op.k + v), 0.0};
+  for (int k = k0; k < k1; ++k, v += g.pxy) {
+    u.n = __ldg(d + v + g.pxy);
+    TMGX_NB(d, u, v)
+    const Pt p = make_pt(g, i, j, k);
+    Coef c;
+    if (VAR) {
+      kq.n = __ldg(op.k + v + g.pxy);
+      c = coef_at<true>(op, p, kq.c, __ldg(op.k + v - 1), __ldg(op.k + v + 1), __ldg(op.k + v - g.px),
+                        __ldg(op.k + v + g.px), kq.m, kq.n);
+      kq.m = kq.c; kq.c = kq.n;
+    } else {
+      c = coef_at<false>(op, p, 0, 0, 0, 0, 0, 0, 0);
+    }
+    const double x1 = x_in ? x_in[v] + u.c : u.c;          // x += 1.0*d
+    const double ad = row_apply(p, c, u.m, dym, dxm, u.c, dxp, dyp, u.n);
+    const double r1 = r_in[v] - ad;                          // r += -1.0*ad
+    const double z = r1 * c.invd;                            // Jacobi
+    const double dn = cs.c1 * u.c + cs.c2 * z;               // d = rho'rho d + 2rho'/delta z
+    if (last) {
+      x_out[v] = x1 + dn;
+    } else {
+      x_out[v] = x1;
+      r_out[v] = r1;
+      d_new[v] = dn;
+    }
+    u.m = u.c; u.c = u.n;
+  }
+}
+
+template <bool VAR, int MODE>  // MODE 0: y = A x ; 1: r = b - A x
+__global__ void __launch_bounds__(kBX* kBY)
+    k_apply(BoxGeo g, OpParams op, const double* __restrict__ x, const double* __restrict__ b,
+            double* __restrict__ y) {
+  const int i = blockIdx.x * kBX + threadIdx.x, j = blockIdx.y * kBY + threadIdx.y;
+  if (i >= g.ex || j >= g.ey) return;
+  const int k0 = blockIdx.z * kZC, k1 = min(k0 + kZC, g.ez);
+  long long v = vidx(g, i, j, k0);
+  ZQ u{__ldg(x + v - g.pxy), __ldg(x + v), 0.0};
+  ZQ kq{0.0, 0.0, 0.0};
+  if (VAR) kq = ZQ{__ldg(op.k + v - g.pxy), __ldg(op.k + v), 0.0};
+  for (int k = k0; k < k1; ++k, v += g.pxy) {
+    u.n = __ldg(x + v + g.pxy);
+    TMGX_NB(x, u, v)
+    const Pt p = make_pt(g, i, j, k);
+    Coef c;
+    if (VAR) {
+      kq.n = __ldg(op.k + v + g.pxy);
+      c = coef_at<true>(op, p, kq.c, __ldg(op.k + v - 1), __ldg(op.k + v + 1), __ldg(op.k + v - g.px),
+                        __ldg(op.k + v + g.px), kq.m, kq.n);
+      kq.m = kq.c; kq.c = kq.n;
+    } else {
+      c = coef_at<false>(op, p, 0, 0, 0, 0, 0, 0, 0);
+    }
+    const double ax = row_apply(p, c, u.m, xym, xxm, u.c, xxp, xyp, u.n);
+    y[v] = MODE == 0 ? ax : b[v] - ax;
+    u.m = u.c; u.c = u.n;
+  }
+}
+
+// w = A p with the block partial of p.w (solver.cpp:235-236)
+template <bool VAR>
+__global__ void __launch_bounds__(kBX* kBY)
+    k_spmv_dot(BoxGeo g, OpParams op, const double* __restrict__ x, double* __restrict__ y,
+               double* __restrict__ part) {
+  __shared__ double sh[32];
+  const int i = blockIdx.x * kBX + threadIdx.x, j = blockIdx.y * kBY + threadIdx.y;
+  double acc = 0.0;
+  if (i < g.ex && j < g.ey) {
+    const int k0 = blockIdx.z * kZC, k1 = min(k0 + kZC, g.ez);
+    long long v = vidx(g, i, j, k0);
+    ZQ u{__ldg(x + v - g.pxy), __ldg(x + v), 0.0};
+    ZQ kq{0.0, 0.0, 0.0};
+    if (VAR) kq = ZQ{__ldg(op.k + v - g.pxy), __ldg(op.k + v), 0.0};
+    for (int k = k0; k < k1; ++k, v += g.pxy) {
+      u.n = __ldg(x + v + g.pxy);
+      TMGX_NB(x, u, v)
+      const Pt p = make_pt(g, i, j, k);
+      Coef c;
+      if (VAR) {
+        kq.n = __ldg(op.k + v + g.pxy);
+        c = coef_at<true>(op, p, kq.c, __ldg(op.k + v - 1), __ldg(op.k + v + 1), __ldg(op.k + v - g.px),
+                          __ldg(op.k + v + g.px), kq.m, kq.n);
+        kq.m = kq.c; kq.c = kq.n;
+      } else {
+        c = coef_at<false>(op, p, 0, 0, 0, 0, 0, 0, 0);
+      }
+      const double ax = row_apply(p, c, u.m, xym, xxm, u.c, xxp, xyp, u.n);
+      y[v] = ax;
+      acc += u.c * ax;
+      u.m = u.c; u.c = u.n;
+    }
+  }
+  const double s = block_sum(acc, sh);
+  if (threadIdx.x == 0 && threadIdx.y == 0) part[blk_linear()] = s;
+}
+
+template <bool VAR>
+__global__ void __launch_bounds__(kBX* kBY)
+    k_jacobi_dot(BoxGeo g, OpParams op, const double* __restrict__ r, double* __restrict__ z,
+                 double* __restrict__ part) {
+  __shared__ double sh[32];
+  const int i = blockIdx.x * kBX + threadIdx.x, j = blockIdx.y * kBY + threadIdx.y;
+  double acc = 0.0;
+  if (i < g.ex && j < g.ey) {
+    const int k0 = blockIdx.z * kZC, k1 = min(k0 + kZC, g.ez);
+    for (int k = k0; k < k1; ++k) {
+      const long long v = vidx(g, i, j, k);
+      double invd = op.cinvd;
+      if (VAR) {
+        const Pt p = make_pt(g, i, j, k);
+        const double* K = op.k;
+        invd = coef_at<true>(op, p, K[v], K[v - 1], K[v + 1], K[v - g.px], K[v + g.px], K[v - g.pxy], K[v + g.pxy]).invd;
+      }
+      const double rv = r[v];
+      const double zv = rv * invd;
+      z[v] = zv;
+      acc += rv * zv;
+    }
+  }
+  const double s = block_sum(acc, sh);
+  if (threadIdx.x == 0 && threadIdx.y == 0) part[blk_linear()] = s;
+}
+
+__global__ void __launch_bounds__(kBX* kBY)
+    k_dot2(BoxGeo g, const double* __restrict__ a, const double* __restrict__ b, const double* __restrict__ c,
+           double* __restrict__ pab, double* __restrict__ pcc) {
+  __shared__ double sh[32];
+  const int i = blockIdx.x * kBX + threadIdx.x, j = blockIdx.y * kBY + threadIdx.y;
+  double s1 = 0.0, s2 = 0.0;
+  if (i < g.ex && j < g.ey) {
+    const int k0 = blockIdx.z * kZC, k1 = min(k0 + kZC, g.ez);
+    for (int k = k0; k < k1; ++k) {
+      const long long v = vidx(g, i, j, k);
+      s1 += a[v] * b[v];
+      const double cv = c[v];
+      s2 += cv * cv;
+    }
+  }
+  const double t1 = block_sum(s1, sh);
+  const double t2 = block_sum(s2, sh);
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+    pab[blk_linear()] = t1;
+    pcc[blk_linear()] = t2;
+  }
+}
+
+__global__ void __launch_bounds__(kBX* kBY)
+    k_cg_update(BoxGeo g, const double* __restrict__ p, const double* __restrict__ w, double* __restrict__ x,
+                double* __restrict__ r, const double* __restrict__ scal, int as, int fs) {
+  if (scal[fs] != 0.0) return;
+  const double alpha = scal[as];
+  const int i = blockIdx.x * kBX + threadIdx.x, j = blockIdx.y * kBY + threadIdx.y;
+  if (i >= g.ex || j >= g.ey) return;
+  const int k0 = blockIdx.z * kZC, k1 = min(k0 + kZC, g.ez);
+  for (int k = k0; k < k1; ++k) {
+    const long long v = vidx(g, i, j, k);
+    x[v] += alpha * p[v];
+    r[v] += -alpha * w[v];
+  }
+}
+
+__global__ void __launch_bounds__(kBX* kBY)
+    k_p_update(BoxGeo g, const double* __restrict__ z, double* __restrict__ p, const double* __restrict__ scal,
+               int bs) {
+  const double beta = scal[bs];
+  const int i = blockIdx.x * kBX + threadIdx.x, j = blockIdx.y * kBY + threadIdx.y;
+  if (i >= g.ex || j >= g.ey) return;
+  const int k0 = blockIdx.z * kZC, k1 = min(k0 + kZC, g.ez);
+  for (int k = k0; k < k1; ++k) {
+    const long long v = vidx(g, i, j, k);
+    p[v] = z[v] + beta * p[v];
+  }
+}
+
+__global__ void __launch_bounds__(kBX* kBY)
+    k_axpy(BoxGeo g, double alpha, const double* __restrict__ x, double* __restrict__ y, int copy) {
+  const int i = blockIdx.x * kBX + threadIdx.x, j = blockIdx.y * kBY + threadIdx.y;
+  if (i >= g.ex || j >= g.ey) return;
+  const int k0 = blockIdx.z * kZC, k1 = min(k0 + kZC, g.ez);
+  for (int k = k0; k < k1; ++k) {
+    const long long v = vidx(g, i, j, k);
+    if (copy)
+      y[v] = x[v];
+    else
+      y[v] += alpha * x[v];
+  }
+}
+
+__global__ void k_zero(double* p, long long n) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
+    p[e] = 0.0;
+}
+
+// ------------------------------------------------------------------------------------------
+// transfer operators
+// ------------------------------------------------------------------------------------------
+
+// bc[I] = 0.125 * sum_{fine f near 2I, ascending natural order} w_f r_f   (R = 2^-3 P^T)
+__global__ void k_restrict(BoxGeo F, BoxGeo Cg, const double* __restrict__ rf, double* __restrict__ bc) {
+  const int I = blockIdx.x * blockDim.x + threadIdx.x, J = blockIdx.y * blockDim.y + threadIdx.y;
+  const int K = blockIdx.z;
+  if (I >= Cg.ex || J >= Cg.ey) return;
+  const int GI = Cg.gx + I, GJ = Cg.gy + J, GK = Cg.gz + K;
+  double acc = 0.0;
+#pragma unroll
+  for (int dk = -1; dk <= 1; ++dk) {
+    const int fk = 2 * GK + dk;
+    if (fk < 0 || fk >= F.Nz) continue;
+    const double wz = dk == 0 ? 1.0 : 0.5;
+#pragma unroll
+    for (int dj = -1; dj <= 1; ++dj) {
+      const int fj = 2 * GJ + dj;
+      if (fj < 0 || fj >= F.Ny) continue;
+      const double wy = dj == 0 ? 1.0 : 0.5;
+      const long long row = vidx(F, 0, fj - F.gy, fk - F.gz);
+#pragma unroll
+      for (int di = -1; di <= 1; ++di) {
+        const int fi = 2 * GI + di;
+        if (fi < 0 || fi >= F.Nx) continue;
+        const double wx = di == 0 ? 1.0 : 0.5;
+        const double w = wx * wy * wz;
+        acc += w * __ldg(rf + row + (fi - F.gx));
+      }
+    }
+  }
+  bc[vidx(Cg, I, J, K)] = 0.125 * acc;
+}
+
+// xf += P xc : per axis coincident (w 1) or midpoint (w 1/2, 1/2); columns ascending.
+__global__ void k_prolong_add(BoxGeo F, BoxGeo Cg, const double* __restrict__ xc, double* __restrict__ xf) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y * blockDim.y + threadIdx.y;
+  const int k = blockIdx.z;
+  if (i >= F.ex || j >= F.ey) return;
+  const int f[3] = {F.gx + i, F.gy + j, F.gz + k};
+  int at[3][2], cnt[3];
+  double w[3][2];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    if ((f[a] & 1) == 0) {
+      at[a][0] = f[a] >> 1; at[a][1] = at[a][0]; w[a][0] = 1.0; w[a][1] = 0.0; cnt[a] = 1;
+    } else {
+      at[a][0] = (f[a] - 1) >> 1; at[a][1] = (f[a] + 1) >> 1; w[a][0] = 0.5; w[a][1] = 0.5; cnt[a] = 2;
+    }
+  }
+  double acc = 0.0;
+  for (int tz = 0; tz < cnt[2]; ++tz)
+    for (int ty = 0; ty < cnt[1]; ++ty) {
+      const long long row = vidx(Cg, 0, at[1][ty] - Cg.gy, at[2][tz] - Cg.gz);
+      for (int tx = 0; tx < cnt[0]; ++tx) {
+        const double ww = w[0][tx] * w[1][ty] * w[2][tz];
+        acc += ww * __ldg(xc + row + (at[0][tx] - Cg.gx));
+      }
+    }
+  const long long v = vidx(F, i, j, k);
+  xf[v] = xf[v] + acc;  // axpy(1.0, P xc, x)
+}
+
+// ------------------------------------------------------------------------------------------
+// reductions and scalar logic
+// ------------------------------------------------------------------------------------------
+
+__global__ void k_reduce_partials(const double* __restrict__ part, int nblk, long long slot_stride,
+                                  double* __restrict__ out, long long out_stride) {
+  __shared__ double sh[32];
+  const int slot = blockIdx.x;
+  const double* p = part + slot * slot_stride;
+  double acc = 0.0;
+  for (int t = threadIdx.x; t < nblk; t += blockDim.x) acc += p[t];
+  const double s = block_sum(acc, sh);
+  if (threadIdx.x == 0) out[slot * out_stride] = s;
+}
+
+__global__ void k_cg_scalars(int op, const double* __restrict__ rs, int R, const int* __restrict__ ranks, int nr,
+                             double* __restrict__ scal) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double s0 = 0.0, s1 = 0.0;
+  for (int q = 0; q < nr; ++q) {
+    s0 += rs[0 * R + ranks[q]];
+    s1 += rs[1 * R + ranks[q]];
+  }
+  if (op == CG_INIT) {  // rz = r.z ; nrm0 = ||z||
+    scal[S_RZ] = s0;
+    scal[S_ZZ] = s1;
+    scal[S_NRM] = sqrt(s1);
+    scal[S_FLAG_PW] = 0.0;
+    scal[S_FLAG_RZ] = 0.0;
+  } else if (op == CG_ALPHA) {  // pw ; alpha = rz/pw (solver.cpp:236-242)
+    scal[S_PW] = s0;
+    const bool bad = s0 <= 0.0 || !isfinite(s0);
+    scal[S_FLAG_PW] = bad ? 1.0 : 0.0;
+    scal[S_ALPHA] = scal[S_RZ] / s0;
+  } else if (op == CG_BETA) {  // rz_new, ||z||, beta (solver.cpp:246-262)
+    const double rz = scal[S_RZ];
+    scal[S_RZNEW] = s0;
+    scal[S_ZZ] = s1;
+    scal[S_NRM] = sqrt(s1);
+    scal[S_RZOLD] = rz;
+    scal[S_FLAG_RZ] = (rz == 0.0 || !isfinite(s0)) ? 1.0 : 0.0;
+    scal[S_BETA] = s0 / rz;
+    scal[S_RZ] = s0;
+  } else {  // SUM2
+    scal[S_TMP0] = s0;
+    scal[S_TMP1] = s1;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// layout conversion and region copies
+// ------------------------------------------------------------------------------------------
+
+__global__ void k_box_compact(BoxGeo g, const double* __restrict__ src, double* __restrict__ dst, int to_compact) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y * blockDim.y + threadIdx.y;
+  const int k = blockIdx.z;
+  if (i >= g.ex || j >= g.ey) return;
+  const long long c = i + (long long)g.ex * (j + (long long)g.ey * k);
+  const long long v = vidx(g, i, j, k);
+  if (to_compact)
+    dst[c] = src[v];
+  else
+    dst[v] = src[c];
+}
+
+__global__ void k_region_copy(const CopyDesc* __restrict__ descs, PtrTable src, PtrTable dst,
+                              const double* __restrict__ sbuf, double* __restrict__ dbuf) {
+  const CopyDesc d = descs[blockIdx.y];
+  const long long n = (long long)d.nx * d.ny * d.nz;
+  const double* s = d.src_slot >= 0 ? src.p[d.src_slot] : sbuf;
+  double* t = d.dst_slot >= 0 ? dst.p[d.dst_slot] : dbuf;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+    const long long a = e % d.nx;
+    const long long q = e / d.nx;
+    const long long b = q % d.ny;
+    const long long c = q / d.ny;
+    t[d.dst_off + a + b * d.dst_px + c * d.dst_pxy] = s[d.src_off + a + b * d.src_px + c * d.src_pxy];
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// coarse direct solve
+// ------------------------------------------------------------------------------------------
+
+// y = Ainv x, one warp per row (fixed shuffle tree: deterministic)
+__global__ void k_dense_matvec(const double* __restrict__ A, int n, const long long* __restrict__ map,
+                               const double* __restrict__ x, double* __restrict__ y) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= n) return;
+  double acc = 0.0;
+  for (int c = lane; c < n; c += 32) acc += A[(long long)warp * n + c] * __ldg(x + map[c]);
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+  if (lane == 0) y[map[warp]] = acc;
+}
+
+// DenseLU::solve (precond.cpp:50-66) in the reference's operation order: the pivot swaps only
+// touch not-yet-updated entries, so they are applied first; the forward sweep is column
+// oriented (each y[k] still receives its updates in ascending j); the back substitution runs
+// in the reference's row order on one thread.
+__global__ void k_lu_solve(const double* __restrict__ lu, const long long* __restrict__ piv, int n,
+                           const long long* __restrict__ map, const double* __restrict__ b, double* __restrict__ x) {
+  extern __shared__ double y[];
+  for (int t = threadIdx.x; t < n; t += blockDim.x) y[t] = b[map[t]];
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int k = 0; k < n; ++k) {
+      const long long p = piv[k];
+      if (p != k) {
+        const double tmp = y[k];
+        y[k] = y[p];
+        y[p] = tmp;
+      }
+    }
+  __syncthreads();
+  for (int j = 0; j < n; ++j) {
+    const double yj = y[j];
+    for (int k = j + 1 + threadIdx.x; k < n; k += blockDim.x) y[k] -= lu[(long long)k * n + j] * yj;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    for (int k = n - 1; k >= 0; --k) {
+      double acc = y[k];
+      for (int j = k + 1; j < n; ++j) acc -= lu[(long long)k * n + j] * y[n + j];
+      y[n + k] = acc / lu[(long long)k * n + k];
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < n; t += blockDim.x) x[map[t]] = y[n + t];
+}
+
+}  // namespace
+
+// ============================================================================================
+// launchers
+// ============================================================================================
+
+int grid_blocks(const BoxGeo& g) {
+  const dim3 gr = tile_grid(g);
+  return gr.x * gr.y * gr.z;
+}
+
+static dim3 plane_grid(const BoxGeo& g, int extra) {
+  return dim3((g.ex + extra + 31) / 32, (g.ey + extra + 3) / 4, g.ez + extra);
+}
+
+int launch_fill_coeff(const BoxGeo& g, double* k, const Sphere* sph, int ns, double k_in, bool varcoef,
+                      cudaStream_t s) {
+  k_fill_coeff<<<plane_grid(g, 2), dim3(32, 4), 0, s>>>(g, k, sph, ns, k_in, varcoef ? 1 : 0);
+  return 1;
+}
+
+int launch_fill_rhs(const BoxGeo& g, double* b, unsigned long long seed, bool bzero, cudaStream_t s) {
+  k_fill_rhs<<<plane_grid(g, 0), dim3(32, 4), 0, s>>>(g, b, seed, bzero ? 1 : 0);
+  return 1;
+}
+
+int launch_cheb_start_zero(const BoxGeo& g, const OpParams& op, const double* b, double* out, double s_theta,
+                           cudaStream_t s) {
+  if (op.k)
+    k_cheb_start_zero<true><<<tile_grid(g), kBlock, 0, s>>>(g, op, b, out, s_theta);
+  else
+    k_cheb_start_zero<false><<<tile_grid(g), kBlock, 0, s>>>(g, op, b, out, s_theta);
+  return 1;
+}
+
+int launch_cheb_start_res(const BoxGeo& g, const OpParams& op, const double* b, const double* x, double* r, double* d,
+                          double s_theta, cudaStream_t s) {
+  if (op.k)
+    k_cheb_start_res<true><<<tile_grid(g), kBlock, 0, s>>>(g, op, b, x, r, d, s_theta);
+  else
+    k_cheb_start_res<false><<<tile_grid(g), kBlock, 0, s>>>(g, op, b, x, r, d, s_theta);
+  return 1;
+}
+
+int launch_cheb_step(const BoxGeo& g, const OpParams& op, const double* d, const double* r_in, const double* x_in,
+                     double* d_new, double* r_out, double* x_out, ChebStep c, bool last, cudaStream_t s) {
+  if (op.k)
+    k_cheb_step<true><<<tile_grid(g), kBlock, 0, s>>>(g, op, d, r_in, x_in, d_new, r_out, x_out, c, last ? 1 : 0);
+  else
+    k_cheb_step<false><<<tile_grid(g), kBlock, 0, s>>>(g, op, d, r_in, x_in, d_new, r_out, x_out, c, last ? 1 : 0);
+  return 1;
+}
+
+int launch_residual(const BoxGeo& g, const OpParams& op, const double* b, const double* x, double* r,
+                    cudaStream_t s) {
+  if (op.k)
+    k_apply<true, 1><<<tile_grid(g), kBlock, 0, s>>>(g, op, x, b, r);
+  else
+    k_apply<false, 1><<<tile_grid(g), kBlock, 0, s>>>(g, op, x, b, r);
+  return 1;
+}
+
+int launch_apply(const BoxGeo& g, const OpParams& op, const double* x, double* y, cudaStream_t s) {
+  if (op.k)
+    k_apply<true, 0><<<tile_grid(g), kBlock, 0, s>>>(g, op, x, nullptr, y);
+  else
+    k_apply<false, 0><<<tile_grid(g), kBlock, 0, s>>>(g, op, x, nullptr, y);
+  return 1;
+}
+
+int launch_restrict(const BoxGeo& fine, const BoxGeo& coarse, const double* rf, double* bc, cudaStream_t s) {
+  k_restrict<<<plane_grid(coarse, 0), dim3(32, 4), 0, s>>>(fine, coarse, rf, bc);
+  return 1;
+}
+
+int launch_prolong_add(const BoxGeo& fine, const BoxGeo& coarse, const double* xc, double* xf, cudaStream_t s) {
+  k_prolong_add<<<plane_grid(fine, 0), dim3(32, 4), 0, s>>>(fine, coarse, xc, xf);
+  return 1;
+}
+
+int launch_spmv_dot(const BoxGeo& g, const OpParams& op, const double* p, double* w, double* part, cudaStream_t s) {
+  if (op.k)
+    k_spmv_dot<true><<<tile_grid(g), kBlock, 0, s>>>(g, op, p, w, part);
+  else
+    k_spmv_dot<false><<<tile_grid(g), kBlock, 0, s>>>(g, op, p, w, part);
+  return 1;
+}
+
+int launch_dot2(const BoxGeo& g, const double* a, const double* b, const double* c, double* pab, double* pcc,
+                cudaStream_t s) {
+  k_dot2<<<tile_grid(g), kBlock, 0, s>>>(g, a, b, c, pab, pcc);
+  return 1;
+}
+
+int launch_jacobi_dot(const BoxGeo& g, const OpParams& op, const double* r, double* z, double* part,
+                      cudaStream_t s) {
+  if (op.k)
+    k_jacobi_dot<true><<<tile_grid(g), kBlock, 0, s>>>(g, op, r, z, part);
+  else
+    k_jacobi_dot<false><<<tile_grid(g), kBlock, 0, s>>>(g, op, r, z, part);
+  return 1;
+}
+
+int launch_cg_update(const BoxGeo& g, const double* p, const double* w, double* x, double* r, const double* scal,
+                     int as, int fs, cudaStream_t s) {
+  k_cg_update<<<tile_grid(g), kBlock, 0, s>>>(g, p, w, x, r, scal, as, fs);
+  return 1;
+}
+
+int launch_p_update(const BoxGeo& g, const double* z, double* p, const double* scal, int bs, cudaStream_t s) {
+  k_p_update<<<tile_grid(g), kBlock, 0, s>>>(g, z, p, scal, bs);
+  return 1;
+}
+
+int launch_copy_interior(const BoxGeo& g, const double* src, double* dst, cudaStream_t s) {
+  k_axpy<<<tile_grid(g), kBlock, 0, s>>>(g, 0.0, src, dst, 1);
+  return 1;
+}
+
+int launch_axpy(const BoxGeo& g, double alpha, const double* x, double* y, cudaStream_t s) {
+  k_axpy<<<tile_grid(g), kBlock, 0, s>>>(g, alpha, x, y, 0);
+  return 1;
+}
+
+int launch_zero(double* p, long long n, cudaStream_t s) {
+  const long long blocks = (n + 255) / 256;
+  k_zero<<<(unsigned)(blocks < 4096 ? (blocks > 0 ? blocks : 1) : 4096), 256, 0, s>>>(p, n);
+  return 1;
+}
+
+int launch_reduce_partials(const double* part, int nblk, int nslots, long long slot_stride, double* out,
+                           long long out_stride, cudaStream_t s) {
+  k_reduce_partials<<<nslots, 512, 0, s>>>(part, nblk, slot_stride, out, out_stride);
+  return 1;
+}
+
+int launch_cg_scalars(int op, const double* rank_sums, int R, const int* ranks_dev, int nranks, double* scal,
+                      cudaStream_t s) {
+  k_cg_scalars<<<1, 32, 0, s>>>(op, rank_sums, R, ranks_dev, nranks, scal);
+  return 1;
+}
+
+int launch_box_to_compact(const BoxGeo& g, const double* box, double* compact, cudaStream_t s) {
+  k_box_compact<<<plane_grid(g, 0), dim3(32, 4), 0, s>>>(g, box, compact, 1);
+  return 1;
+}
+
+int launch_compact_to_box(const BoxGeo& g, const double* compact, double* box, cudaStream_t s) {
+  k_box_compact<<<plane_grid(g, 0), dim3(32, 4), 0, s>>>(g, compact, box, 0);
+  return 1;
+}
+
+int launch_region_copy(const CopyDesc* desc_dev, int ndesc, int max_elems, const PtrTable& src, const PtrTable& dst,
+                       double* src_buf, double* dst_buf, cudaStream_t s) {
+  if (ndesc <= 0) return 0;
+  int bx = (max_elems + 255) / 256;
+  if (bx > 1024) bx = 1024;
+  if (bx < 1) bx = 1;
+  k_region_copy<<<dim3(bx, ndesc), 256, 0, s>>>(desc_dev, src, dst, src_buf, dst_buf);
+  return 1;
+}
+
+int launch_dense_matvec(const double* A, int n, const long long* map, const double* x, double* y, cudaStream_t s) {
+  const int threads = 256;
+  const int blocks = (n * 32 + threads - 1) / threads;
+  k_dense_matvec<<<blocks, threads, 0, s>>>(A, n, map, x, y);
+  return 1;
+}
+
+int launch_lu_solve(const double* lu, const long long* piv, int n, const long long* map, const double* b, double* x,
+                    cudaStream_t s) {
+  const size_t shmem = sizeof(double) * 2 * (size_t)n;
+  if (shmem > 48 * 1024) cudaFuncSetAttribute(k_lu_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem);
+  k_lu_solve<<<1, 256, shmem, s>>>(lu, piv, n, map, b, x);
+  return 1;
+}
+
+bool parity_build() {
+#ifdef TMGX_PARITY
+  return true;
+#else
+  return false;
+#endif
+}
+
+}  // namespace tmgx

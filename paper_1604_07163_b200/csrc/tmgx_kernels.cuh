@@ -1,0 +1,126 @@
+// sm_100a kernels for the MG-CG hot path (declarations of the host launchers).
+//
+// Data layout in HBM: every reference rank's box of a level is stored as a
+// padded array with a one-vertex ghost ring on every side; element (i,j,k) of the box
+// (i-fastest, i in [-1, ex]) lives at base + i + px*j + pxy*k. base puts i = 0 on a 32-byte
+// sector boundary, px is a multiple of 4 doubles. Ghost entries carry neighbour boxes'
+// values after a halo exchange; the kernels never read ghosts outside the global grid.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace tmgx {
+
+constexpr int kXO = 4;         // padding so that i = 0 is sector aligned
+constexpr int kBX = 32;        // threads along x per block
+constexpr int kBY = 4;         // threads along y per block
+constexpr int kZC = 16;        // z planes marched per block
+constexpr int kMaxLocal = 64;  // local boxes per process
+
+struct BoxGeo {
+  int ex, ey, ez;  // extents
+  int gx, gy, gz;  // global lower corner
+  int Nx, Ny, Nz;  // global grid
+  long long px, pxy, base, total;
+};
+
+// Operator parameters for the 7-point FD operator of one level.
+struct OpParams {
+  double ih2x, ih2y, ih2z;  // 1/h^2 per axis (grid.cpp:144-151 spacing)
+  double cdiag;             // constant-coefficient diagonal (sum of the six face terms)
+  double cinvd;             // 1.0 / cdiag (precond.cpp:179)
+  const double* k;          // vertex coefficient (padded layout, ghosts filled); nullptr = k == 1
+};
+
+struct Sphere {
+  double cx, cy, cz, r;
+};
+
+struct ChebStep {
+  double c1, c2;  // d_new = c1*d + c2*z  (solver.cpp:106-108)
+};
+
+// Region-copy descriptor: a 3D sub-box copied between two padded arrays or a packed buffer.
+struct CopyDesc {
+  int src_slot, dst_slot;     // index into the pointer tables (-1 = packed buffer)
+  long long src_off, dst_off; // element offset of the region origin (or buffer offset)
+  int nx, ny, nz;
+  long long src_px, src_pxy, dst_px, dst_pxy;  // pitches (packed: nx, nx*ny)
+};
+
+struct PtrTable {
+  double* p[kMaxLocal];
+};
+
+// ---- launchers (all asynchronous on `s`; return number of kernels launched) ----
+int launch_fill_coeff(const BoxGeo& g, double* k, const Sphere* spheres_dev, int n_spheres, double k_in,
+                      bool varcoef, cudaStream_t s);
+int launch_fill_rhs(const BoxGeo& g, double* b, unsigned long long seed, bool boundary_zero, cudaStream_t s);
+
+// Chebyshev(Jacobi) smoother pieces (solver.cpp:79-110 + precond.cpp:183-185).
+// start_zero: d = (b * invd) * s_theta ; if write_x: x = d instead.
+int launch_cheb_start_zero(const BoxGeo& g, const OpParams& op, const double* b, double* d_or_x, double s_theta,
+                           cudaStream_t s);
+// start_res: r = b - A x ; d = (r*invd)*s_theta  (x needs halo)
+int launch_cheb_start_res(const BoxGeo& g, const OpParams& op, const double* b, const double* x, double* r,
+                          double* d, double s_theta, cudaStream_t s);
+// step: x1 = x_in + d (x_in null -> d) ; r1 = r_in - A d ; d_new = c1 d + c2 (r1*invd);
+// last: x_out = x1 + d_new only ; else x_out = x1, r_out = r1, d_new.
+int launch_cheb_step(const BoxGeo& g, const OpParams& op, const double* d, const double* r_in, const double* x_in,
+                     double* d_new, double* r_out, double* x_out, ChebStep c, bool last, cudaStream_t s);
+int launch_residual(const BoxGeo& g, const OpParams& op, const double* b, const double* x, double* r,
+                    cudaStream_t s);
+int launch_apply(const BoxGeo& g, const OpParams& op, const double* x, double* y, cudaStream_t s);
+// bc = 2^-3 P^T rf over the coarse box (rf needs a box halo incl. corners).
+int launch_restrict(const BoxGeo& fine, const BoxGeo& coarse, const double* rf, double* bc, cudaStream_t s);
+// xf += P xc (xc needs a box halo incl. corners).
+int launch_prolong_add(const BoxGeo& fine, const BoxGeo& coarse, const double* xc, double* xf, cudaStream_t s);
+
+// CG / estimator pieces; partials: per-block fp64 partial sums (deterministic tree).
+int grid_blocks(const BoxGeo& g);
+int launch_spmv_dot(const BoxGeo& g, const OpParams& op, const double* p, double* w, double* part,
+                    cudaStream_t s);
+int launch_dot2(const BoxGeo& g, const double* a, const double* b, const double* c, double* part_ab,
+                double* part_cc, cudaStream_t s);  // a.b and c.c
+int launch_jacobi_dot(const BoxGeo& g, const OpParams& op, const double* r, double* z, double* part,
+                      cudaStream_t s);  // z = r*invd, part = r.z
+// x += alpha p ; r += (-alpha) w ; alpha = scal[alpha_slot]; skipped when scal[flag_slot] != 0.
+int launch_cg_update(const BoxGeo& g, const double* p, const double* w, double* x, double* r, const double* scal,
+                     int alpha_slot, int flag_slot, cudaStream_t s);
+// p = z + beta p ; beta = scal[beta_slot]
+int launch_p_update(const BoxGeo& g, const double* z, double* p, const double* scal, int beta_slot, cudaStream_t s);
+int launch_copy_interior(const BoxGeo& g, const double* src, double* dst, cudaStream_t s);
+int launch_axpy(const BoxGeo& g, double alpha, const double* x, double* y, cudaStream_t s);  // y += alpha x
+int launch_zero(double* p, long long n, cudaStream_t s);
+// Sum `nblk` partials of each of `nslots` slots (stride `slot_stride`) into out[slot*out_stride].
+int launch_reduce_partials(const double* part, int nblk, int nslots, long long slot_stride, double* out,
+                           long long out_stride, cudaStream_t s);
+
+// Scalar finalisation. rank_sums[slot*R + rank]; sums over the listed ranks in order.
+enum ScalSlot {
+  S_RZ = 0, S_PW, S_ALPHA, S_BETA, S_RZNEW, S_ZZ, S_NRM, S_FLAG_PW, S_FLAG_RZ, S_RZOLD, S_TMP0, S_TMP1,
+  S_NSLOTS = 16
+};
+enum CgOp { CG_INIT = 0, CG_ALPHA = 1, CG_BETA = 2, SUM2 = 3 };
+int launch_cg_scalars(int op, const double* rank_sums, int R, const int* ranks_dev, int nranks, double* scal,
+                      cudaStream_t s);
+
+// Compact (rank-block local order) <-> padded box.
+int launch_box_to_compact(const BoxGeo& g, const double* box, double* compact, cudaStream_t s);
+int launch_compact_to_box(const BoxGeo& g, const double* compact, double* box, cudaStream_t s);
+
+// Region copies (halo exchange, telescope gather/scatter, pack/unpack).
+int launch_region_copy(const CopyDesc* desc_dev, int ndesc, int max_elems, const PtrTable& src,
+                       const PtrTable& dst, double* src_buf, double* dst_buf, cudaStream_t s);
+
+// Coarse direct solve: perf build y = Ainv x ; parity build: DenseLU::solve loop order.
+// `map[c]` = padded-box element offset of compact (natural) index c.
+int launch_dense_matvec(const double* A, int n, const long long* map, const double* x, double* y, cudaStream_t s);
+int launch_lu_solve(const double* lu, const long long* piv, int n, const long long* map, const double* b,
+                    double* x, cudaStream_t s);
+
+bool parity_build();
+
+}  // namespace tmgx

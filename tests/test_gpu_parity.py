@@ -1,0 +1,259 @@
+"""GPU parity: the sm_100a path (through the C-ABI) against the pinned CPU oracle.
+
+Bar (BASELINE.json north_star): index maps bit-exact; CG iteration counts equal (or +-1);
+solution relative difference <= 1e-9 in fp64. The parity build (-fmad=false) must reproduce
+the oracle's stencil, smoother, transfer, coarse-solve and V-cycle arithmetic bit for bit;
+the performance build (FMA contraction) within 1e-12 relative on those kernels.
+"""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_1604_07163_b200 import tmgx as T
+
+pytestmark = pytest.mark.gpu
+
+TOL_KERNEL = 1e-12  # perf build vs oracle per kernel (FMA contraction only)
+TOL_SOLUTION = 1e-9  # north_star: final solution relative agreement
+
+
+def _need_gpu():
+    try:
+        import torch
+
+        if not torch.cuda.is_available():
+            pytest.skip("no CUDA device")
+    except ImportError:
+        pytest.skip("torch missing")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def gpu():
+    _need_gpu()
+
+
+def rel(a, b):
+    return np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300)
+
+
+def check(a, b, parity):
+    if parity:
+        assert np.array_equal(a, b), f"not bitwise: max rel {rel(a, b):.3e}"
+    else:
+        assert rel(a, b) <= TOL_KERNEL, f"rel {rel(a, b):.3e}"
+
+
+def make(np3, nlevels, kind=T.POISSON7, m=2, est=T.EST_LANCZOS, parity=False, n_ranks=1, bounds=None,
+         telescope=(), hint=None, seed_k=7):
+    w = T.World(n_ranks=n_ranks, parity=parity)
+    s = T.SolverNode(w, T.Problem(np3, kind, proc_grid_hint=hint, seed_k=seed_k),
+                     T.MGConfig(nlevels, m, est, cheb_bounds=bounds, telescope=list(telescope)))
+    return w, s
+
+
+def oracle_mg(np3, nlevels, kind=O.POISSON7, m=2, est=O.EST_LANCZOS, seed_k=7):
+    return O.MG(np3, nlevels, kind=kind, smooth_its=m, est_mode=est, seed_k=seed_k)
+
+
+def oracle_bounds(mg, nlevels):
+    b = np.zeros(2 * nlevels)
+    for l in range(1, nlevels):
+        b[2 * l], b[2 * l + 1] = mg.bounds(l)
+    return b
+
+
+KINDS = [(T.POISSON7, O.POISSON7), (T.VARCOEF7_HARMONIC, O.VARCOEF7)]
+
+
+@pytest.mark.parametrize("parity", [True, False])
+@pytest.mark.parametrize("kind", KINDS)
+def test_operator_apply(parity, kind):
+    np3, nl = (17, 33, 9), 3
+    om = oracle_mg(np3, nl, kind[1])
+    w, s = make(np3, nl, kind[0], parity=parity, bounds=oracle_bounds(om, nl))
+    rng = np.random.default_rng(1)
+    for level in range(nl):
+        n = om.level_size(level)
+        x = rng.standard_normal(n)
+        check(s.level_apply(level, x), om.apply(level, x), parity)
+
+
+@pytest.mark.parametrize("parity", [True, False])
+@pytest.mark.parametrize("kind", KINDS)
+@pytest.mark.parametrize("m", [1, 2, 3])
+def test_smoother(parity, kind, m):
+    np3, nl = (17, 17, 17), 3
+    om = oracle_mg(np3, nl, kind[1], m=m)
+    w, s = make(np3, nl, kind[0], m=m, parity=parity, bounds=oracle_bounds(om, nl))
+    rng = np.random.default_rng(2)
+    n = om.level_size(2)
+    b = rng.standard_normal(n)
+    check(s.level_smooth(2, b), om.smooth(2, b), parity)  # from x = 0
+    x0 = rng.standard_normal(n)
+    check(s.level_smooth(2, b, x0), om.smooth(2, b, x0), parity)
+
+
+@pytest.mark.parametrize("parity", [True, False])
+def test_transfer_and_coarse(parity):
+    np3, nl = (17, 33, 17), 3
+    om = oracle_mg(np3, nl, O.VARCOEF7)
+    w, s = make(np3, nl, T.VARCOEF7_HARMONIC, parity=parity, bounds=oracle_bounds(om, nl))
+    rng = np.random.default_rng(3)
+    n2, n1, n0 = om.level_size(2), om.level_size(1), om.level_size(0)
+    b, x = rng.standard_normal(n2), rng.standard_normal(n2)
+    r = b - om.apply(2, x)
+    check(s.residual_restrict(2, b, x), om.restrict(2, r), parity)
+    xc, xf = rng.standard_normal(n1), rng.standard_normal(n2)
+    check(s.prolong_add(2, xc, xf), om.prolong_add(2, xc, xf), parity)
+    bc = rng.standard_normal(n0)
+    got, want = s.coarse_solve(bc), om.coarse_solve(bc)
+    if parity:
+        assert np.array_equal(got, want)
+    else:  # explicit inverse from the same LU factors
+        assert rel(got, want) < 1e-12
+
+
+@pytest.mark.parametrize("parity", [True, False])
+@pytest.mark.parametrize("kind", KINDS)
+def test_vcycle(parity, kind):
+    np3, nl = (33, 33, 33), 4
+    om = oracle_mg(np3, nl, kind[1])
+    w, s = make(np3, nl, kind[0], parity=parity, bounds=oracle_bounds(om, nl))
+    b = O.rhs(np3, 42)
+    got, want = s.pc_apply(b), om.vcycle(nl - 1, b)
+    if parity:
+        assert np.array_equal(got, want)
+    else:
+        assert rel(got, want) < 1e-11
+
+
+@pytest.mark.parametrize("est", [T.EST_LANCZOS, T.EST_REFERENCE])
+@pytest.mark.parametrize("kind", KINDS)
+def test_estimator(est, kind):
+    np3, nl = (33, 33, 33), 4
+    om = oracle_mg(np3, nl, kind[1], est=est)
+    w, s = make(np3, nl, kind[0], est=est)
+    for l in range(1, nl):
+        lo, hi = s.bounds(l)
+        olo, ohi = om.bounds(l)
+        assert abs(hi - ohi) / ohi < 1e-10 and abs(lo - olo) / olo < 1e-10
+
+
+def test_rhs_bitwise():
+    w, s = make((33, 17, 9), 2)
+    assert np.array_equal(s.rhs(42), O.rhs((33, 17, 9), 42))
+
+
+GOLDEN = [  # SURVEY.md §8(c) table, reproduced bitwise by the oracle
+    ((33,) * 3, 4, 2, T.EST_LANCZOS, 10, 0.059938767310706596),
+    ((65,) * 3, 5, 2, T.EST_LANCZOS, 10, 0.060110378198142883),
+    ((65,) * 3, 5, 3, T.EST_LANCZOS, 6, 0.060110378065276547),
+    ((33,) * 3, 4, 2, T.EST_REFERENCE, 52, 0.059938766918487769),
+    ((65,) * 3, 5, 2, T.EST_REFERENCE, 60, 0.060110377849060662),
+]
+
+
+@pytest.mark.parametrize("parity", [False, True])
+@pytest.mark.parametrize("np3,nl,m,est,its,xnorm", GOLDEN)
+def test_mgcg_golden(parity, np3, nl, m, est, its, xnorm):
+    w, s = make(np3, nl, m=m, est=est, parity=parity)
+    b = O.rhs(np3, 42)
+    x, rep = s.solve(b, cfg=T.KrylovConfig("cg", rtol=1e-8))
+    assert rep.converged()
+    assert abs(rep.iterations - its) <= 1
+    assert abs(np.sqrt(np.dot(x, x)) - xnorm) / xnorm < TOL_SOLUTION
+    if rep.iterations == its:
+        om = oracle_mg(np3, nl, m=m, est=est)
+        xo, orep = om.solve(b, rtol=1e-8)
+        assert rel(x, xo) < TOL_SOLUTION
+        np.testing.assert_allclose(rep.residual_history, orep["history"], rtol=1e-9)
+
+
+@pytest.mark.parametrize("np3,nl,m", [((33, 33, 33), 4, 3), ((65, 65, 33), 5, 2)])
+def test_mgcg_varcoef(np3, nl, m):
+    om = oracle_mg(np3, nl, O.VARCOEF7, m=m)
+    b = O.rhs(np3, 1234)
+    xo, orep = om.solve(b, rtol=1e-8)
+    w, s = make(np3, nl, T.VARCOEF7_HARMONIC, m=m)
+    x, rep = s.solve(b, cfg=T.KrylovConfig("cg", rtol=1e-8))
+    assert abs(rep.iterations - orep["iterations"]) <= 1
+    if rep.iterations == orep["iterations"]:
+        assert rel(x, xo) < TOL_SOLUTION
+
+
+def _decomposed(np3, nl, n_ranks, telescope=(), kind=T.POISSON7, m=2, hint=None):
+    w, s = make(np3, nl, kind, m=m, n_ranks=n_ranks, telescope=telescope, hint=hint)
+    h, _ = s.level_info(nl - 1)
+    perm = T.rank_block_to_natural(h)
+    return w, s, h, perm
+
+
+@pytest.mark.parametrize("n_ranks,tele", [
+    (2, ()), (4, ()), (8, ()),
+    (8, (T.TelescopeStage(1, 8),)),
+    (8, (T.TelescopeStage(2, 8),)),
+    (4, (T.TelescopeStage(2, 4),)),
+    (8, (T.TelescopeStage(2, 4), T.TelescopeStage(1, 2))),
+    (8, (T.TelescopeStage(2, 2, (None, None, 1)), T.TelescopeStage(1, 4))),
+    (6, (T.TelescopeStage(1, 6),)),
+])
+def test_decomposed_and_telescoped(n_ranks, tele):
+    """Box decompositions over emulated ranks on one GPU (spawn_world-style), with single and
+    nested telescoping: same iterations (+-1) and solution (1e-9) as the 1-rank oracle."""
+    np3, nl = (33, 33, 33), 4
+    if not tele:
+        # an untelescoped multi-rank hierarchy cannot end in LU on more than one rank
+        with pytest.raises(T.ConfigError):
+            make(np3, nl, n_ranks=n_ranks)
+        tele = (T.TelescopeStage(0, n_ranks),)
+    w, s, h, perm = _decomposed(np3, nl, n_ranks, tele)
+    b_nat = O.rhs(np3, 42)
+    x, rep = s.solve(b_nat[perm], cfg=T.KrylovConfig("cg", rtol=1e-8))
+    x_nat = np.empty_like(x)
+    x_nat[perm] = x
+    om = oracle_mg(np3, nl)
+    xo, orep = om.solve(b_nat, rtol=1e-8)
+    assert abs(rep.iterations - orep["iterations"]) <= 1
+    if rep.iterations == orep["iterations"]:
+        assert rel(x_nat, xo) < TOL_SOLUTION
+
+
+def test_vcycle_partition_independent_bitwise():
+    """With fixed Chebyshev bounds the V-cycle has no reductions, and every kernel evaluates in
+    natural order, so decomposed + telescoped V-cycles are bitwise equal to the 1-rank one."""
+    np3, nl = (33, 33, 33), 4
+    om = oracle_mg(np3, nl)
+    bounds = oracle_bounds(om, nl)
+    b_nat = O.rhs(np3, 42)
+    w1, s1 = make(np3, nl, parity=True, bounds=bounds)
+    y1 = s1.pc_apply(b_nat)
+    assert np.array_equal(y1, om.vcycle(nl - 1, b_nat))
+    w8, s8 = make(np3, nl, parity=True, n_ranks=8, bounds=bounds,
+                  telescope=[T.TelescopeStage(2, 4), T.TelescopeStage(1, 2)])
+    h, _ = s8.level_info(nl - 1)
+    perm = T.rank_block_to_natural(h)
+    y8 = s8.pc_apply(b_nat[perm])
+    y8n = np.empty_like(y8)
+    y8n[perm] = y8
+    assert np.array_equal(y8n, y1)
+
+
+def test_telescope_gather_scatter_maps():
+    """Gather == P-hat^T x then ScatterPlan::to_sub (bitwise); scatter inverts it (AC3)."""
+    np3, nl = (65, 65, 33), 3
+    w, s = make(np3, nl, n_ranks=8, telescope=[T.TelescopeStage(1, 4)])
+    hp, n_par = s.level_info(2)  # outer level
+    # stage 0 sits at level 1: parent header = outer level-1 header
+    hp1 = T.coarsen(hp)
+    sp = T.split_strided(8, 4)
+    hn = T.repartition_onto(hp1, sp)
+    assert hn.proc_grid == (1, 2, 1)
+    n1 = hp1.n_unknowns()
+    x_par = np.arange(n1, dtype=np.float64) * 0.5 + 1.0  # rank-block order of parent level 1
+    y = s.telescope_gather(0, x_par, n1)
+    cols = T.build_permutation(hp1, hn)
+    want = np.empty(n1)
+    want[cols] = x_par  # (P-hat^T x)[q] with q = cols[p]
+    assert np.array_equal(y, want)
+    back = s.telescope_scatter(0, y, n1)
+    assert np.array_equal(back, x_par)
