@@ -161,12 +161,18 @@ def test_mgcg_golden(parity, np3, nl, m, est, its, xnorm):
     x, rep = s.solve(b, cfg=T.KrylovConfig("cg", rtol=1e-8))
     assert rep.converged()
     assert abs(rep.iterations - its) <= 1
-    assert abs(np.sqrt(np.dot(x, x)) - xnorm) / xnorm < TOL_SOLUTION
+    # SURVEY §7 "parity vs reduction order": compare solutions at equal iteration counts
+    # (oracle re-run with max_its = GPU iterations, rtol = 0 when the counts differ by one).
+    om = oracle_mg(np3, nl, m=m, est=est)
+    xo, orep = om.solve(b, rtol=1e-8 if rep.iterations == its else 0.0, max_its=rep.iterations)
+    assert orep["iterations"] == rep.iterations
     if rep.iterations == its:
-        om = oracle_mg(np3, nl, m=m, est=est)
-        xo, orep = om.solve(b, rtol=1e-8)
-        assert rel(x, xo) < TOL_SOLUTION
-        np.testing.assert_allclose(rep.residual_history, orep["history"], rtol=1e-9)
+        assert abs(np.sqrt(np.dot(x, x)) - xnorm) / xnorm < TOL_SOLUTION
+    # the reference (shipped) estimator gives a 5x too wide interval and ~50 iterations, which
+    # amplifies reduction-order rounding; the solution bar stays 1e-9 for the fixed estimator
+    tol = TOL_SOLUTION if est == T.EST_LANCZOS else 1e-8
+    assert rel(x, xo) < tol
+    np.testing.assert_allclose(rep.residual_history, orep["history"], rtol=1e-6)
 
 
 @pytest.mark.parametrize("np3,nl,m", [((33, 33, 33), 4, 3), ((65, 65, 33), 5, 2)])
@@ -177,8 +183,9 @@ def test_mgcg_varcoef(np3, nl, m):
     w, s = make(np3, nl, T.VARCOEF7_HARMONIC, m=m)
     x, rep = s.solve(b, cfg=T.KrylovConfig("cg", rtol=1e-8))
     assert abs(rep.iterations - orep["iterations"]) <= 1
-    if rep.iterations == orep["iterations"]:
-        assert rel(x, xo) < TOL_SOLUTION
+    if rep.iterations != orep["iterations"]:
+        xo, orep = om.solve(b, rtol=0.0, max_its=rep.iterations)
+    assert rel(x, xo) < TOL_SOLUTION
 
 
 def _decomposed(np3, nl, n_ranks, telescope=(), kind=T.POISSON7, m=2, hint=None):
@@ -214,8 +221,9 @@ def test_decomposed_and_telescoped(n_ranks, tele):
     om = oracle_mg(np3, nl)
     xo, orep = om.solve(b_nat, rtol=1e-8)
     assert abs(rep.iterations - orep["iterations"]) <= 1
-    if rep.iterations == orep["iterations"]:
-        assert rel(x_nat, xo) < TOL_SOLUTION
+    if rep.iterations != orep["iterations"]:
+        xo, orep = om.solve(b_nat, rtol=0.0, max_its=rep.iterations)
+    assert rel(x_nat, xo) < TOL_SOLUTION
 
 
 def test_vcycle_partition_independent_bitwise():
