@@ -73,7 +73,8 @@ static BoxGeo make_geo(const tmg::GridHeader& h, int m) {
   g.Nx = (int)h.npoints[0];
   g.Ny = (int)h.npoints[1];
   g.Nz = (int)h.npoints[2];
-  g.px = ((kXO + g.ex + 1) + 3) / 4 * 4;
+  g.zc = choose_zc(g.ex, g.ey, g.ez);
+  g.px =((kXO + g.ex + 1) + 3) / 4 * 4;
   g.pxy = g.px * (g.ey + 2);
   g.base = kXO + g.px + g.pxy;
   g.total = g.pxy * (g.ez + 2) + 8;
@@ -323,6 +324,7 @@ static OpParams make_op(const tmg::GridHeader& h) {
 
 Solver::Solver(World& W_, const ProblemDesc& P, const MGDesc& M) : W(W_), prob(P), mgd(M) {
   CK(cudaSetDevice(W.device));
+  if (const char* e = std::getenv("TMGX_GRAPHS")) use_graphs = std::string(e) != "0";
   if (mgd.nlevels < 1) throw tmg::ConfigError("mg: number of levels must be >= 1");
   if (mgd.m < 1) throw tmg::ConfigError("mg: smoother iterations must be >= 1");
   if (prob.kind == 1) {
@@ -403,9 +405,20 @@ void Solver::build_nodes() {
     throw tmg::ConfigError("pc_type lu needs a single-rank communicator; repartition first, e.g. pc_type telescope "
                            "with <prefix>telescope_pc_type lu");
 
+  // CG workspace; the top node's V-cycle input/output are the CG's r and z (fixed bindings,
+  // so the captured iteration graph stays valid)
+  {
+    const Dist& D0 = *nodes[0].dist;
+    cx = make_field(arena, D0);
+    cr = make_field(arena, D0);
+    cz = make_field(arena, D0);
+    cp = make_field(arena, D0);
+    cw = make_field(arena, D0);
+  }
   // buffers, operators, plans
   int nloc_max = 1;
-  for (auto& nd : nodes) {
+  for (size_t ni = 0; ni < nodes.size(); ++ni) {
+    Node& nd = nodes[ni];
     const Dist& D = *nd.dist;
     nloc_max = std::max<int>(nloc_max, (int)D.local.size());
     if (prob.kind == 1) {
@@ -421,8 +434,8 @@ void Solver::build_nodes() {
       nblk_max = std::max(nblk_max, grid_blocks(D.geo[q]));
       staging_n = std::max<long long>(staging_n, D.local_unknowns());
     }
-    nd.b = make_field(arena, D);
-    nd.x = make_field(arena, D);
+    nd.b = ni == 0 ? cr : make_field(arena, D);
+    nd.x = ni == 0 ? cz : make_field(arena, D);
     if (nd.kind == SMOOTH) {
       nd.r = make_field(arena, D);
       nd.d = make_field(arena, D);
@@ -445,11 +458,6 @@ void Solver::build_nodes() {
     const Dist& D0 = *nodes[0].dist;
     ranks_dev = arena.alloc_t<int>(D0.h.n_ranks());
     CK(cudaMemcpy(ranks_dev, D0.wr.data(), sizeof(int) * D0.wr.size(), cudaMemcpyHostToDevice));
-    cx = make_field(arena, D0);
-    cr = make_field(arena, D0);
-    cz = make_field(arena, D0);
-    cp = make_field(arena, D0);
-    cw = make_field(arena, D0);
   }
   setup_coarse(nodes.back());
   CK(cudaStreamSynchronize(W.stream));
@@ -677,12 +685,22 @@ void Solver::device_allreduce_ranksums(int nslots) {
 // Deterministic collective sums for node i's distribution: per-box block partials are reduced
 // in a fixed tree, then summed over the communicator's ranks in rank order (the reference's
 // ordered_fold_sum, comm.cpp:338-351, at box granularity). Identical on every process.
-std::array<double, 2> Solver::collect2(int i, int nslots) {
+// The parity build replaces the tree by the reference's serial left fold (a.b recomputed).
+void Solver::reduce_local(const Dist& D, int nslots, const Field* a, const Field* b, const Field* c) {
+  for (size_t q = 0; q < D.local.size(); ++q) {
+    double* out = rank_sums + D.wr[D.local[q]];
+    if (parity_build() && a && b)
+      W.cnt.launches += launch_fold_dot(D.geo[q], a->p[q], b->p[q], c ? c->p[q] : nullptr, out, W.R, W.stream);
+    else
+      W.cnt.launches += launch_reduce_partials(part + part_off[q], grid_blocks(D.geo[q]), nslots, nblk_max, out,
+                                               W.R, W.stream);
+  }
+}
+
+std::array<double, 2> Solver::collect2(int i, int nslots, const Field* a, const Field* b) {
   const Dist& D = *nodes[i].dist;
   CK(cudaMemsetAsync(rank_sums, 0, sizeof(double) * 2 * W.R, W.stream));
-  for (size_t q = 0; q < D.local.size(); ++q)
-    W.cnt.launches += launch_reduce_partials(part + part_off[q], grid_blocks(D.geo[q]), nslots, nblk_max,
-                                             rank_sums + D.wr[D.local[q]], W.R, W.stream);
+  reduce_local(D, nslots, a, b, nullptr);
   device_allreduce_ranksums(nslots);
   CK(cudaMemcpyAsync(host_scal, rank_sums, sizeof(double) * 2 * W.R, cudaMemcpyDeviceToHost, W.stream));
   CK(cudaStreamSynchronize(W.stream));
@@ -735,7 +753,7 @@ void Solver::estimate(int i, int mode) {
   for (size_t q = 0; q < nb; ++q) W.cnt.launches += launch_fill_rhs(D.geo[q], r.p[q], 0x5eedbeefULL, false, W.stream);
   for (size_t q = 0; q < nb; ++q)
     W.cnt.launches += launch_jacobi_dot(D.geo[q], nd.op[q], r.p[q], z.p[q], part + part_off[q], W.stream);
-  double rz = collect2(i, 1)[0];
+  double rz = collect2(i, 1, &r, &z)[0];
   for (size_t q = 0; q < nb; ++q) W.cnt.launches += launch_copy_interior(D.geo[q], z.p[q], p.p[q], W.stream);
   std::vector<double> alphas, betas;
   bool broke = false;
@@ -744,7 +762,7 @@ void Solver::estimate(int i, int mode) {
     halo(i, p);
     for (size_t q = 0; q < nb; ++q)
       W.cnt.launches += launch_spmv_dot(D.geo[q], nd.op[q], p.p[q], w.p[q], part + part_off[q], W.stream);
-    const double pw = collect2(i, 1)[0];
+    const double pw = collect2(i, 1, &p, &w)[0];
     if (pw <= 0.0 || !std::isfinite(pw)) {
       if (alphas.empty()) broke = true;
       break;
@@ -753,7 +771,7 @@ void Solver::estimate(int i, int mode) {
     for (size_t q = 0; q < nb; ++q) W.cnt.launches += launch_axpy(D.geo[q], -alpha, w.p[q], r.p[q], W.stream);
     for (size_t q = 0; q < nb; ++q)
       W.cnt.launches += launch_jacobi_dot(D.geo[q], nd.op[q], r.p[q], z.p[q], part + part_off[q], W.stream);
-    const double rz_new = collect2(i, 1)[0];
+    const double rz_new = collect2(i, 1, &r, &z)[0];
     alphas.push_back(alpha);
     if (rz_new <= 0.0 || !std::isfinite(rz_new)) break;
     const double beta = rz_new / rz;
@@ -824,8 +842,66 @@ void Solver::download(int i, const Field& f, double* dst, bool on_device) {
 }
 
 // krylov_solve -> solve_cg (solver.cpp:214-266) with PcApply = one V-cycle. Scalars stay on
-// the device; the host reads back {pw, ||z||, flags} once per iteration for the stopping test
-// ||z_k|| <= max(rtol ||z_0||, atol) (solver.cpp:71-77).
+// the device; one CG iteration (p = z + beta p, w = A p with p.w, x/r update, V-cycle, r.z and
+// z.z) is a single CUDA-graph launch, after which the host reads {pw, ||z||, flags} for the
+// stopping test ||z_k|| <= max(rtol ||z_0||, atol) (solver.cpp:71-77).
+void Solver::cg_dots(int op) {
+  const Dist& D = *nodes[0].dist;
+  CK(cudaMemsetAsync(rank_sums, 0, sizeof(double) * 2 * W.R, W.stream));
+  if (!parity_build())
+    for (size_t q = 0; q < D.local.size(); ++q)
+      W.cnt.launches += launch_dot2(D.geo[q], cr.p[q], cz.p[q], cz.p[q], part + part_off[q],
+                                    part + part_off[q] + nblk_max, W.stream);
+  reduce_local(D, 2, &cr, &cz, &cz);
+  device_allreduce_ranksums(2);
+  W.cnt.launches += launch_cg_scalars(op, rank_sums, W.R, ranks_dev, D.h.n_ranks(), scal, W.stream);
+}
+
+void Solver::cg_iteration() {
+  Node& top = nodes[0];
+  const Dist& D = *top.dist;
+  const size_t nb = D.local.size();
+  for (size_t q = 0; q < nb; ++q) W.cnt.launches += launch_p_update(D.geo[q], cz.p[q], cp.p[q], scal, S_BETA, W.stream);
+  halo(0, cp);
+  CK(cudaMemsetAsync(rank_sums, 0, sizeof(double) * 2 * W.R, W.stream));
+  for (size_t q = 0; q < nb; ++q)
+    W.cnt.launches += launch_spmv_dot(D.geo[q], top.op[q], cp.p[q], cw.p[q], part + part_off[q], W.stream);
+  reduce_local(D, 1, &cp, &cw, nullptr);
+  device_allreduce_ranksums(1);
+  W.cnt.launches += launch_cg_scalars(CG_ALPHA, rank_sums, W.R, ranks_dev, D.h.n_ranks(), scal, W.stream);
+  for (size_t q = 0; q < nb; ++q)
+    W.cnt.launches += launch_cg_update(D.geo[q], cp.p[q], cw.p[q], cx.p[q], cr.p[q], scal, S_ALPHA, S_FLAG_PW,
+                                       W.stream);
+  vcycle(0);
+  cg_dots(CG_BETA);
+  CK(cudaMemcpyAsync(host_scal, scal, sizeof(double) * S_NSLOTS, cudaMemcpyDeviceToHost, W.stream));
+}
+
+void Solver::run_iteration() {
+  if (!use_graphs) {
+    cg_iteration();
+    return;
+  }
+  if (!iter_exec) {
+    const long long l0 = W.cnt.launches;
+    cudaGraph_t g;
+    CK(cudaStreamBeginCapture(W.stream, cudaStreamCaptureModeThreadLocal));
+    cg_iteration();
+    CK(cudaStreamEndCapture(W.stream, &g));
+    CK(cudaGraphInstantiate(&iter_exec, g, 0));
+    CK(cudaGraphDestroy(g));
+    iter_launches = W.cnt.launches - l0;
+    W.cnt.launches = l0;
+  }
+  CK(cudaGraphLaunch(iter_exec, W.stream));
+  W.cnt.launches += iter_launches;
+}
+
+Solver::~Solver() {
+  if (iter_exec) cudaGraphExecDestroy(iter_exec);
+  if (host_scal) cudaFreeHost(host_scal);
+}
+
 int Solver::solve(const double* b, double* x, bool on_device, int method, double rtol, double atol, int max_its,
                   double* hist, int* reason, int* its, double* norm0, double* normf, double* t_ms, bool seeded,
                   unsigned long long seed) {
@@ -833,9 +909,6 @@ int Solver::solve(const double* b, double* x, bool on_device, int method, double
   Node& top = nodes[0];
   const Dist& D = *top.dist;
   const size_t nb = D.local.size();
-  Field saved_b = top.b, saved_x = top.x;
-  top.b = cr;
-  top.x = cz;
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
@@ -848,97 +921,60 @@ int Solver::solve(const double* b, double* x, bool on_device, int method, double
   } else {
     upload(0, cw, b, on_device);
   }
+  int rc = 0;
   if (method == 5) {  // preonly: x = M b
     for (size_t q = 0; q < nb; ++q) W.cnt.launches += launch_copy_interior(D.geo[q], cw.p[q], cr.p[q], W.stream);
     vcycle(0);
     if (x) download(0, cz, x, on_device);
-    CK(cudaEventRecord(e1, W.stream));
-    CK(cudaEventSynchronize(e1));
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, e0, e1);
-    *t_ms = ms;
     *reason = 3;
     *its = 1;
-    top.b = saved_b;
-    top.x = saved_x;
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    return 0;
-  }
-  if (x && !seeded)
-    upload(0, cx, x, on_device);
-  else
-    for (size_t q = 0; q < nb; ++q) CK(cudaMemsetAsync(cx.p[q], 0, sizeof(double) * D.geo[q].total, W.stream));
-  halo(0, cx);
-  for (size_t q = 0; q < nb; ++q)
-    W.cnt.launches += launch_residual(D.geo[q], top.op[q], cw.p[q], cx.p[q], cr.p[q], W.stream);
-  vcycle(0);
-  auto dots = [&](int op) {
-    CK(cudaMemsetAsync(rank_sums, 0, sizeof(double) * 2 * W.R, W.stream));
-    for (size_t q = 0; q < nb; ++q) {
-      W.cnt.launches += launch_dot2(D.geo[q], cr.p[q], cz.p[q], cz.p[q], part + part_off[q],
-                                    part + part_off[q] + nblk_max, W.stream);
-      W.cnt.launches += launch_reduce_partials(part + part_off[q], grid_blocks(D.geo[q]), 2, nblk_max,
-                                               rank_sums + D.wr[D.local[q]], W.R, W.stream);
-    }
-    device_allreduce_ranksums(2);
-    W.cnt.launches += launch_cg_scalars(op, rank_sums, W.R, ranks_dev, D.h.n_ranks(), scal, W.stream);
-  };
-  dots(CG_INIT);
-  CK(cudaMemcpyAsync(host_scal, scal, sizeof(double) * S_NSLOTS, cudaMemcpyDeviceToHost, W.stream));
-  CK(cudaStreamSynchronize(W.stream));
-  const double nrm0 = host_scal[S_NRM];
-  *norm0 = nrm0;
-  *normf = nrm0;
-  if (hist) hist[0] = nrm0;
-  const double tol = std::max(rtol * nrm0, atol);
-  int rc = 0;
-  if (nrm0 <= tol) {
-    *reason = nrm0 <= atol ? 1 : 0;
+    *norm0 = *normf = 0.0;
   } else {
-    for (size_t q = 0; q < nb; ++q) W.cnt.launches += launch_copy_interior(D.geo[q], cz.p[q], cp.p[q], W.stream);
-    *reason = 2;
-    for (int it = 1; it <= max_its; ++it) {
-      halo(0, cp);
-      CK(cudaMemsetAsync(rank_sums, 0, sizeof(double) * 2 * W.R, W.stream));
-      for (size_t q = 0; q < nb; ++q) {
-        W.cnt.launches += launch_spmv_dot(D.geo[q], top.op[q], cp.p[q], cw.p[q], part + part_off[q], W.stream);
-        W.cnt.launches += launch_reduce_partials(part + part_off[q], grid_blocks(D.geo[q]), 1, nblk_max,
-                                                 rank_sums + D.wr[D.local[q]], W.R, W.stream);
+    if (x && !seeded)
+      upload(0, cx, x, on_device);
+    else
+      for (size_t q = 0; q < nb; ++q) CK(cudaMemsetAsync(cx.p[q], 0, sizeof(double) * D.geo[q].total, W.stream));
+    halo(0, cx);
+    for (size_t q = 0; q < nb; ++q)
+      W.cnt.launches += launch_residual(D.geo[q], top.op[q], cw.p[q], cx.p[q], cr.p[q], W.stream);
+    vcycle(0);
+    cg_dots(CG_INIT);  // also sets beta = 0 so that the first p = z + 0 p = z
+    CK(cudaMemcpyAsync(host_scal, scal, sizeof(double) * S_NSLOTS, cudaMemcpyDeviceToHost, W.stream));
+    CK(cudaStreamSynchronize(W.stream));
+    const double nrm0 = host_scal[S_NRM];
+    *norm0 = nrm0;
+    *normf = nrm0;
+    if (hist) hist[0] = nrm0;
+    const double tol = std::max(rtol * nrm0, atol);
+    if (nrm0 <= tol) {
+      *reason = nrm0 <= atol ? 1 : 0;
+    } else {
+      for (size_t q = 0; q < nb; ++q) CK(cudaMemsetAsync(cp.p[q], 0, sizeof(double) * D.geo[q].total, W.stream));
+      for (int it = 1; it <= max_its; ++it) {
+        run_iteration();
+        CK(cudaStreamSynchronize(W.stream));
+        if (host_scal[S_FLAG_PW] != 0.0) {  // solver.cpp:237-241 (x, r not updated)
+          *reason = 4;
+          rc = 2;
+          break;
+        }
+        const double nrm = host_scal[S_NRM];
+        *its = it;
+        *normf = nrm;
+        if (hist) hist[it] = nrm;
+        if (nrm <= tol) {
+          *reason = nrm <= atol ? 1 : 0;
+          break;
+        }
+        if (host_scal[S_FLAG_RZ] != 0.0) {  // solver.cpp:254-258
+          *reason = 4;
+          rc = 2;
+          break;
+        }
       }
-      device_allreduce_ranksums(1);
-      W.cnt.launches += launch_cg_scalars(CG_ALPHA, rank_sums, W.R, ranks_dev, D.h.n_ranks(), scal, W.stream);
-      for (size_t q = 0; q < nb; ++q)
-        W.cnt.launches += launch_cg_update(D.geo[q], cp.p[q], cw.p[q], cx.p[q], cr.p[q], scal, S_ALPHA, S_FLAG_PW,
-                                           W.stream);
-      vcycle(0);
-      dots(CG_BETA);
-      CK(cudaMemcpyAsync(host_scal, scal, sizeof(double) * S_NSLOTS, cudaMemcpyDeviceToHost, W.stream));
-      CK(cudaStreamSynchronize(W.stream));
-      if (host_scal[S_FLAG_PW] != 0.0) {
-        *reason = 4;
-        rc = 2;
-        break;
-      }
-      const double nrm = host_scal[S_NRM];
-      *its = it;
-      *normf = nrm;
-      if (hist) hist[it] = nrm;
-      if (nrm <= tol) {
-        *reason = nrm <= atol ? 1 : 0;
-        break;
-      }
-      if (host_scal[S_FLAG_RZ] != 0.0) {
-        *reason = 4;
-        rc = 2;
-        break;
-      }
-      for (size_t q = 0; q < nb; ++q)
-        W.cnt.launches += launch_p_update(D.geo[q], cz.p[q], cp.p[q], scal, S_BETA, W.stream);
     }
-    if (*reason == 2) rc = 0;
+    if (x) download(0, cx, x, on_device);
   }
-  if (x) download(0, cx, x, on_device);
   CK(cudaEventRecord(e1, W.stream));
   CK(cudaEventSynchronize(e1));
   float ms = 0.f;
@@ -946,8 +982,6 @@ int Solver::solve(const double* b, double* x, bool on_device, int method, double
   *t_ms = ms;
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
-  top.b = saved_b;
-  top.x = saved_x;
   CK(cudaGetLastError());
   return rc;
 }

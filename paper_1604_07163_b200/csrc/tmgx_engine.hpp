@@ -152,7 +152,9 @@ struct Node {
 class Solver {
  public:
   Solver(World& W, const ProblemDesc& P, const MGDesc& M);
-  ~Solver() = default;
+  ~Solver();
+  Solver(const Solver&) = delete;
+  Solver& operator=(const Solver&) = delete;
 
   World& W;
   ProblemDesc prob;
@@ -187,7 +189,8 @@ class Solver {
   void estimate(int i, int mode);
 
   // collectives: per-box partials -> deterministic rank-ordered sums over dist (host)
-  std::array<double, 2> collect2(int i, int nslots);
+  std::array<double, 2> collect2(int i, int nslots, const Field* a, const Field* b);
+  void reduce_local(const Dist& D, int nslots, const Field* a, const Field* b, const Field* c);
   void device_allreduce_ranksums(int nslots);
 
   // compact (host or device) <-> field
@@ -197,6 +200,14 @@ class Solver {
   int solve(const double* b, double* x, bool on_device, int method, double rtol, double atol, int max_its,
             double* hist, int* reason, int* its, double* norm0, double* normf, double* t_ms, bool seeded,
             unsigned long long seed);
+
+  // CG iteration as one CUDA graph (TMGX_GRAPHS=0 disables capture)
+  bool use_graphs = true;
+  cudaGraphExec_t iter_exec = nullptr;
+  long long iter_launches = 0;
+  void cg_dots(int op);
+  void cg_iteration();
+  void run_iteration();
 
  private:
   void build_nodes();

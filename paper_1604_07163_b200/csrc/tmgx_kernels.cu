@@ -133,7 +133,7 @@ __device__ __forceinline__ int blk_linear() {
 }
 
 dim3 tile_grid(const BoxGeo& g) {
-  return dim3((g.ex + kBX - 1) / kBX, (g.ey + kBY - 1) / kBY, (g.ez + kZC - 1) / kZC);
+  return dim3((g.ex + kBX - 1) / kBX, (g.ey + kBY - 1) / kBY, (g.ez + g.zc - 1) / g.zc);
 }
 const dim3 kBlock(kBX, kBY, 1);
 
@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(kBX* kBY) k_cheb_start_zero(BoxGeo g, OpParams
                                                                double* __restrict__ out, double s_theta) {
   const int i = blockIdx.x * kBX + threadIdx.x, j = blockIdx.y * kBY + threadIdx.y;
   if (i >= g.ex || j >= g.ey) return;
-  const int k0 = blockIdx.z * kZC, k1 = min(k0 + kZC, g.ez);
+  const int k0 = blockIdx.z * g.zc, k1 = min(k0 + g.zc, g.ez);
   for (int k = k0; k < k1; ++k) {
     const long long v = vidx(g, i, j, k);
     const Pt p = make_pt(g, i, j, k);
@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(kBX* kBY)
                      double* __restrict__ r, double* __restrict__ d, double s_theta) {
   const int i = blockIdx.x * kBX + threadIdx.x, j = blockIdx.y * kBY + threadIdx.y;
   if (i >= g.ex || j >= g.ey) return;
-  const int k0 = blockIdx.z * kZC, k1 = min(k0 + kZC, g.ez);
+  const int k0 = blockIdx.z * g.zc, k1 = min(k0 + g.zc, g.ez);
   long long v = vidx(g, i, j, k0);
   ZQ u{__ldg(x + v - g.pxy), __ldg(x + v), 0.0};
   ZQ kq{0.0, 0.0, 0.0};
@@ -263,7 +263,7 @@ __global__ void __launch_bounds__(kBX* kBY)
                 double* __restrict__ d_new, double* r_out, double* x_out, ChebStep cs, int last) {
   const int i = blockIdx.x * kBX + threadIdx.x, j = blockIdx.y * kBY + threadIdx.y;
   if (i >= g.ex || j >= g.ey) return;
-  const int k0 = blockIdx.z * kZC, k1 = min(k0 + kZC, g.ez);
+  const int k0 = blockIdx.z * g.zc, k1 = min(k0 + g.zc, g.ez);
   long long v = vidx(g, i, j, k0);
   ZQ u{__ldg(d + v - g.pxy), __ldg(d + v), 0.0};
   ZQ kq{0.0, 0.0, 0.0};
@@ -303,7 +303,7 @@ __global__ void __launch_bounds__(kBX* kBY)
             double* __restrict__ y) {
   const int i = blockIdx.x * kBX + threadIdx.x, j = blockIdx.y * kBY + threadIdx.y;
   if (i >= g.ex || j >= g.ey) return;
-  const int k0 = blockIdx.z * kZC, k1 = min(k0 + kZC, g.ez);
+  const int k0 = blockIdx.z * g.zc, k1 = min(k0 + g.zc, g.ez);
   long long v = vidx(g, i, j, k0);
   ZQ u{__ldg(x + v - g.pxy), __ldg(x + v), 0.0};
   ZQ kq{0.0, 0.0, 0.0};
@@ -336,7 +336,7 @@ __global__ void __launch_bounds__(kBX* kBY)
   const int i = blockIdx.x * kBX + threadIdx.x, j = blockIdx.y * kBY + threadIdx.y;
   double acc = 0.0;
   if (i < g.ex && j < g.ey) {
-    const int k0 = blockIdx.z * kZC, k1 = min(k0 + kZC, g.ez);
+    const int k0 = blockIdx.z * g.zc, k1 = min(k0 + g.zc, g.ez);
     long long v = vidx(g, i, j, k0);
     ZQ u{__ldg(x + v - g.pxy), __ldg(x + v), 0.0};
     ZQ kq{0.0, 0.0, 0.0};
@@ -372,7 +372,7 @@ __global__ void __launch_bounds__(kBX* kBY)
   const int i = blockIdx.x * kBX + threadIdx.x, j = blockIdx.y * kBY + threadIdx.y;
   double acc = 0.0;
   if (i < g.ex && j < g.ey) {
-    const int k0 = blockIdx.z * kZC, k1 = min(k0 + kZC, g.ez);
+    const int k0 = blockIdx.z * g.zc, k1 = min(k0 + g.zc, g.ez);
     for (int k = k0; k < k1; ++k) {
       const long long v = vidx(g, i, j, k);
       double invd = op.cinvd;
@@ -398,7 +398,7 @@ __global__ void __launch_bounds__(kBX* kBY)
   const int i = blockIdx.x * kBX + threadIdx.x, j = blockIdx.y * kBY + threadIdx.y;
   double s1 = 0.0, s2 = 0.0;
   if (i < g.ex && j < g.ey) {
-    const int k0 = blockIdx.z * kZC, k1 = min(k0 + kZC, g.ez);
+    const int k0 = blockIdx.z * g.zc, k1 = min(k0 + g.zc, g.ez);
     for (int k = k0; k < k1; ++k) {
       const long long v = vidx(g, i, j, k);
       s1 += a[v] * b[v];
@@ -421,7 +421,7 @@ __global__ void __launch_bounds__(kBX* kBY)
   const double alpha = scal[as];
   const int i = blockIdx.x * kBX + threadIdx.x, j = blockIdx.y * kBY + threadIdx.y;
   if (i >= g.ex || j >= g.ey) return;
-  const int k0 = blockIdx.z * kZC, k1 = min(k0 + kZC, g.ez);
+  const int k0 = blockIdx.z * g.zc, k1 = min(k0 + g.zc, g.ez);
   for (int k = k0; k < k1; ++k) {
     const long long v = vidx(g, i, j, k);
     x[v] += alpha * p[v];
@@ -435,7 +435,7 @@ __global__ void __launch_bounds__(kBX* kBY)
   const double beta = scal[bs];
   const int i = blockIdx.x * kBX + threadIdx.x, j = blockIdx.y * kBY + threadIdx.y;
   if (i >= g.ex || j >= g.ey) return;
-  const int k0 = blockIdx.z * kZC, k1 = min(k0 + kZC, g.ez);
+  const int k0 = blockIdx.z * g.zc, k1 = min(k0 + g.zc, g.ez);
   for (int k = k0; k < k1; ++k) {
     const long long v = vidx(g, i, j, k);
     p[v] = z[v] + beta * p[v];
@@ -446,7 +446,7 @@ __global__ void __launch_bounds__(kBX* kBY)
     k_axpy(BoxGeo g, double alpha, const double* __restrict__ x, double* __restrict__ y, int copy) {
   const int i = blockIdx.x * kBX + threadIdx.x, j = blockIdx.y * kBY + threadIdx.y;
   if (i >= g.ex || j >= g.ey) return;
-  const int k0 = blockIdx.z * kZC, k1 = min(k0 + kZC, g.ez);
+  const int k0 = blockIdx.z * g.zc, k1 = min(k0 + g.zc, g.ez);
   for (int k = k0; k < k1; ++k) {
     const long long v = vidx(g, i, j, k);
     if (copy)
@@ -501,24 +501,18 @@ __global__ void k_prolong_add(BoxGeo F, BoxGeo Cg, const double* __restrict__ xc
   const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y * blockDim.y + threadIdx.y;
   const int k = blockIdx.z;
   if (i >= F.ex || j >= F.ey) return;
-  const int f[3] = {F.gx + i, F.gy + j, F.gz + k};
-  int at[3][2], cnt[3];
-  double w[3][2];
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    if ((f[a] & 1) == 0) {
-      at[a][0] = f[a] >> 1; at[a][1] = at[a][0]; w[a][0] = 1.0; w[a][1] = 0.0; cnt[a] = 1;
-    } else {
-      at[a][0] = (f[a] - 1) >> 1; at[a][1] = (f[a] + 1) >> 1; w[a][0] = 0.5; w[a][1] = 0.5; cnt[a] = 2;
-    }
-  }
+  const int fx = F.gx + i, fy = F.gy + j, fz = F.gz + k;
+  // per axis: coincident vertex (one coarse column, weight 1) or midpoint (two, 1/2 each)
+  const int nx = 1 + (fx & 1), ny = 1 + (fy & 1), nz = 1 + (fz & 1);
+  const int cx0 = (fx >> 1) - Cg.gx, cy0 = (fy >> 1) - Cg.gy, cz0 = (fz >> 1) - Cg.gz;
+  const double wx = nx == 2 ? 0.5 : 1.0, wy = ny == 2 ? 0.5 : 1.0, wz = nz == 2 ? 0.5 : 1.0;
   double acc = 0.0;
-  for (int tz = 0; tz < cnt[2]; ++tz)
-    for (int ty = 0; ty < cnt[1]; ++ty) {
-      const long long row = vidx(Cg, 0, at[1][ty] - Cg.gy, at[2][tz] - Cg.gz);
-      for (int tx = 0; tx < cnt[0]; ++tx) {
-        const double ww = w[0][tx] * w[1][ty] * w[2][tz];
-        acc += ww * __ldg(xc + row + (at[0][tx] - Cg.gx));
+  for (int tz = 0; tz < nz; ++tz)
+    for (int ty = 0; ty < ny; ++ty) {
+      const double* row = xc + vidx(Cg, cx0, cy0 + ty, cz0 + tz);
+      for (int tx = 0; tx < nx; ++tx) {
+        const double ww = wx * wy * wz;  // grid.cpp:421 (aw0 * aw1 * aw2)
+        acc += ww * __ldg(row + tx);
       }
     }
   const long long v = vidx(F, i, j, k);
@@ -540,6 +534,27 @@ __global__ void k_reduce_partials(const double* __restrict__ part, int nblk, lon
   if (threadIdx.x == 0) out[slot * out_stride] = s;
 }
 
+// Parity build: dist_vector.cpp:33-38 + comm.cpp:338-351 on one rank is a serial left fold of
+// the products in local (natural) order; one thread reproduces it exactly.
+__global__ void k_fold_dot(BoxGeo g, const double* __restrict__ a, const double* __restrict__ b,
+                           const double* __restrict__ c, double* __restrict__ out, long long out_stride) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double s0 = 0.0, s1 = 0.0;
+  for (int k = 0; k < g.ez; ++k)
+    for (int j = 0; j < g.ey; ++j)
+      for (int i = 0; i < g.ex; ++i) {
+        const long long v = vidx(g, i, j, k);
+        const double p = a[v] * b[v];
+        s0 += p;
+        if (c) {
+          const double q = c[v] * c[v];
+          s1 += q;
+        }
+      }
+  out[0] = s0;
+  if (c) out[out_stride] = s1;
+}
+
 __global__ void k_cg_scalars(int op, const double* __restrict__ rs, int R, const int* __restrict__ ranks, int nr,
                              double* __restrict__ scal) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
@@ -554,6 +569,7 @@ __global__ void k_cg_scalars(int op, const double* __restrict__ rs, int R, const
     scal[S_NRM] = sqrt(s1);
     scal[S_FLAG_PW] = 0.0;
     scal[S_FLAG_RZ] = 0.0;
+    scal[S_BETA] = 0.0;  // first iteration: p = z + 0 p (p zeroed) == p = z
   } else if (op == CG_ALPHA) {  // pw ; alpha = rz/pw (solver.cpp:236-242)
     scal[S_PW] = s0;
     const bool bad = s0 <= 0.0 || !isfinite(s0);
@@ -788,6 +804,12 @@ int launch_zero(double* p, long long n, cudaStream_t s) {
 int launch_reduce_partials(const double* part, int nblk, int nslots, long long slot_stride, double* out,
                            long long out_stride, cudaStream_t s) {
   k_reduce_partials<<<nslots, 512, 0, s>>>(part, nblk, slot_stride, out, out_stride);
+  return 1;
+}
+
+int launch_fold_dot(const BoxGeo& g, const double* a, const double* b, const double* c, double* out,
+                    long long out_stride, cudaStream_t s) {
+  k_fold_dot<<<1, 32, 0, s>>>(g, a, b, c, out, out_stride);
   return 1;
 }
 

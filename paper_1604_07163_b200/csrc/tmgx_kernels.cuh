@@ -23,8 +23,19 @@ struct BoxGeo {
   int ex, ey, ez;  // extents
   int gx, gy, gz;  // global lower corner
   int Nx, Ny, Nz;  // global grid
+  int zc;          // z planes marched per block (kZC on large boxes, fewer on coarse levels)
   long long px, pxy, base, total;
 };
+
+// z-chunk so that a level launches >= kMinBlocks blocks: large boxes stream 16 planes per
+// block (register queue reuse), coarse boxes trade reuse for parallelism (latency-bound).
+constexpr int kMinBlocks = 8 * 148;
+inline int choose_zc(int ex, int ey, int ez) {
+  const int bxy = ((ex + kBX - 1) / kBX) * ((ey + kBY - 1) / kBY);
+  for (int zc = kZC; zc > 1; zc >>= 1)
+    if ((long long)bxy * ((ez + zc - 1) / zc) >= kMinBlocks) return zc;
+  return 1;
+}
 
 // Operator parameters for the 7-point FD operator of one level.
 struct OpParams {
@@ -97,6 +108,11 @@ int launch_zero(double* p, long long n, cudaStream_t s);
 // Sum `nblk` partials of each of `nslots` slots (stride `slot_stride`) into out[slot*out_stride].
 int launch_reduce_partials(const double* part, int nblk, int nslots, long long slot_stride, double* out,
                            long long out_stride, cudaStream_t s);
+
+// Parity build only: serial left fold of a.b (and c.c when c != null) in local order into
+// out[0] (and out[out_stride]) -- the reference's ordered_fold_sum on one rank.
+int launch_fold_dot(const BoxGeo& g, const double* a, const double* b, const double* c, double* out,
+                    long long out_stride, cudaStream_t s);
 
 // Scalar finalisation. rank_sums[slot*R + rank]; sums over the listed ranks in order.
 enum ScalSlot {
