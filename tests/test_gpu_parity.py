@@ -177,7 +177,10 @@ def test_mgcg_golden(parity, np3, nl, m, est, its, xnorm):
     # amplifies reduction-order rounding; the solution bar stays 1e-9 for the fixed estimator
     tol = TOL_SOLUTION if est == T.EST_LANCZOS else 1e-8
     assert rel(x, xo) < tol
-    np.testing.assert_allclose(rep.residual_history, orep["history"], rtol=1e-6 if est == T.EST_LANCZOS else 1e-3)
+    if est == T.EST_LANCZOS:
+        np.testing.assert_allclose(rep.residual_history, orep["history"], rtol=1e-6)
+    else:  # late residuals of the badly smoothed run oscillate around 1e-10: compare vs ||z0||
+        np.testing.assert_allclose(rep.residual_history, orep["history"], rtol=0, atol=1e-5 * orep["history"][0])
 
 
 @pytest.mark.parametrize("parity", [True, False])

@@ -142,6 +142,71 @@ __global__ void __launch_bounds__(BX* BY) kS(G g, const double* __restrict__ d, 
   }
 }
 
+// P: like A but with an explicit one-plane software prefetch of the streamed operands
+template <int BX, int BY, int ZC>
+__global__ void __launch_bounds__(BX* BY) kP(G g, const double* __restrict__ d, const double* __restrict__ r,
+                                             double* __restrict__ x, double c1, double c2, double dg, double a,
+                                             double invd) {
+  const int i = blockIdx.x * BX + threadIdx.x, j = blockIdx.y * BY + threadIdx.y;
+  if (i >= g.ex || j >= g.ey) return;
+  const int k0 = blockIdx.z * ZC, k1 = min(k0 + ZC, g.ez);
+  long long v = g.base + i + g.px * j + g.pxy * k0;
+  double um = __ldg(d + v - g.pxy), uc = __ldg(d + v), un = __ldg(d + v + g.pxy);
+  double rc = __ldg(r + v), xc = x[v];
+  for (int k = k0; k < k1; ++k, v += g.pxy) {
+    double unn = 0, rn = 0, xn = 0;
+    if (k + 1 < k1) {
+      unn = __ldg(d + v + 2 * g.pxy);
+      rn = __ldg(r + v + g.pxy);
+      xn = x[v + g.pxy];
+    }
+    const double ax = row(g, i, j, k, uc, um, __ldg(d + v - g.px), __ldg(d + v - 1), __ldg(d + v + 1),
+                          __ldg(d + v + g.px), un, dg, a);
+    const double r1 = rc - ax;
+    const double dn = c1 * uc + c2 * (r1 * invd);
+    x[v] = (xc + uc) + dn;
+    um = uc;
+    uc = un;
+    un = unn;
+    rc = rn;
+    xc = xn;
+  }
+}
+
+// V: two x-points per thread with 16-byte loads (pairs (2t, 2t+1) are 16-byte aligned)
+template <int BX, int BY, int ZC>
+__global__ void __launch_bounds__(BX* BY) kV(G g, const double* __restrict__ d, const double* __restrict__ r,
+                                             double* __restrict__ x, double c1, double c2, double dg, double a,
+                                             double invd) {
+  const int i0 = 2 * (blockIdx.x * BX + threadIdx.x), j = blockIdx.y * BY + threadIdx.y;
+  if (i0 >= g.ex || j >= g.ey) return;
+  const bool two = i0 + 1 < g.ex;
+  const int k0 = blockIdx.z * ZC, k1 = min(k0 + ZC, g.ez);
+  long long v = g.base + i0 + g.px * j + g.pxy * k0;
+  auto ld2 = [](const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); };
+  double2 um = ld2(d + v - g.pxy), uc = ld2(d + v);
+  for (int k = k0; k < k1; ++k, v += g.pxy) {
+    const double2 un = ld2(d + v + g.pxy);
+    const double2 ym = ld2(d + v - g.px), yp = ld2(d + v + g.px);
+    const double xl = __ldg(d + v - 1), xr = __ldg(d + v + 2);
+    const double2 rr = ld2(r + v);
+    double2 xx = *reinterpret_cast<const double2*>(x + v);
+    const double a0 = row(g, i0, j, k, uc.x, um.x, ym.x, xl, uc.y, yp.x, un.x, dg, a);
+    const double r0 = rr.x - a0;
+    xx.x = (xx.x + uc.x) + (c1 * uc.x + c2 * (r0 * invd));
+    if (two) {
+      const double a1 = row(g, i0 + 1, j, k, uc.y, um.y, ym.y, uc.x, xr, yp.y, un.y, dg, a);
+      const double r1 = rr.y - a1;
+      xx.y = (xx.y + uc.y) + (c1 * uc.y + c2 * (r1 * invd));
+      *reinterpret_cast<double2*>(x + v) = xx;
+    } else {
+      x[v] = xx.x;
+    }
+    um = uc;
+    uc = un;
+  }
+}
+
 // C: pure copy-ish streaming reference: x = x + d + r (reads 3, writes 1 = 32 B/pt)
 __global__ void kC(G g, const double* __restrict__ d, const double* __restrict__ r, double* __restrict__ x,
                    long long n) {
@@ -223,6 +288,24 @@ int main(int argc, char** argv) {
   RUN_S(32, 4, 16);
   RUN_S(32, 8, 16);
   RUN_S(64, 4, 32);
+#define RUN_P(BX, BY, ZC)                                                                                    \
+  timeit("P prefetch " #BX "x" #BY " zc" #ZC, [&] {                                                          \
+    kP<BX, BY, ZC><<<dim3((N + BX - 1) / BX, (N + BY - 1) / BY, (N + ZC - 1) / ZC), dim3(BX, BY)>>>(          \
+        g, d, r, x, c1, c2, dg, a, invd);                                                                    \
+  })
+  RUN_P(32, 4, 8);
+  RUN_P(32, 4, 16);
+  RUN_P(32, 8, 16);
+#define RUN_V(BX, BY, ZC)                                                                                    \
+  timeit("V dbl2 " #BX "x" #BY " zc" #ZC, [&] {                                                              \
+    kV<BX, BY, ZC><<<dim3((N + 2 * BX - 1) / (2 * BX), (N + BY - 1) / BY, (N + ZC - 1) / ZC), dim3(BX, BY)>>>( \
+        g, d, r, x, c1, c2, dg, a, invd);                                                                    \
+  })
+  RUN_V(32, 4, 8);
+  RUN_V(32, 4, 16);
+  RUN_V(32, 8, 8);
+  RUN_V(16, 8, 8);
+  RUN_V(64, 2, 8);
   timeit("C streaming 3r1w", [&] { kC<<<148 * 8, 512>>>(g, d, r, x, total - 16); });
   return 0;
 }
