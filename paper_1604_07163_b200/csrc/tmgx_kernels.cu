@@ -132,17 +132,29 @@ __device__ __forceinline__ int blk_linear() {
   return blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
 }
 
+// Tiles: 32x4 threads, each thread owns the vertex pair (i0, i0+1), i0 = 2*(32*bx + tx), so a
+// warp covers 64 consecutive x-vertices with 16-byte loads/stores (pairs are 16-byte aligned
+// because base and px are multiples of 4 doubles). Each block marches g.zc z-planes.
 dim3 tile_grid(const BoxGeo& g) {
-  return dim3((g.ex + kBX - 1) / kBX, (g.ey + kBY - 1) / kBY, (g.ez + g.zc - 1) / g.zc);
+  return dim3((g.ex + 2 * kBX - 1) / (2 * kBX), (g.ey + kBY - 1) / kBY, (g.ez + g.zc - 1) / g.zc);
 }
 const dim3 kBlock(kBX, kBY, 1);
 
-// Loads the 7-point neighbourhood of a field around vertex v with a z queue.
-#define TMGX_NB(u, q, v)                                   \
-  const double u##xm = __ldg((u) + (v) - 1);               \
-  const double u##xp = __ldg((u) + (v) + 1);               \
-  const double u##ym = __ldg((u) + (v) - g.px);            \
-  const double u##yp = __ldg((u) + (v) + g.px);
+__device__ __forceinline__ double2 ld2(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
+__device__ __forceinline__ double2 ld2rw(const double* p) { return *reinterpret_cast<const double2*>(p); }
+__device__ __forceinline__ double get(const double2& a, int q) { return q ? a.y : a.x; }
+__device__ __forceinline__ void set(double2& a, int q, double v) {
+  if (q)
+    a.y = v;
+  else
+    a.x = v;
+}
+__device__ __forceinline__ void st2(double* p, const double2& v, bool two) {
+  if (two)
+    *reinterpret_cast<double2*>(p) = v;
+  else
+    *p = v.x;
+}
 
 // ------------------------------------------------------------------------------------------
 // coefficient and right-hand-side generators
@@ -201,192 +213,248 @@ __global__ void k_fill_rhs(BoxGeo g, double* __restrict__ b, unsigned long long 
 }
 
 // ------------------------------------------------------------------------------------------
-// Chebyshev smoother kernels
+// Generic stencil pass: z-march over a tile of vertex pairs with a register queue for the
+// stencil operand u (and k), one-plane software prefetch of u and of the functor's streamed
+// operands, and the per-vertex row evaluated exactly as the reference's CSR row loop. The
+// functor F supplies the streamed inputs (load), the per-vertex update (point), the stores,
+// and optionally two dot-product partials (block-reduced at the end).
+// ------------------------------------------------------------------------------------------
+
+template <bool VAR, class F>
+__global__ void __launch_bounds__(kBX* kBY)
+    k_march(BoxGeo g, OpParams op, const double* __restrict__ u, F f) {
+  __shared__ double sh[32];
+  const int i0 = 2 * (blockIdx.x * kBX + threadIdx.x), j = blockIdx.y * kBY + threadIdx.y;
+  double acc0 = 0.0, acc1 = 0.0;
+  if (i0 < g.ex && j < g.ey) {
+    const bool two = i0 + 1 < g.ex;
+    const int k0 = blockIdx.z * g.zc, k1 = min(k0 + g.zc, g.ez);
+    long long v = vidx(g, i0, j, k0);
+    double2 um = ld2(u + v - g.pxy), uc = ld2(u + v), un = ld2(u + v + g.pxy);
+    double2 km{1.0, 1.0}, kc{1.0, 1.0}, kn{1.0, 1.0};
+    if (VAR) {
+      km = ld2(op.k + v - g.pxy);
+      kc = ld2(op.k + v);
+      kn = ld2(op.k + v + g.pxy);
+    }
+    typename F::In in = f.load(v);
+    for (int k = k0; k < k1; ++k, v += g.pxy) {
+      double2 unn{0.0, 0.0}, knn{1.0, 1.0};
+      typename F::In inn{};
+      if (k + 1 < k1) {  // prefetch the next plane
+        unn = ld2(u + v + 2 * g.pxy);
+        if (VAR) knn = ld2(op.k + v + 2 * g.pxy);
+        inn = f.load(v + g.pxy);
+      }
+      const double2 uym = ld2(u + v - g.px), uyp = ld2(u + v + g.px);
+      const double uxl = __ldg(u + v - 1), uxr = __ldg(u + v + 2);
+      double2 kym{1.0, 1.0}, kyp{1.0, 1.0};
+      double kxl = 1.0, kxr = 1.0;
+      if (VAR) {
+        kym = ld2(op.k + v - g.px);
+        kyp = ld2(op.k + v + g.px);
+        kxl = __ldg(op.k + v - 1);
+        kxr = __ldg(op.k + v + 2);
+      }
+      typename F::Out out{};
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        if (q == 1 && !two) break;
+        const Pt p = make_pt(g, i0 + q, j, k);
+        const double kxm = q ? kc.x : kxl, kxp = q ? kxr : kc.y;
+        const Coef c = coef_at<VAR>(op, p, get(kc, q), kxm, kxp, get(kym, q), get(kyp, q), get(km, q), get(kn, q));
+        const double uxm = q ? uc.x : uxl, uxp = q ? uxr : uc.y;
+        const double au = row_apply(p, c, get(um, q), get(uym, q), uxm, get(uc, q), uxp, get(uyp, q), get(un, q));
+        f.point(q, au, c.invd, get(uc, q), in, out, acc0, acc1);
+      }
+      f.store(v, out, two);
+      um = uc;
+      uc = un;
+      un = unn;
+      if (VAR) {
+        km = kc;
+        kc = kn;
+        kn = knn;
+      }
+      in = inn;
+    }
+  }
+  if (F::kDots) {
+    const double s0 = block_sum(acc0, sh);
+    const double s1 = F::kDots > 1 ? block_sum(acc1, sh) : 0.0;
+    if (threadIdx.x == 0 && threadIdx.y == 0) f.partials(blk_linear(), s0, s1);
+  }
+}
+
+struct NoIn {};
+
+// y = A u  (MODE 0) or  y = b - A u  (MODE 1)     (spmv dist_matrix.cpp:182-224; residual)
+template <int MODE>
+struct FApply {
+  const double* b;
+  double* y;
+  static constexpr int kDots = 0;
+  struct In {
+    double2 b;
+  };
+  struct Out {
+    double2 y;
+  };
+  __device__ In load(long long v) const {
+    In i{};
+    if (MODE) i.b = ld2(b + v);
+    return i;
+  }
+  __device__ void point(int q, double au, double, double, const In& in, Out& o, double&, double&) const {
+    set(o.y, q, MODE ? get(in.b, q) - au : au);
+  }
+  __device__ void store(long long v, const Out& o, bool two) const { st2(y + v, o.y, two); }
+  __device__ void partials(int, double, double) const {}
+};
+
+// post-smooth start: r = b - A x ; d = (r * invd) * s_theta   (solver.cpp:94-98)
+struct FStartRes {
+  const double* b;
+  double *r, *d;
+  double s_theta;
+  static constexpr int kDots = 0;
+  struct In {
+    double2 b;
+  };
+  struct Out {
+    double2 r, d;
+  };
+  __device__ In load(long long v) const { return In{ld2(b + v)}; }
+  __device__ void point(int q, double au, double invd, double, const In& in, Out& o, double&, double&) const {
+    const double rr = get(in.b, q) - au;
+    set(o.r, q, rr);
+    set(o.d, q, (rr * invd) * s_theta);
+  }
+  __device__ void store(long long v, const Out& o, bool two) const {
+    st2(r + v, o.r, two);
+    st2(d + v, o.d, two);
+  }
+  __device__ void partials(int, double, double) const {}
+};
+
+// Chebyshev pass (solver.cpp:100-110): x1 = x + d ; r1 = r - A d ; d' = c1 d + c2 D^-1 r1 ;
+// last pass: x = x1 + d' only.
+struct FStep {
+  const double* r_in;
+  const double* x_in;  // null: x == 0 before this pass
+  double *d_new, *r_out, *x_out;
+  double c1, c2;
+  int last;
+  static constexpr int kDots = 0;
+  struct In {
+    double2 r, x;
+  };
+  struct Out {
+    double2 x, r, d;
+  };
+  __device__ In load(long long v) const {
+    In i;
+    i.r = ld2rw(r_in + v);
+    i.x = x_in ? ld2rw(x_in + v) : double2{0.0, 0.0};
+    return i;
+  }
+  __device__ void point(int q, double au, double invd, double uc, const In& in, Out& o, double&, double&) const {
+    const double x1 = x_in ? get(in.x, q) + uc : uc;
+    const double r1 = get(in.r, q) - au;
+    const double z = r1 * invd;
+    const double dn = c1 * uc + c2 * z;
+    if (last) {
+      set(o.x, q, x1 + dn);
+    } else {
+      set(o.x, q, x1);
+      set(o.r, q, r1);
+      set(o.d, q, dn);
+    }
+  }
+  __device__ void store(long long v, const Out& o, bool two) const {
+    st2(x_out + v, o.x, two);
+    if (!last) {
+      st2(r_out + v, o.r, two);
+      st2(d_new + v, o.d, two);
+    }
+  }
+  __device__ void partials(int, double, double) const {}
+};
+
+// w = A p with the block partial of p.w (solver.cpp:235-236)
+struct FSpmvDot {
+  double* w;
+  double* part;
+  static constexpr int kDots = 1;
+  struct In {};
+  struct Out {
+    double2 w;
+  };
+  __device__ In load(long long) const { return In{}; }
+  __device__ void point(int q, double au, double, double uc, const In&, Out& o, double& a0, double&) const {
+    set(o.w, q, au);
+    a0 += uc * au;
+  }
+  __device__ void store(long long v, const Out& o, bool two) const { st2(w + v, o.w, two); }
+  __device__ void partials(int blk, double s0, double) const { part[blk] = s0; }
+};
+
+// ------------------------------------------------------------------------------------------
+// pointwise passes over vertex pairs (same tiles, so partial counts match grid_blocks)
 // ------------------------------------------------------------------------------------------
 
 template <bool VAR>
+__device__ __forceinline__ double invd_at(const BoxGeo& g, const OpParams& op, int i, int j, int k, long long v) {
+  if (!VAR) return op.cinvd;
+  const Pt p = make_pt(g, i, j, k);
+  const double* K = op.k;
+  return coef_at<true>(op, p, K[v], K[v - 1], K[v + 1], K[v - g.px], K[v + g.px], K[v - g.pxy], K[v + g.pxy]).invd;
+}
+
+#define TMGX_PAIR_LOOP_BEGIN                                                  \
+  const int i0 = 2 * (blockIdx.x * kBX + threadIdx.x), j = blockIdx.y * kBY + threadIdx.y; \
+  if (i0 < g.ex && j < g.ey) {                                                \
+    const bool two = i0 + 1 < g.ex;                                           \
+    const int k0 = blockIdx.z * g.zc, k1 = min(k0 + g.zc, g.ez);              \
+    for (int k = k0; k < k1; ++k) {                                           \
+      const long long v = vidx(g, i0, j, k);
+
+#define TMGX_PAIR_LOOP_END \
+  }                        \
+  }
+
+// pre-smooth start from x = 0 (r = b): d0 = (b * invd) * s_theta ; or x = d0 when m == 1
+template <bool VAR>
 __global__ void __launch_bounds__(kBX* kBY) k_cheb_start_zero(BoxGeo g, OpParams op, const double* __restrict__ b,
                                                                double* __restrict__ out, double s_theta) {
-  const int i = blockIdx.x * kBX + threadIdx.x, j = blockIdx.y * kBY + threadIdx.y;
-  if (i >= g.ex || j >= g.ey) return;
-  const int k0 = blockIdx.z * g.zc, k1 = min(k0 + g.zc, g.ez);
-  for (int k = k0; k < k1; ++k) {
-    const long long v = vidx(g, i, j, k);
-    const Pt p = make_pt(g, i, j, k);
-    double invd;
-    if (VAR) {
-      const double* K = op.k;
-      invd = coef_at<true>(op, p, K[v], K[v - 1], K[v + 1], K[v - g.px], K[v + g.px], K[v - g.pxy], K[v + g.pxy]).invd;
-    } else {
-      invd = op.cinvd;
-    }
-    const double z = b[v] * invd;  // r = b - A*0 = b
-    out[v] = z * s_theta;
-  }
+  TMGX_PAIR_LOOP_BEGIN
+  const double2 bb = ld2(b + v);
+  double2 o;
+  o.x = (bb.x * invd_at<VAR>(g, op, i0, j, k, v)) * s_theta;
+  o.y = two ? (bb.y * invd_at<VAR>(g, op, i0 + 1, j, k, v + 1)) * s_theta : 0.0;
+  st2(out + v, o, two);
+  TMGX_PAIR_LOOP_END
 }
 
-template <bool VAR>
-__global__ void __launch_bounds__(kBX* kBY)
-    k_cheb_start_res(BoxGeo g, OpParams op, const double* __restrict__ b, const double* __restrict__ x,
-                     double* __restrict__ r, double* __restrict__ d, double s_theta) {
-  const int i = blockIdx.x * kBX + threadIdx.x, j = blockIdx.y * kBY + threadIdx.y;
-  if (i >= g.ex || j >= g.ey) return;
-  const int k0 = blockIdx.z * g.zc, k1 = min(k0 + g.zc, g.ez);
-  long long v = vidx(g, i, j, k0);
-  ZQ u{__ldg(x + v - g.pxy), __ldg(x + v), 0.0};
-  ZQ kq{0.0, 0.0, 0.0};
-  if (VAR) kq = ZQ{__ldg(op.k + v - g.pxy), __ldg(op.k + v), 0.0};
-  for (int k = k0; k < k1; ++k, v += g.pxy) {
-    u.n = __ldg(x + v + g.pxy);
-    TMGX_NB(x, u, v)
-    const Pt p = make_pt(g, i, j, k);
-    Coef c;
-    if (VAR) {
-      kq.n = __ldg(op.k + v + g.pxy);
-      c = coef_at<true>(op, p, kq.c, __ldg(op.k + v - 1), __ldg(op.k + v + 1), __ldg(op.k + v - g.px),
-                        __ldg(op.k + v + g.px), kq.m, kq.n);
-      kq.m = kq.c; kq.c = kq.n;
-    } else {
-      c = coef_at<false>(op, p, 0, 0, 0, 0, 0, 0, 0);
-    }
-    const double ax = row_apply(p, c, u.m, xym, xxm, u.c, xxp, xyp, u.n);
-    const double rr = b[v] - ax;
-    r[v] = rr;
-    d[v] = (rr * c.invd) * s_theta;
-    u.m = u.c; u.c = u.n;
-  }
-}
-
-template <bool VAR>
-__global__ void __launch_bounds__(kBX* kBY)
-    k_cheb_step(BoxGeo g, OpParams op, const double* __restrict__ d, const double* r_in, const double* x_in,
-                double* __restrict__ d_new, double* r_out, double* x_out, ChebStep cs, int last) {
-  const int i = blockIdx.x * kBX + threadIdx.x, j = blockIdx.y * kBY + threadIdx.y;
-  if (i >= g.ex || j >= g.ey) return;
-  const int k0 = blockIdx.z * g.zc, k1 = min(k0 + g.zc, g.ez);
-  long long v = vidx(g, i, j, k0);
-  ZQ u{__ldg(d + v - g.pxy), __ldg(d + v), 0.0};
-  ZQ kq{0.0, 0.0, 0.0};
-  if (VAR) kq = ZQ{__ldg(op.k + v - g.pxy), __ldg(op.k + v), 0.0};
-  for (int k = k0; k < k1; ++k, v += g.pxy) {
-    u.n = __ldg(d + v + g.pxy);
-    TMGX_NB(d, u, v)
-    const Pt p = make_pt(g, i, j, k);
-    Coef c;
-    if (VAR) {
-      kq.n = __ldg(op.k + v + g.pxy);
-      c = coef_at<true>(op, p, kq.c, __ldg(op.k + v - 1), __ldg(op.k + v + 1), __ldg(op.k + v - g.px),
-                        __ldg(op.k + v + g.px), kq.m, kq.n);
-      kq.m = kq.c; kq.c = kq.n;
-    } else {
-      c = coef_at<false>(op, p, 0, 0, 0, 0, 0, 0, 0);
-    }
-    const double x1 = x_in ? x_in[v] + u.c : u.c;          // x += 1.0*d
-    const double ad = row_apply(p, c, u.m, dym, dxm, u.c, dxp, dyp, u.n);
-    const double r1 = r_in[v] - ad;                          // r += -1.0*ad
-    const double z = r1 * c.invd;                            // Jacobi
-    const double dn = cs.c1 * u.c + cs.c2 * z;               // d = rho'rho d + 2rho'/delta z
-    if (last) {
-      x_out[v] = x1 + dn;
-    } else {
-      x_out[v] = x1;
-      r_out[v] = r1;
-      d_new[v] = dn;
-    }
-    u.m = u.c; u.c = u.n;
-  }
-}
-
-template <bool VAR, int MODE>  // MODE 0: y = A x ; 1: r = b - A x
-__global__ void __launch_bounds__(kBX* kBY)
-    k_apply(BoxGeo g, OpParams op, const double* __restrict__ x, const double* __restrict__ b,
-            double* __restrict__ y) {
-  const int i = blockIdx.x * kBX + threadIdx.x, j = blockIdx.y * kBY + threadIdx.y;
-  if (i >= g.ex || j >= g.ey) return;
-  const int k0 = blockIdx.z * g.zc, k1 = min(k0 + g.zc, g.ez);
-  long long v = vidx(g, i, j, k0);
-  ZQ u{__ldg(x + v - g.pxy), __ldg(x + v), 0.0};
-  ZQ kq{0.0, 0.0, 0.0};
-  if (VAR) kq = ZQ{__ldg(op.k + v - g.pxy), __ldg(op.k + v), 0.0};
-  for (int k = k0; k < k1; ++k, v += g.pxy) {
-    u.n = __ldg(x + v + g.pxy);
-    TMGX_NB(x, u, v)
-    const Pt p = make_pt(g, i, j, k);
-    Coef c;
-    if (VAR) {
-      kq.n = __ldg(op.k + v + g.pxy);
-      c = coef_at<true>(op, p, kq.c, __ldg(op.k + v - 1), __ldg(op.k + v + 1), __ldg(op.k + v - g.px),
-                        __ldg(op.k + v + g.px), kq.m, kq.n);
-      kq.m = kq.c; kq.c = kq.n;
-    } else {
-      c = coef_at<false>(op, p, 0, 0, 0, 0, 0, 0, 0);
-    }
-    const double ax = row_apply(p, c, u.m, xym, xxm, u.c, xxp, xyp, u.n);
-    y[v] = MODE == 0 ? ax : b[v] - ax;
-    u.m = u.c; u.c = u.n;
-  }
-}
-
-// w = A p with the block partial of p.w (solver.cpp:235-236)
-template <bool VAR>
-__global__ void __launch_bounds__(kBX* kBY)
-    k_spmv_dot(BoxGeo g, OpParams op, const double* __restrict__ x, double* __restrict__ y,
-               double* __restrict__ part) {
-  __shared__ double sh[32];
-  const int i = blockIdx.x * kBX + threadIdx.x, j = blockIdx.y * kBY + threadIdx.y;
-  double acc = 0.0;
-  if (i < g.ex && j < g.ey) {
-    const int k0 = blockIdx.z * g.zc, k1 = min(k0 + g.zc, g.ez);
-    long long v = vidx(g, i, j, k0);
-    ZQ u{__ldg(x + v - g.pxy), __ldg(x + v), 0.0};
-    ZQ kq{0.0, 0.0, 0.0};
-    if (VAR) kq = ZQ{__ldg(op.k + v - g.pxy), __ldg(op.k + v), 0.0};
-    for (int k = k0; k < k1; ++k, v += g.pxy) {
-      u.n = __ldg(x + v + g.pxy);
-      TMGX_NB(x, u, v)
-      const Pt p = make_pt(g, i, j, k);
-      Coef c;
-      if (VAR) {
-        kq.n = __ldg(op.k + v + g.pxy);
-        c = coef_at<true>(op, p, kq.c, __ldg(op.k + v - 1), __ldg(op.k + v + 1), __ldg(op.k + v - g.px),
-                          __ldg(op.k + v + g.px), kq.m, kq.n);
-        kq.m = kq.c; kq.c = kq.n;
-      } else {
-        c = coef_at<false>(op, p, 0, 0, 0, 0, 0, 0, 0);
-      }
-      const double ax = row_apply(p, c, u.m, xym, xxm, u.c, xxp, xyp, u.n);
-      y[v] = ax;
-      acc += u.c * ax;
-      u.m = u.c; u.c = u.n;
-    }
-  }
-  const double s = block_sum(acc, sh);
-  if (threadIdx.x == 0 && threadIdx.y == 0) part[blk_linear()] = s;
-}
-
+// z = r * invd with the block partial of r.z (estimator, solver.cpp:535, 554-556)
 template <bool VAR>
 __global__ void __launch_bounds__(kBX* kBY)
     k_jacobi_dot(BoxGeo g, OpParams op, const double* __restrict__ r, double* __restrict__ z,
                  double* __restrict__ part) {
   __shared__ double sh[32];
-  const int i = blockIdx.x * kBX + threadIdx.x, j = blockIdx.y * kBY + threadIdx.y;
   double acc = 0.0;
-  if (i < g.ex && j < g.ey) {
-    const int k0 = blockIdx.z * g.zc, k1 = min(k0 + g.zc, g.ez);
-    for (int k = k0; k < k1; ++k) {
-      const long long v = vidx(g, i, j, k);
-      double invd = op.cinvd;
-      if (VAR) {
-        const Pt p = make_pt(g, i, j, k);
-        const double* K = op.k;
-        invd = coef_at<true>(op, p, K[v], K[v - 1], K[v + 1], K[v - g.px], K[v + g.px], K[v - g.pxy], K[v + g.pxy]).invd;
-      }
-      const double rv = r[v];
-      const double zv = rv * invd;
-      z[v] = zv;
-      acc += rv * zv;
-    }
+  TMGX_PAIR_LOOP_BEGIN
+  const double2 rr = ld2(r + v);
+  double2 zz;
+  zz.x = rr.x * invd_at<VAR>(g, op, i0, j, k, v);
+  acc += rr.x * zz.x;
+  zz.y = 0.0;
+  if (two) {
+    zz.y = rr.y * invd_at<VAR>(g, op, i0 + 1, j, k, v + 1);
+    acc += rr.y * zz.y;
   }
+  st2(z + v, zz, two);
+  TMGX_PAIR_LOOP_END
   const double s = block_sum(acc, sh);
   if (threadIdx.x == 0 && threadIdx.y == 0) part[blk_linear()] = s;
 }
@@ -395,17 +463,16 @@ __global__ void __launch_bounds__(kBX* kBY)
     k_dot2(BoxGeo g, const double* __restrict__ a, const double* __restrict__ b, const double* __restrict__ c,
            double* __restrict__ pab, double* __restrict__ pcc) {
   __shared__ double sh[32];
-  const int i = blockIdx.x * kBX + threadIdx.x, j = blockIdx.y * kBY + threadIdx.y;
   double s1 = 0.0, s2 = 0.0;
-  if (i < g.ex && j < g.ey) {
-    const int k0 = blockIdx.z * g.zc, k1 = min(k0 + g.zc, g.ez);
-    for (int k = k0; k < k1; ++k) {
-      const long long v = vidx(g, i, j, k);
-      s1 += a[v] * b[v];
-      const double cv = c[v];
-      s2 += cv * cv;
-    }
+  TMGX_PAIR_LOOP_BEGIN
+  const double2 av = ld2(a + v), bv = ld2(b + v), cv = ld2(c + v);
+  s1 += av.x * bv.x;
+  s2 += cv.x * cv.x;
+  if (two) {
+    s1 += av.y * bv.y;
+    s2 += cv.y * cv.y;
   }
+  TMGX_PAIR_LOOP_END
   const double t1 = block_sum(s1, sh);
   const double t2 = block_sum(s2, sh);
   if (threadIdx.x == 0 && threadIdx.y == 0) {
@@ -414,46 +481,52 @@ __global__ void __launch_bounds__(kBX* kBY)
   }
 }
 
+// x += alpha p ; r += (-alpha) w   (solver.cpp:243-244), skipped on breakdown
 __global__ void __launch_bounds__(kBX* kBY)
     k_cg_update(BoxGeo g, const double* __restrict__ p, const double* __restrict__ w, double* __restrict__ x,
                 double* __restrict__ r, const double* __restrict__ scal, int as, int fs) {
   if (scal[fs] != 0.0) return;
   const double alpha = scal[as];
-  const int i = blockIdx.x * kBX + threadIdx.x, j = blockIdx.y * kBY + threadIdx.y;
-  if (i >= g.ex || j >= g.ey) return;
-  const int k0 = blockIdx.z * g.zc, k1 = min(k0 + g.zc, g.ez);
-  for (int k = k0; k < k1; ++k) {
-    const long long v = vidx(g, i, j, k);
-    x[v] += alpha * p[v];
-    r[v] += -alpha * w[v];
-  }
+  TMGX_PAIR_LOOP_BEGIN
+  const double2 pv = ld2(p + v), wv = ld2(w + v);
+  double2 xv = ld2rw(x + v), rv = ld2rw(r + v);
+  xv.x += alpha * pv.x;
+  rv.x += -alpha * wv.x;
+  xv.y += alpha * pv.y;
+  rv.y += -alpha * wv.y;
+  st2(x + v, xv, two);
+  st2(r + v, rv, two);
+  TMGX_PAIR_LOOP_END
 }
 
+// p = z + beta p   (solver.cpp:261-262)
 __global__ void __launch_bounds__(kBX* kBY)
     k_p_update(BoxGeo g, const double* __restrict__ z, double* __restrict__ p, const double* __restrict__ scal,
                int bs) {
   const double beta = scal[bs];
-  const int i = blockIdx.x * kBX + threadIdx.x, j = blockIdx.y * kBY + threadIdx.y;
-  if (i >= g.ex || j >= g.ey) return;
-  const int k0 = blockIdx.z * g.zc, k1 = min(k0 + g.zc, g.ez);
-  for (int k = k0; k < k1; ++k) {
-    const long long v = vidx(g, i, j, k);
-    p[v] = z[v] + beta * p[v];
-  }
+  TMGX_PAIR_LOOP_BEGIN
+  const double2 zv = ld2(z + v);
+  double2 pv = ld2rw(p + v);
+  pv.x = zv.x + beta * pv.x;
+  pv.y = zv.y + beta * pv.y;
+  st2(p + v, pv, two);
+  TMGX_PAIR_LOOP_END
 }
 
 __global__ void __launch_bounds__(kBX* kBY)
     k_axpy(BoxGeo g, double alpha, const double* __restrict__ x, double* __restrict__ y, int copy) {
-  const int i = blockIdx.x * kBX + threadIdx.x, j = blockIdx.y * kBY + threadIdx.y;
-  if (i >= g.ex || j >= g.ey) return;
-  const int k0 = blockIdx.z * g.zc, k1 = min(k0 + g.zc, g.ez);
-  for (int k = k0; k < k1; ++k) {
-    const long long v = vidx(g, i, j, k);
-    if (copy)
-      y[v] = x[v];
-    else
-      y[v] += alpha * x[v];
+  TMGX_PAIR_LOOP_BEGIN
+  const double2 xv = ld2(x + v);
+  double2 yv;
+  if (copy) {
+    yv = xv;
+  } else {
+    yv = ld2rw(y + v);
+    yv.x += alpha * xv.x;
+    yv.y += alpha * xv.y;
   }
+  st2(y + v, yv, two);
+  TMGX_PAIR_LOOP_END
 }
 
 __global__ void k_zero(double* p, long long n) {
@@ -706,38 +779,34 @@ int launch_cheb_start_zero(const BoxGeo& g, const OpParams& op, const double* b,
   return 1;
 }
 
+template <class F>
+static void march(const BoxGeo& g, const OpParams& op, const double* u, const F& f, cudaStream_t s) {
+  if (op.k)
+    k_march<true, F><<<tile_grid(g), kBlock, 0, s>>>(g, op, u, f);
+  else
+    k_march<false, F><<<tile_grid(g), kBlock, 0, s>>>(g, op, u, f);
+}
+
 int launch_cheb_start_res(const BoxGeo& g, const OpParams& op, const double* b, const double* x, double* r, double* d,
                           double s_theta, cudaStream_t s) {
-  if (op.k)
-    k_cheb_start_res<true><<<tile_grid(g), kBlock, 0, s>>>(g, op, b, x, r, d, s_theta);
-  else
-    k_cheb_start_res<false><<<tile_grid(g), kBlock, 0, s>>>(g, op, b, x, r, d, s_theta);
+  march(g, op, x, FStartRes{b, r, d, s_theta}, s);
   return 1;
 }
 
 int launch_cheb_step(const BoxGeo& g, const OpParams& op, const double* d, const double* r_in, const double* x_in,
                      double* d_new, double* r_out, double* x_out, ChebStep c, bool last, cudaStream_t s) {
-  if (op.k)
-    k_cheb_step<true><<<tile_grid(g), kBlock, 0, s>>>(g, op, d, r_in, x_in, d_new, r_out, x_out, c, last ? 1 : 0);
-  else
-    k_cheb_step<false><<<tile_grid(g), kBlock, 0, s>>>(g, op, d, r_in, x_in, d_new, r_out, x_out, c, last ? 1 : 0);
+  march(g, op, d, FStep{r_in, x_in, d_new, r_out, x_out, c.c1, c.c2, last ? 1 : 0}, s);
   return 1;
 }
 
 int launch_residual(const BoxGeo& g, const OpParams& op, const double* b, const double* x, double* r,
                     cudaStream_t s) {
-  if (op.k)
-    k_apply<true, 1><<<tile_grid(g), kBlock, 0, s>>>(g, op, x, b, r);
-  else
-    k_apply<false, 1><<<tile_grid(g), kBlock, 0, s>>>(g, op, x, b, r);
+  march(g, op, x, FApply<1>{b, r}, s);
   return 1;
 }
 
 int launch_apply(const BoxGeo& g, const OpParams& op, const double* x, double* y, cudaStream_t s) {
-  if (op.k)
-    k_apply<true, 0><<<tile_grid(g), kBlock, 0, s>>>(g, op, x, nullptr, y);
-  else
-    k_apply<false, 0><<<tile_grid(g), kBlock, 0, s>>>(g, op, x, nullptr, y);
+  march(g, op, x, FApply<0>{nullptr, y}, s);
   return 1;
 }
 
@@ -752,10 +821,7 @@ int launch_prolong_add(const BoxGeo& fine, const BoxGeo& coarse, const double* x
 }
 
 int launch_spmv_dot(const BoxGeo& g, const OpParams& op, const double* p, double* w, double* part, cudaStream_t s) {
-  if (op.k)
-    k_spmv_dot<true><<<tile_grid(g), kBlock, 0, s>>>(g, op, p, w, part);
-  else
-    k_spmv_dot<false><<<tile_grid(g), kBlock, 0, s>>>(g, op, p, w, part);
+  march(g, op, p, FSpmvDot{w, part}, s);
   return 1;
 }
 

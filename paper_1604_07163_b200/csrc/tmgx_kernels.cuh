@@ -31,7 +31,7 @@ struct BoxGeo {
 // block (register queue reuse), coarse boxes trade reuse for parallelism (latency-bound).
 constexpr int kMinBlocks = 8 * 148;
 inline int choose_zc(int ex, int ey, int ez) {
-  const int bxy = ((ex + kBX - 1) / kBX) * ((ey + kBY - 1) / kBY);
+  const int bxy = ((ex + 2 * kBX - 1) / (2 * kBX)) * ((ey + kBY - 1) / kBY);  // pair tiles
   for (int zc = kZC; zc > 1; zc >>= 1)
     if ((long long)bxy * ((ez + zc - 1) / zc) >= kMinBlocks) return zc;
   return 1;
