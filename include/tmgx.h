@@ -189,6 +189,14 @@ typedef struct {
 } tmgx_counters;
 int tmgx_get_counters(tmgx_solver s, tmgx_counters *c);
 
+/* Host-only (no GPU): the data-movement plans process `proc` of `nproc` would build for this
+ * problem/hierarchy. One record of 6 int64 per (plan, peer): {plan_id (3*node + 0 halo,
+ * +1 telescope gather, +2 telescope scatter), kind (0 send, 1 recv, 2 local copy), peer
+ * process, vertex count, checksum of the global vertex indices moved, level}. Used by the
+ * multi-process consistency tests (every send must match the peer's receive). */
+int tmgx_plan_summary(int n_ranks, int nproc, int proc, const tmgx_problem *prob, const tmgx_mg_cfg *mg,
+                      int64_t *records, int max_records, int *n_records);
+
 /* Kernel micro-timing for the roofline (bench.py): launches kernel `which` on `level` `iters`
  * times back to back on the library stream between CUDA events. Outputs the mean device time
  * per launch and the algorithmic HBM bytes one launch must move (DESIGN.md §5 table).

@@ -58,6 +58,33 @@ void from_hdr(const tmg::GridHeader& g, tmgx_header* h) {
   }
 }
 
+tmgx::ProblemDesc to_problem(const tmgx_problem* p) {
+  tmgx::ProblemDesc pd;
+  pd.kind = p->kind;
+  for (int a = 0; a < 3; ++a) {
+    pd.np[a] = p->np[a];
+    pd.pg_hint[a] = p->pg_hint[a];
+  }
+  pd.seed_k = p->seed_k;
+  pd.n_spheres = p->n_spheres;
+  pd.k_in = p->k_in;
+  if (pd.kind != TMGX_POISSON7 && pd.kind != TMGX_VARCOEF7_HARMONIC) throw tmg::ConfigError("unknown operator kind");
+  return pd;
+}
+
+tmgx::MGDesc to_mg(const tmgx_mg_cfg* m) {
+  tmgx::MGDesc md;
+  md.nlevels = m->nlevels;
+  md.m = m->smooth_its;
+  md.est_mode = m->est_mode;
+  if (m->cheb_bounds) md.bounds.assign(m->cheb_bounds, m->cheb_bounds + 2 * m->nlevels);
+  if (m->n_telescope < 0 || m->n_telescope > TMGX_MAX_TELESCOPE) throw tmg::ConfigError("bad telescope count");
+  for (int t = 0; t < m->n_telescope; ++t)
+    md.tele.push_back({m->telescope[t].level, m->telescope[t].reduction_factor,
+                       {m->telescope[t].override_[0], m->telescope[t].override_[1], m->telescope[t].override_[2]}});
+  return md;
+}
+
 int check_level(tmgx_solver s, int level) {
   if (!s || !s->s) throw tmg::Error("null solver");
   if (level < 0 || level >= s->s->mgd.nlevels) throw tmg::Error("level out of range");
@@ -185,25 +212,8 @@ int tmgx_world_local_ranks(tmgx_world w, int* first, int* end) {
 
 int tmgx_solver_create(tmgx_world w, const tmgx_problem* p, const tmgx_mg_cfg* m, tmgx_solver* out) {
   return guard([&] {
-    tmgx::ProblemDesc pd;
-    pd.kind = p->kind;
-    for (int a = 0; a < 3; ++a) {
-      pd.np[a] = p->np[a];
-      pd.pg_hint[a] = p->pg_hint[a];
-    }
-    pd.seed_k = p->seed_k;
-    pd.n_spheres = p->n_spheres;
-    pd.k_in = p->k_in;
-    if (pd.kind != TMGX_POISSON7 && pd.kind != TMGX_VARCOEF7_HARMONIC) throw tmg::ConfigError("unknown operator kind");
-    tmgx::MGDesc md;
-    md.nlevels = m->nlevels;
-    md.m = m->smooth_its;
-    md.est_mode = m->est_mode;
-    if (m->cheb_bounds) md.bounds.assign(m->cheb_bounds, m->cheb_bounds + 2 * m->nlevels);
-    if (m->n_telescope < 0 || m->n_telescope > TMGX_MAX_TELESCOPE) throw tmg::ConfigError("bad telescope count");
-    for (int t = 0; t < m->n_telescope; ++t)
-      md.tele.push_back({m->telescope[t].level, m->telescope[t].reduction_factor,
-                         {m->telescope[t].override_[0], m->telescope[t].override_[1], m->telescope[t].override_[2]}});
+    const tmgx::ProblemDesc pd = to_problem(p);
+    const tmgx::MGDesc md = to_mg(m);
     auto s = new tmgx_solver_s;
     s->world = w;
     try {
@@ -409,6 +419,41 @@ int tmgx_telescope_scatter(tmgx_solver s, int stage, const double* ys, double* y
     S.upload(i + 1, S.nodes[i + 1].x, ys, false);
     tmgx::run_plan(S.W, S.nodes[i].scatter, S.nodes[i + 1].x, S.nodes[i].x, true);
     S.download(i, S.nodes[i].x, yp, false);
+    return 0;
+  });
+}
+
+int tmgx_plan_summary(int n_ranks, int nproc, int proc, const tmgx_problem* p, const tmgx_mg_cfg* m, int64_t* out,
+                      int max_records, int* n_records) {
+  return guard([&] {
+    const tmgx::Owners W(n_ranks, nproc, proc);
+    const auto specs = tmgx::build_node_specs(W, to_problem(p), to_mg(m));
+    int n = 0;
+    auto emit = [&](int plan_id, int kind, int peer, long long count, unsigned long long sum, int level) {
+      if (n >= max_records) throw tmg::Error("plan_summary: record buffer too small");
+      int64_t* r = out + 6 * n++;
+      r[0] = plan_id;
+      r[1] = kind;
+      r[2] = peer;
+      r[3] = count;
+      r[4] = (int64_t)sum;
+      r[5] = level;
+    };
+    auto dump = [&](int plan_id, const tmgx::PlanHost& ph, int level) {
+      for (size_t q = 0; q < ph.sends.size(); ++q)
+        emit(plan_id, 0, ph.sends[q].proc, ph.sends[q].count, ph.send_sum[q], level);
+      for (size_t q = 0; q < ph.recvs.size(); ++q)
+        emit(plan_id, 1, ph.recvs[q].proc, ph.recvs[q].count, ph.recv_sum[q], level);
+      emit(plan_id, 2, proc, ph.local_count, 0, level);
+    };
+    for (size_t i = 0; i < specs.size(); ++i) {
+      dump(3 * (int)i, tmgx::halo_plan_host(W, *specs[i].dist), specs[i].level);
+      if (specs[i].kind == tmgx::TELESCOPE) {
+        dump(3 * (int)i + 1, tmgx::transfer_plan_host(W, *specs[i].dist, *specs[i + 1].dist), specs[i].level);
+        dump(3 * (int)i + 2, tmgx::transfer_plan_host(W, *specs[i + 1].dist, *specs[i].dist), specs[i].level);
+      }
+    }
+    *n_records = n;
     return 0;
   });
 }

@@ -19,11 +19,14 @@ void nccl_check(ncclResult_t e, const char* what) {
 // World
 // ------------------------------------------------------------------------------------------
 
-World::World(int R_, int P_, int me_, int device_, const void* nccl_id) : R(R_), P(P_), me(me_), device(device_) {
+Owners::Owners(int R_, int P_, int me_) : R(R_), P(P_), me(me_) {
   if (R < 1 || P < 1 || me < 0 || me >= P || R < P)
     throw tmg::ConfigError("world: need n_ranks >= nproc >= 1 and 0 <= proc < nproc");
   first = (int)((long long)me * R / P);
   end = (int)((long long)(me + 1) * R / P);
+}
+
+World::World(int R_, int P_, int me_, int device_, const void* nccl_id) : Owners(R_, P_, me_), device(device_) {
   CK(cudaSetDevice(device));
   CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
   if (P > 1) {
@@ -39,7 +42,7 @@ World::~World() {
   if (stream) cudaStreamDestroy(stream);
 }
 
-int World::owner(int wr) const {
+int Owners::owner(int wr) const {
   for (int p = 0; p < P; ++p)
     if (wr < (int)((long long)(p + 1) * R / P)) return p;
   return P - 1;
@@ -85,7 +88,7 @@ static long long geo_off(const BoxGeo& g, long long i, long long j, long long k)
   return g.base + (i - g.gx) + g.px * (j - g.gy) + g.pxy * (k - g.gz);
 }
 
-std::shared_ptr<Dist> make_dist(const World& W, const tmg::GridHeader& h, const std::vector<int>& wr) {
+std::shared_ptr<Dist> make_dist(const Owners& W, const tmg::GridHeader& h, const std::vector<int>& wr) {
   auto D = std::make_shared<Dist>();
   D->h = h;
   D->wr = wr;
@@ -130,13 +133,21 @@ Field make_field(DeviceArena& A, const Dist& D) {
 
 namespace {
 
+// checksum of the global vertex indices of a region (both ends compute it from the headers)
+unsigned long long region_sum(const tmg::GridBox& reg, const tmg::GridHeader& h) {
+  unsigned long long s = 0;
+  for (long long k = reg.lo[2]; k < reg.hi[2]; ++k)
+    for (long long j = reg.lo[1]; j < reg.hi[1]; ++j)
+      for (long long i = reg.lo[0]; i < reg.hi[0]; ++i) {
+        const unsigned long long nat = (unsigned long long)(i + h.npoints[0] * (j + h.npoints[1] * k));
+        s = s * 1099511628211ULL + (nat ^ 0x9e3779b97f4a7c15ULL);
+      }
+  return s;
+}
+
 template <class RegionFn>
-RegionPlan build_plan(World& W, DeviceArena& A, const Dist& S, const Dist& T, RegionFn region) {
-  RegionPlan plan;
-  std::vector<CopyDesc> loc, pack, unpack;
-  struct Seg {
-    long long count = 0;
-  };
+PlanHost plan_host(const Owners& W, const Dist& S, const Dist& T, RegionFn region) {
+  PlanHost plan;
   std::vector<long long> scount(W.P, 0), rcount(W.P, 0);
   // pass 1: count per peer
   for (int m = 0; m < T.h.n_ranks(); ++m)
@@ -149,14 +160,22 @@ RegionPlan build_plan(World& W, DeviceArena& A, const Dist& S, const Dist& T, Re
       if (ot == W.me) rcount[os] += reg.n_vertices();
     }
   std::vector<long long> soff(W.P, 0), roff(W.P, 0);
-  long long st = 0, rt = 0;
+  std::vector<int> sidx(W.P, -1), ridx(W.P, -1);
   for (int p = 0; p < W.P; ++p) {
-    soff[p] = st;
-    roff[p] = rt;
-    if (scount[p]) plan.sends.push_back({p, st, scount[p]});
-    if (rcount[p]) plan.recvs.push_back({p, rt, rcount[p]});
-    st += scount[p];
-    rt += rcount[p];
+    soff[p] = plan.send_total;
+    roff[p] = plan.recv_total;
+    if (scount[p]) {
+      sidx[p] = (int)plan.sends.size();
+      plan.sends.push_back({p, plan.send_total, scount[p]});
+      plan.send_sum.push_back(0);
+    }
+    if (rcount[p]) {
+      ridx[p] = (int)plan.recvs.size();
+      plan.recvs.push_back({p, plan.recv_total, rcount[p]});
+      plan.recv_sum.push_back(0);
+    }
+    plan.send_total += scount[p];
+    plan.recv_total += rcount[p];
   }
   // pass 2: descriptors in (m asc, s asc) order, identical on both sides of every pair
   for (int m = 0; m < T.h.n_ranks(); ++m)
@@ -164,6 +183,7 @@ RegionPlan build_plan(World& W, DeviceArena& A, const Dist& S, const Dist& T, Re
       tmg::GridBox reg;
       if (!region(s, m, reg)) continue;
       const int os = W.owner(S.wr[s]), ot = W.owner(T.wr[m]);
+      if (os != W.me && ot != W.me) continue;
       CopyDesc d{};
       d.nx = (int)reg.extent(0);
       d.ny = (int)reg.extent(1);
@@ -186,7 +206,8 @@ RegionPlan build_plan(World& W, DeviceArena& A, const Dist& S, const Dist& T, Re
         d.dst_pxy = gt.pxy;
       }
       if (os == W.me && ot == W.me) {
-        loc.push_back(d);
+        plan.loc.push_back(d);
+        plan.local_count += n;
         plan.max_local = std::max<long long>(plan.max_local, n);
       } else if (os == W.me) {
         d.dst_slot = -1;
@@ -194,38 +215,52 @@ RegionPlan build_plan(World& W, DeviceArena& A, const Dist& S, const Dist& T, Re
         d.dst_px = d.nx;
         d.dst_pxy = (long long)d.nx * d.ny;
         soff[ot] += n;
-        pack.push_back(d);
+        plan.pack.push_back(d);
         plan.max_pack = std::max<long long>(plan.max_pack, n);
-      } else if (ot == W.me) {
+        auto& cs = plan.send_sum[sidx[ot]];
+        cs = cs * 31 + region_sum(reg, T.h);
+      } else {
         d.src_slot = -1;
         d.src_off = roff[os];
         d.src_px = d.nx;
         d.src_pxy = (long long)d.nx * d.ny;
         roff[os] += n;
-        unpack.push_back(d);
+        plan.unpack.push_back(d);
         plan.max_unpack = std::max<long long>(plan.max_unpack, n);
+        auto& cs = plan.recv_sum[ridx[os]];
+        cs = cs * 31 + region_sum(reg, T.h);
       }
     }
-  auto upload = [&](const std::vector<CopyDesc>& v, CopyDesc*& dst, int& n) {
-    n = (int)v.size();
-    if (!n) return;
-    dst = A.alloc_t<CopyDesc>(n);
-    CK(cudaMemcpy(dst, v.data(), sizeof(CopyDesc) * v.size(), cudaMemcpyHostToDevice));
-  };
-  upload(loc, plan.d_local, plan.n_local);
-  upload(pack, plan.d_pack, plan.n_pack);
-  upload(unpack, plan.d_unpack, plan.n_unpack);
-  if (st) plan.sendbuf = A.alloc(st);
-  if (rt) plan.recvbuf = A.alloc(rt);
   return plan;
 }
 
 }  // namespace
 
+RegionPlan upload_plan(DeviceArena& A, const PlanHost& h) {
+  RegionPlan plan;
+  auto up = [&](const std::vector<CopyDesc>& v, CopyDesc*& dst, int& n) {
+    n = (int)v.size();
+    if (!n) return;
+    dst = A.alloc_t<CopyDesc>(n);
+    CK(cudaMemcpy(dst, v.data(), sizeof(CopyDesc) * v.size(), cudaMemcpyHostToDevice));
+  };
+  up(h.loc, plan.d_local, plan.n_local);
+  up(h.pack, plan.d_pack, plan.n_pack);
+  up(h.unpack, plan.d_unpack, plan.n_unpack);
+  plan.max_local = h.max_local;
+  plan.max_pack = h.max_pack;
+  plan.max_unpack = h.max_unpack;
+  plan.sends = h.sends;
+  plan.recvs = h.recvs;
+  if (h.send_total) plan.sendbuf = A.alloc(h.send_total);
+  if (h.recv_total) plan.recvbuf = A.alloc(h.recv_total);
+  return plan;
+}
+
 // ghost_exchange (grid.cpp:645-696): every rank's halo box (width 1, clipped to the grid,
 // edges and corners included) is filled from the owning boxes.
-RegionPlan build_halo_plan(World& W, DeviceArena& A, const Dist& D) {
-  return build_plan(W, A, D, D, [&](int s, int m, tmg::GridBox& reg) {
+PlanHost halo_plan_host(const Owners& W, const Dist& D) {
+  return plan_host(W, D, D, [&](int s, int m, tmg::GridBox& reg) {
     if (s == m) return false;
     tmg::GridBox hb = D.h.box(m);
     for (int a = 0; a < 3; ++a) {
@@ -240,8 +275,8 @@ RegionPlan build_halo_plan(World& W, DeviceArena& A, const Dist& D) {
 // P-hat^T composed with ScatterPlan::to_sub (grid.cpp:582-599, scatter_plan.cpp:40-77):
 // every vertex moves from its parent owner box to the member box that owns it in the
 // repartitioned header, i.e. box intersections of the two decompositions.
-RegionPlan build_transfer_plan(World& W, DeviceArena& A, const Dist& S, const Dist& T) {
-  return build_plan(W, A, S, T, [&](int s, int m, tmg::GridBox& reg) {
+PlanHost transfer_plan_host(const Owners& W, const Dist& S, const Dist& T) {
+  return plan_host(W, S, T, [&](int s, int m, tmg::GridBox& reg) {
     reg = tmg::intersect(S.h.box(s), T.h.box(m));
     return !reg.empty();
   });
@@ -351,7 +386,8 @@ int Solver::node_for_level(int level) const {
   return best;
 }
 
-void Solver::build_nodes() {
+std::vector<NodeSpec> build_node_specs(const Owners& W, const ProblemDesc& prob, const MGDesc& mgd) {
+  if (mgd.nlevels < 1) throw tmg::ConfigError("mg: number of levels must be >= 1");
   const int top = mgd.nlevels - 1;
   std::optional<std::array<int, 3>> hint;
   if (prob.pg_hint[0] || prob.pg_hint[1] || prob.pg_hint[2]) hint = prob.pg_hint;
@@ -366,17 +402,18 @@ void Solver::build_nodes() {
     if (t && tele[t].level == tele[t - 1].level) throw tmg::ConfigError("telescope: two stages on one level");
     if (tele[t].r < 1) throw tmg::ConfigError("telescope: reduction factor must be >= 1");
   }
+  std::vector<NodeSpec> out;
   const int T = (int)tele.size();
   int seg_top = top;
   for (int s = 0; s <= T; ++s) {
     const int bottom = s < T ? tele[s].level : 0;
     for (int l = seg_top; l >= bottom; --l) {
-      Node nd;
+      NodeSpec nd;
       nd.level = l;
       nd.stage = (s < T && l == bottom) ? s : -1;
       nd.kind = (s < T && l == bottom) ? TELESCOPE : (l == 0 ? COARSE : SMOOTH);
       nd.dist = make_dist(W, H, wr);
-      nodes.push_back(std::move(nd));
+      out.push_back(nd);
       if (l > bottom) {
         auto c = tmg::try_coarsen_header(H);
         if (!c)
@@ -388,7 +425,7 @@ void Solver::build_nodes() {
         H = *c;
       }
     }
-    if (s < T) {
+    if (s < T) {  // TelescopePC setup: split_strided + repartition_onto
       const tmg::SplitResult sp = tmg::split_strided(H.n_ranks(), tele[s].r);
       std::array<std::optional<int>, 3> ov;
       for (int a = 0; a < 3; ++a)
@@ -398,12 +435,24 @@ void Solver::build_nodes() {
       for (int mm : sp.member_map) nwr.push_back(wr[mm]);
       wr = nwr;
       seg_top = bottom;
-      stage_node.push_back((int)nodes.size() - 1);
     }
   }
-  if (nodes.back().dist->h.n_ranks() != 1)
+  if (out.back().dist->h.n_ranks() != 1)
     throw tmg::ConfigError("pc_type lu needs a single-rank communicator; repartition first, e.g. pc_type telescope "
                            "with <prefix>telescope_pc_type lu");
+  return out;
+}
+
+void Solver::build_nodes() {
+  for (const NodeSpec& sp : build_node_specs(W, prob, mgd)) {
+    Node nd;
+    nd.kind = sp.kind;
+    nd.level = sp.level;
+    nd.stage = sp.stage;
+    nd.dist = sp.dist;
+    if (nd.kind == TELESCOPE) stage_node.push_back((int)nodes.size());
+    nodes.push_back(std::move(nd));
+  }
 
   // CG workspace; the top node's V-cycle input/output are the CG's r and z (fixed bindings,
   // so the captured iteration graph stays valid)
@@ -441,12 +490,12 @@ void Solver::build_nodes() {
       nd.d = make_field(arena, D);
       nd.d2 = make_field(arena, D);
     }
-    nd.halo = build_halo_plan(W, arena, D);
+    nd.halo = upload_plan(arena, halo_plan_host(W, D));
   }
   for (size_t i = 0; i < nodes.size(); ++i)
     if (nodes[i].kind == TELESCOPE) {
-      nodes[i].gather = build_transfer_plan(W, arena, *nodes[i].dist, *nodes[i + 1].dist);
-      nodes[i].scatter = build_transfer_plan(W, arena, *nodes[i + 1].dist, *nodes[i].dist);
+      nodes[i].gather = upload_plan(arena, transfer_plan_host(W, *nodes[i].dist, *nodes[i + 1].dist));
+      nodes[i].scatter = upload_plan(arena, transfer_plan_host(W, *nodes[i + 1].dist, *nodes[i].dist));
     }
   part = arena.alloc((long long)nloc_max * 2 * nblk_max);
   for (int q = 0; q < nloc_max; ++q) part_off.push_back((long long)q * 2 * nblk_max);

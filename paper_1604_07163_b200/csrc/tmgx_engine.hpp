@@ -36,19 +36,25 @@ struct Counters {
   long long allreduces = 0;
 };
 
-struct World {
-  int R = 1;       // reference ranks (grid boxes)
+// Which process owns which reference rank: process p owns [p*R/P, (p+1)*R/P).
+struct Owners {
+  int R = 1;  // reference ranks (grid boxes)
   int P = 1, me = 0;
-  int device = 0;
   int first = 0, end = 1;  // local reference ranks
+  Owners() = default;
+  Owners(int R, int P, int me);
+  int owner(int world_rank) const;
+  bool local(int world_rank) const { return owner(world_rank) == me; }
+};
+
+struct World : Owners {
+  int device = 0;
   cudaStream_t stream = nullptr;
   ncclComm_t nccl = nullptr;
   Counters cnt;
 
   World(int R, int P, int me, int device, const void* nccl_id);
   ~World();
-  int owner(int world_rank) const;
-  bool local(int world_rank) const { return owner(world_rank) == me; }
 };
 
 // A GridHeader over a communicator whose comm rank m is reference rank wr[m].
@@ -61,7 +67,7 @@ struct Dist {
   long long local_unknowns() const;
 };
 
-std::shared_ptr<Dist> make_dist(const World& W, const tmg::GridHeader& h, const std::vector<int>& wr);
+std::shared_ptr<Dist> make_dist(const Owners& W, const tmg::GridHeader& h, const std::vector<int>& wr);
 
 // Per-local-box device buffers of one logical vector.
 struct Field {
@@ -102,8 +108,20 @@ struct RegionPlan {
   bool empty() const { return n_local == 0 && sends.empty() && recvs.empty(); }
 };
 
-RegionPlan build_halo_plan(World& W, DeviceArena& A, const Dist& D);
-RegionPlan build_transfer_plan(World& W, DeviceArena& A, const Dist& S, const Dist& T);
+// Host half of a plan: descriptors in (target rank asc, source rank asc) order, identical on
+// both ends of every process pair; per-peer segment sizes and a checksum of the global vertex
+// indices moved (for cross-process consistency tests).
+struct PlanHost {
+  std::vector<CopyDesc> loc, pack, unpack;
+  std::vector<RegionPlan::Peer> sends, recvs;
+  std::vector<unsigned long long> send_sum, recv_sum;  // aligned with sends / recvs
+  long long local_count = 0;
+  int max_local = 0, max_pack = 0, max_unpack = 0;
+  long long send_total = 0, recv_total = 0;
+};
+PlanHost halo_plan_host(const Owners& W, const Dist& D);
+PlanHost transfer_plan_host(const Owners& W, const Dist& S, const Dist& T);
+RegionPlan upload_plan(DeviceArena& A, const PlanHost& h);
 void run_plan(World& W, const RegionPlan& plan, const Field& src, const Field& dst, bool telescope);
 
 struct ProblemDesc {
@@ -130,6 +148,16 @@ struct MGDesc {
 };
 
 enum NodeKind { SMOOTH = 0, TELESCOPE = 1, COARSE = 2 };
+
+// The V-cycle node list (host-only): outer levels on the world, TELESCOPE nodes at each stage
+// level, the members' inner levels, COARSE (LU) at level 0 on a single rank.
+struct NodeSpec {
+  NodeKind kind;
+  int level;
+  int stage;
+  std::shared_ptr<Dist> dist;
+};
+std::vector<NodeSpec> build_node_specs(const Owners& W, const ProblemDesc& P, const MGDesc& M);
 
 struct Node {
   NodeKind kind;

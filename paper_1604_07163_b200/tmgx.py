@@ -84,7 +84,7 @@ EXPORTS = [
     "tmgx_solver_level_info", "tmgx_solver_bounds", "tmgx_fill_rhs", "tmgx_solve", "tmgx_solve_seeded",
     "tmgx_pc_apply", "tmgx_level_apply", "tmgx_level_smooth", "tmgx_level_residual_restrict",
     "tmgx_level_prolong_add", "tmgx_coarse_solve", "tmgx_telescope_gather", "tmgx_telescope_scatter",
-    "tmgx_get_counters", "tmgx_parity_build", "tmgx_last_error", "tmgx_bench_kernel",
+    "tmgx_get_counters", "tmgx_parity_build", "tmgx_last_error", "tmgx_bench_kernel", "tmgx_plan_summary",
 ]
 
 _libs = {}
@@ -136,6 +136,7 @@ def load(parity: bool = False):
         "tmgx_telescope_scatter": [C.c_void_p, C.c_int, D, D],
         "tmgx_get_counters": [C.c_void_p, P(_Counters)],
         "tmgx_bench_kernel": [C.c_void_p, C.c_int, C.c_int, C.c_int, D, D],
+        "tmgx_plan_summary": [C.c_int, C.c_int, C.c_int, P(_Problem), P(_MG), I64, C.c_int, P(C.c_int)],
     }
     sig["tmgx_repartition_header"] = [H, C.c_int, P(C.c_int), H]
     for name, args in sig.items():
@@ -383,31 +384,54 @@ class World:
             pass
 
 
+def _c_problem(problem: Problem):
+    p = _Problem()
+    p.kind = problem.kind
+    for a in range(3):
+        p.np[a] = problem.npoints[a]
+        p.pg_hint[a] = problem.proc_grid_hint[a] if problem.proc_grid_hint else 0
+    p.seed_k, p.n_spheres, p.k_in = problem.seed_k, problem.n_spheres, problem.k_in
+    return p
+
+
+def _c_mg(mg: MGConfig):
+    m = _MG()
+    m.nlevels, m.smooth_its, m.est_mode = mg.nlevels, mg.smooth_its, mg.est_mode
+    bounds = None
+    if mg.cheb_bounds is not None:
+        bounds = np.ascontiguousarray(mg.cheb_bounds, dtype=np.float64)
+        m.cheb_bounds = _dp(bounds)
+    m.n_telescope = len(mg.telescope)
+    for t, st in enumerate(mg.telescope):
+        m.telescope[t].level = st.level
+        m.telescope[t].reduction_factor = st.reduction_factor
+        for a in range(3):
+            o = st.repart_da_processors[a]
+            m.telescope[t].override_[a] = 0 if o is None else o
+    return m, bounds
+
+
+def plan_summary(n_ranks, nproc, proc, problem: Problem, mg: MGConfig, max_records=100000):
+    """Host-only: the halo / telescope plans process `proc` would build (tmgx_plan_summary).
+    Returns a list of (plan_id, kind, peer, count, checksum, level); kind 0 send, 1 recv, 2 local."""
+    L = load()
+    p = _c_problem(problem)
+    m, _keep = _c_mg(mg)
+    out = np.zeros(6 * max_records, dtype=np.int64)
+    n = C.c_int()
+    _check(L, L.tmgx_plan_summary(n_ranks, nproc, proc, C.byref(p), C.byref(m), _i64(out), max_records,
+                                  C.byref(n)))
+    return [tuple(int(v) for v in out[6 * i: 6 * i + 6]) for i in range(n.value)]
+
+
 class SolverNode:
     """SolverNode (solver.hpp:72-93): CG + MG(Chebyshev-Jacobi, telescope, LU) on tmgx."""
 
     def __init__(self, world: World, problem: Problem, mg: MGConfig):
         self.world, self.problem, self.mg = world, problem, mg
         self.L = world.L
-        p = _Problem()
-        p.kind = problem.kind
-        for a in range(3):
-            p.np[a] = problem.npoints[a]
-            p.pg_hint[a] = problem.proc_grid_hint[a] if problem.proc_grid_hint else 0
-        p.seed_k, p.n_spheres, p.k_in = problem.seed_k, problem.n_spheres, problem.k_in
-        m = _MG()
-        m.nlevels, m.smooth_its, m.est_mode = mg.nlevels, mg.smooth_its, mg.est_mode
-        self._bounds = None
-        if mg.cheb_bounds is not None:
-            self._bounds = np.ascontiguousarray(mg.cheb_bounds, dtype=np.float64)
-            m.cheb_bounds = _dp(self._bounds)
-        m.n_telescope = len(mg.telescope)
-        for t, st in enumerate(mg.telescope):
-            m.telescope[t].level = st.level
-            m.telescope[t].reduction_factor = st.reduction_factor
-            for a in range(3):
-                o = st.repart_da_processors[a]
-                m.telescope[t].override_[a] = 0 if o is None else o
+        p = _c_problem(problem)
+        m, self._bounds = _c_mg(mg)
         self.h = C.c_void_p()
         _check(self.L, self.L.tmgx_solver_create(world.h, C.byref(p), C.byref(m), C.byref(self.h)))
 

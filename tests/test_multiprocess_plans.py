@@ -1,0 +1,128 @@
+"""CPU, multi-process (gloo, world_size 2 and 4): the one-box-per-GPU path's host logic.
+
+Every process builds the halo and telescope plans it would execute with NCCL send/recv
+(tmgx_plan_summary, no GPU needed). The processes exchange their plans over gloo and check:
+  * every send p->q matches q's receive from p (same vertex count and the same checksum of
+    the global vertex indices, i.e. the same regions in the same order);
+  * halo plans move exactly the vertices of each rank's clipped box halo that other ranks own
+    (recomputed here independently from the GridHeader boxes);
+  * telescope gathers/scatters move every vertex of the level exactly once (P-hat^T + row
+    fusion is a bijection, AC3), and non-members of a sub-communicator receive nothing.
+"""
+import os
+import socket
+
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1604_07163_b200 import tmgx as T
+
+CASES = [
+    # (n_ranks, problem npoints, nlevels, telescope stages)
+    (2, (33, 33, 33), 4, [T.TelescopeStage(0, 2)]),
+    (2, (65, 33, 33), 4, [T.TelescopeStage(1, 2)]),
+    (4, (257, 257, 257), 7, [T.TelescopeStage(3, 4)]),  # cfg2 @4: (1,2,2), r=4 at 33^3
+    (4, (65, 65, 65), 5, [T.TelescopeStage(2, 2), T.TelescopeStage(1, 2)]),
+    (4, (65, 65, 33), 4, [T.TelescopeStage(1, 2, (None, None, 1)), T.TelescopeStage(0, 2)]),
+]
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _halo_expect(h: T.GridHeader, me_ranks):
+    """vertices each (src rank -> dst rank) halo pair moves, from the boxes."""
+    out = {}
+    for m in range(h.n_ranks()):
+        lo, hi = h.box(m)
+        hlo = [max(0, lo[a] - 1) for a in range(3)]
+        hhi = [min(h.npoints[a], hi[a] + 1) for a in range(3)]
+        for s in range(h.n_ranks()):
+            if s == m:
+                continue
+            slo, shi = h.box(s)
+            n = 1
+            for a in range(3):
+                n *= max(0, min(hhi[a], shi[a]) - max(hlo[a], slo[a]))
+            if n:
+                out[(s, m)] = n
+    return out
+
+
+def _worker(rank, world, port, case_idx, results):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n_ranks, np3, nl, tele = CASES[case_idx]
+        prob = T.Problem(np3, T.POISSON7)
+        mg = T.MGConfig(nl, 2, T.EST_LANCZOS, telescope=tele)
+        mine = T.plan_summary(n_ranks, world, rank, prob, mg)
+        allp = [None] * world
+        dist.all_gather_object(allp, mine)
+        ok = True
+        msgs = []
+        # send/recv symmetry
+        sends = {}
+        recvs = {}
+        for p, recs in enumerate(allp):
+            for (pid, kind, peer, cnt, cs, lvl) in recs:
+                if kind == 0:
+                    sends[(pid, p, peer)] = (cnt, cs)
+                elif kind == 1:
+                    recvs[(pid, peer, p)] = (cnt, cs)
+        if sends != recvs:
+            ok = False
+            msgs.append(f"send/recv mismatch {sorted(set(sends) ^ set(recvs))[:5]}")
+        # totals per plan: halo plans vs box halos (one box per process here)
+        tot = {}
+        for p, recs in enumerate(allp):
+            for (pid, kind, peer, cnt, cs, lvl) in recs:
+                if kind in (0, 2):
+                    tot[pid] = tot.get(pid, 0) + cnt
+        results[rank] = (ok, msgs, tot)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case_idx", range(len(CASES)))
+def test_plans_consistent_across_processes(case_idx):
+    n_ranks = CASES[case_idx][0]
+    world = n_ranks
+    mgr = mp.Manager()
+    results = mgr.dict()
+    mp.spawn(_worker, args=(world, _free_port(), case_idx, results), nprocs=world, join=True)
+    for r in range(world):
+        ok, msgs, tot = results[r]
+        assert ok, msgs
+    # independent expectation for the finest-level halo plan (node 0) and telescope transfers
+    _, np3, nl, tele = CASES[case_idx]
+    h = T.create_grid_header(n_ranks, np3)
+    exp = sum(_halo_expect(h, None).values())
+    tot = results[0][2]
+    assert tot.get(0, 0) == exp
+    # every telescope gather/scatter plan moves each vertex of its level exactly once
+    for pid, cnt in tot.items():
+        if pid % 3 in (1, 2):
+            lvl_n = None
+            # level of that plan: recover from records
+            for (p2, kind, peer, c2, cs, lvl) in T.plan_summary(n_ranks, world, 0, T.Problem(np3), T.MGConfig(
+                    nl, 2, T.EST_LANCZOS, telescope=tele)):
+                if p2 == pid:
+                    lvl_n = lvl
+                    break
+            hh = h
+            for _ in range(nl - 1 - lvl_n):
+                hh = T.coarsen(hh) if hh.n_ranks() == n_ranks else hh
+            assert cnt == hh.npoints[0] * hh.npoints[1] * hh.npoints[2]
+
+
+def test_plan_summary_single_process_is_all_local():
+    recs = T.plan_summary(8, 1, 0, T.Problem((33, 33, 33)), T.MGConfig(4, 2, telescope=[T.TelescopeStage(1, 8)]))
+    assert all(k == 2 for (_, k, _, _, _, _) in recs)
