@@ -121,6 +121,7 @@ typedef struct {
   const double *cheb_bounds; /* optional: [2*nlevels] (lo,hi) per level; NULL = estimate (solver.cpp:591) */
   int n_telescope;
   tmgx_telescope_stage telescope[TMGX_MAX_TELESCOPE];
+  int galerkin; /* -pc_mg_galerkin: levels below the finest are 2^-3 P^T A P (27-point), else rediscretised */
 } tmgx_mg_cfg;
 
 /* KrylovConfig (solver.hpp:27-37) subset on this path. */

@@ -52,6 +52,7 @@ class MGCfg(C.Structure):
         ("k_in", C.c_double),
         ("cheb_lo_fac", C.c_double),
         ("cheb_hi_fac", C.c_double),
+        ("galerkin", C.c_int),
     ]
 
 
@@ -100,6 +101,7 @@ def lib():
         L.orc_mg_level_n.argtypes = [C.c_void_p, C.c_int, I64]
         L.orc_mg_bounds.argtypes = [C.c_void_p, C.c_int, D, D]
         L.orc_mg_coeff.argtypes = [C.c_void_p, C.c_int, D]
+        L.orc_mg_stencil27.argtypes = [C.c_void_p, C.c_int, D]
         L.orc_rhs.argtypes = [I64, C.c_uint64, D]
         L.orc_fill_random.argtypes = [C.c_int64, C.c_uint64, D]
         for fn in ("orc_apply", "orc_jacobi", "orc_smooth", "orc_restrict", "orc_prolong_add", "orc_vcycle"):
@@ -198,7 +200,7 @@ class MG:
     """1-rank MG hierarchy (level 0 = coarsest, LU)."""
 
     def __init__(self, np3, nlevels, kind=POISSON7, smooth_its=2, est_mode=EST_LANCZOS,
-                 zero_coarse_bc=0, seed_k=7, n_spheres=32, k_in=1e4):
+                 zero_coarse_bc=0, seed_k=7, n_spheres=32, k_in=1e4, galerkin=False):
         cfg = MGCfg()
         cfg.kind = kind
         cfg.np = (C.c_int64 * 3)(*np3)
@@ -210,6 +212,7 @@ class MG:
         cfg.n_spheres = n_spheres
         cfg.k_in = k_in
         cfg.cheb_lo_fac, cfg.cheb_hi_fac = 0.1, 1.1
+        cfg.galerkin = int(galerkin)
         self.cfg = cfg
         self.nlevels = nlevels
         self.h = lib().orc_mg_create(C.byref(cfg))
@@ -239,6 +242,12 @@ class MG:
         out = np.zeros(self.level_size(level))
         lib().orc_mg_coeff(self.h, level, _dp(out))
         return out
+
+    def stencil27(self, level):
+        out = np.zeros(27 * self.level_size(level))
+        if not lib().orc_mg_stencil27(self.h, level, _dp(out)):
+            return None
+        return out.reshape(27, -1)
 
     def _lv(self, fn, level, x, out=None):
         x = np.ascontiguousarray(x, dtype=np.float64)

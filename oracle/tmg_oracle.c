@@ -312,6 +312,7 @@ typedef struct {
   double *diag;
   double *inv_diag; /* precond.cpp:179 */
   double lo, hi;    /* chebyshev interval */
+  double *S;        /* Galerkin level: 27 row coefficients, S[s*nv + v] (NULL = 7-point) */
 } orc_level;
 
 struct orc_mg {
@@ -406,6 +407,21 @@ static void level_build(const orc_mg_cfg *cfg, orc_level *L) {
 static void level_apply(const orc_level *L, const double *x, double *y) {
   const int64_t nx = L->n[0], ny = L->n[1], nz = L->n[2];
   const int64_t sy = nx, sz = nx * ny;
+  if (L->S) { /* 27-point Galerkin row, columns ascending (dz, dy, dx lexicographic) */
+    for (int64_t k = 0; k < nz; ++k)
+      for (int64_t j = 0; j < ny; ++j)
+        for (int64_t i = 0; i < nx; ++i) {
+          const int64_t v = i + nx * (j + ny * k);
+          double acc = 0.0;
+          for (int s = 0; s < 27; ++s) {
+            const int dz = s / 9 - 1, dy = (s / 3) % 3 - 1, dx = s % 3 - 1;
+            if (k + dz < 0 || k + dz >= nz || j + dy < 0 || j + dy >= ny || i + dx < 0 || i + dx >= nx) continue;
+            acc += L->S[s * L->nv + v] * x[v + dz * sz + dy * sy + dx];
+          }
+          y[v] = acc;
+        }
+    return;
+  }
   for (int64_t k = 0; k < nz; ++k)
     for (int64_t j = 0; j < ny; ++j)
       for (int64_t i = 0; i < nx; ++i) {
@@ -424,6 +440,76 @@ static void level_apply(const orc_level *L, const double *x, double *y) {
         }
         y[v] = acc;
       }
+}
+
+/* Row of a 7-point level as 27 slots (s = (dz+1)*9 + (dy+1)*3 + (dx+1)); zeros elsewhere. */
+static void row27_7pt(const orc_level *L, int64_t i, int64_t j, int64_t k, double a[27]) {
+  const int64_t nx = L->n[0], ny = L->n[1], nz = L->n[2];
+  const int64_t v = i + nx * (j + ny * k), sy = nx, sz = nx * ny;
+  for (int s = 0; s < 27; ++s) a[s] = 0.0;
+  a[13] = L->diag[v];
+  if (is_bnd(L, i, j, k)) return;
+  if (k - 1 > 0) a[4] = L->czp[v - sz];
+  if (j - 1 > 0) a[10] = L->cyp[v - sy];
+  if (i - 1 > 0) a[12] = L->cxp[v - 1];
+  if (i + 1 < nx - 1) a[14] = L->cxp[v];
+  if (j + 1 < ny - 1) a[16] = L->cyp[v];
+  if (k + 1 < nz - 1) a[22] = L->czp[v];
+}
+
+static double pw1(int64_t d) { return d == 0 ? 1.0 : ((d == 1 || d == -1) ? 0.5 : 0.0); }
+
+/* Galerkin coarse operator A_c = R A_f P with R = 2^-3 P^T (ptap, dist_matrix.cpp:462-468,
+ * with the SURVEY App. A-C6 restriction scaling), as 27-point rows. For each coarse row I and
+ * column slot J the terms are summed over the fine rows f of R's support (ascending natural)
+ * and the fine columns g of A's row f (ascending natural): (R(I,f) a(f,g)) P(g,J). */
+static void galerkin_build(const orc_level *F, orc_level *C) {
+  const int64_t cn = C->nv;
+  C->S = calloc((size_t)(27 * cn), sizeof(double));
+  for (int64_t K = 0; K < C->n[2]; ++K)
+    for (int64_t J = 0; J < C->n[1]; ++J)
+      for (int64_t I = 0; I < C->n[0]; ++I) {
+        double acc[27];
+        for (int t = 0; t < 27; ++t) acc[t] = 0.0;
+        for (int64_t fk = 2 * K - 1; fk <= 2 * K + 1; ++fk) {
+          if (fk < 0 || fk >= F->n[2]) continue;
+          for (int64_t fj = 2 * J - 1; fj <= 2 * J + 1; ++fj) {
+            if (fj < 0 || fj >= F->n[1]) continue;
+            for (int64_t fi = 2 * I - 1; fi <= 2 * I + 1; ++fi) {
+              if (fi < 0 || fi >= F->n[0]) continue;
+              const double wr = 0.125 * (pw1(fi - 2 * I) * pw1(fj - 2 * J) * pw1(fk - 2 * K));
+              double a[27];
+              if (F->S) {
+                const int64_t fv = fi + F->n[0] * (fj + F->n[1] * fk);
+                for (int s = 0; s < 27; ++s) a[s] = F->S[s * F->nv + fv];
+              } else {
+                row27_7pt(F, fi, fj, fk, a);
+              }
+              for (int s = 0; s < 27; ++s) {
+                const int64_t gk = fk + s / 9 - 1, gj = fj + (s / 3) % 3 - 1, gi = fi + s % 3 - 1;
+                if (gk < 0 || gk >= F->n[2] || gj < 0 || gj >= F->n[1] || gi < 0 || gi >= F->n[0]) continue;
+                const double ra = wr * a[s];
+                for (int t = 0; t < 27; ++t) {
+                  const int64_t cK = K + t / 9 - 1, cJ = J + (t / 3) % 3 - 1, cI = I + t % 3 - 1;
+                  const double wp = pw1(gi - 2 * cI) * pw1(gj - 2 * cJ) * pw1(gk - 2 * cK);
+                  if (wp != 0.0) acc[t] += ra * wp;
+                }
+              }
+            }
+          }
+        }
+        const int64_t cv = I + C->n[0] * (J + C->n[1] * K);
+        for (int t = 0; t < 27; ++t) C->S[t * cn + cv] = acc[t];
+        C->diag[cv] = acc[13];
+        C->inv_diag[cv] = 1.0 / acc[13];
+      }
+}
+
+int orc_mg_stencil27(const orc_mg *mg, int level, double *out) {
+  const orc_level *L = &mg->lev[level];
+  if (!L->S) return 0;
+  memcpy(out, L->S, sizeof(double) * 27 * L->nv);
+  return 1;
 }
 
 /* dist_vector.cpp:33-38 + comm.cpp:338-351 (1 rank: serial left fold) */
@@ -740,6 +826,7 @@ orc_mg *orc_mg_create(const orc_mg_cfg *cfg) {
     orc_level *L = &mg->lev[l];
     memcpy(L->n, n, sizeof n);
     level_build(cfg, L);
+    if (cfg->galerkin && l < mg->nl - 1) galerkin_build(&mg->lev[l + 1], L);
     if (l > 0) {
       for (int a = 0; a < 3; ++a) {
         if (n[a] < 3 || n[a] % 2 == 0) { orc_mg_destroy(mg); return NULL; }
@@ -756,7 +843,7 @@ void orc_mg_destroy(orc_mg *mg) {
   if (!mg) return;
   for (int l = 0; l < mg->nl; ++l) {
     orc_level *L = &mg->lev[l];
-    free(L->k); free(L->cxp); free(L->cyp); free(L->czp); free(L->diag); free(L->inv_diag);
+    free(L->k); free(L->cxp); free(L->cyp); free(L->czp); free(L->diag); free(L->inv_diag); free(L->S);
   }
   free(mg->lu); free(mg->piv);
   free(mg);

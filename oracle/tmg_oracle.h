@@ -72,6 +72,7 @@ typedef struct {
   int n_spheres;       /* 32 */
   double k_in;         /* 1e4 */
   double cheb_lo_fac, cheb_hi_fac; /* 0.1, 1.1 (solver.cpp:580) */
+  int galerkin;        /* 1: levels below the finest are 2^-3 P^T A P (ptap, dist_matrix.cpp:462-468) */
 } orc_mg_cfg;
 
 orc_mg *orc_mg_create(const orc_mg_cfg *cfg);
@@ -79,6 +80,9 @@ void orc_mg_destroy(orc_mg *mg);
 int64_t orc_mg_level_n(const orc_mg *mg, int level, int64_t np_out[3]);
 void orc_mg_bounds(const orc_mg *mg, int level, double *lo, double *hi);
 void orc_mg_coeff(const orc_mg *mg, int level, double *k_out); /* vertex coefficient field */
+/* 27-point row coefficients of a Galerkin level: out[s*n + v], s = (dz+1)*9+(dy+1)*3+(dx+1);
+ * returns 0 if the level is not Galerkin. */
+int orc_mg_stencil27(const orc_mg *mg, int level, double *out);
 
 void orc_rhs(const int64_t np[3], uint64_t seed, double *b);        /* f = 2u-1 interior, 0 boundary */
 void orc_fill_random(int64_t n, uint64_t seed, double *x);           /* dist_vector.cpp:61-65, natural key */

@@ -77,6 +77,7 @@ tmgx::MGDesc to_mg(const tmgx_mg_cfg* m) {
   md.nlevels = m->nlevels;
   md.m = m->smooth_its;
   md.est_mode = m->est_mode;
+  md.galerkin = m->galerkin != 0;
   if (m->cheb_bounds) md.bounds.assign(m->cheb_bounds, m->cheb_bounds + 2 * m->nlevels);
   if (m->n_telescope < 0 || m->n_telescope > TMGX_MAX_TELESCOPE) throw tmg::ConfigError("bad telescope count");
   for (int t = 0; t < m->n_telescope; ++t)

@@ -508,6 +508,7 @@ void Solver::build_nodes() {
     ranks_dev = arena.alloc_t<int>(D0.h.n_ranks());
     CK(cudaMemcpy(ranks_dev, D0.wr.data(), sizeof(int) * D0.wr.size(), cudaMemcpyHostToDevice));
   }
+  if (mgd.galerkin) build_galerkin();
   setup_coarse(nodes.back());
   CK(cudaStreamSynchronize(W.stream));
 
@@ -525,6 +526,39 @@ void Solver::build_nodes() {
   CK(cudaStreamSynchronize(W.stream));
 }
 
+// Galerkin coarse operators (mg_setup with galerkin; ptap dist_matrix.cpp:462-468):
+// every level below the finest gets 27-point rows 2^-3 P^T A P computed on the device from the
+// level above (whose 27 planes are halo-exchanged first). At a telescope stage the member
+// operator is the parent's rows moved with the gather plan, i.e. C3(i) A' = P-hat^T A P-hat
+// followed by row fusion, with no explicit permutation matrix.
+void Solver::build_galerkin() {
+  auto planes = [&](const Node& nd, int s) {
+    Field f;
+    for (size_t q = 0; q < nd.S.p.size(); ++q) f.p.push_back(nd.S.p[q] + (long long)s * nd.dist->geo[q].total);
+    return f;
+  };
+  for (size_t i = 1; i < nodes.size(); ++i) {
+    Node& nd = nodes[i];
+    Node& up = nodes[i - 1];
+    const Dist& D = *nd.dist;
+    if (nd.level == up.level && up.S.p.empty()) continue;  // telescope of the finest (7-point) level
+    for (const auto& g : D.geo) nd.S.p.push_back(arena.alloc(27 * g.total));
+    if (nd.level == up.level) {
+      for (int s = 0; s < 27; ++s) run_plan(W, up.gather, planes(up, s), planes(nd, s), true);
+    } else {
+      if (!up.S.p.empty())
+        for (int s = 0; s < 27; ++s) run_plan(W, up.halo, planes(up, s), planes(up, s), false);
+      for (size_t q = 0; q < D.local.size(); ++q)
+        W.cnt.launches += launch_galerkin(up.dist->geo[q], up.op[q], D.geo[q], nd.S.p[q], D.geo[q].total, W.stream);
+    }
+    for (size_t q = 0; q < D.local.size(); ++q) {
+      nd.op[q].S = nd.S.p[q];
+      nd.op[q].S_stride = D.geo[q].total;
+    }
+  }
+  CK(cudaStreamSynchronize(W.stream));
+}
+
 // LUPC (precond.cpp:220-229): dense LU of the coarse operator, factored on the host with
 // DenseLU::factor's partial pivoting (precond.cpp:11-48).
 void Solver::setup_coarse(Node& nd) {
@@ -534,14 +568,29 @@ void Solver::setup_coarse(Node& nd) {
   const int nx = g.ex, ny = g.ey, nz = g.ez;
   const int n = nx * ny * nz;
   nd.nc = n;
+  std::vector<double> a((size_t)n * n, 0.0);
+  if (!nd.S.p.empty()) {  // 27-point Galerkin rows from the device
+    std::vector<double> S((size_t)27 * g.total);
+    CK(cudaMemcpy(S.data(), nd.S.p[0], sizeof(double) * S.size(), cudaMemcpyDeviceToHost));
+    for (int k = 0; k < nz; ++k)
+      for (int j = 0; j < ny; ++j)
+        for (int i = 0; i < nx; ++i) {
+          const int v = i + nx * (j + ny * k);
+          const long long pv = g.base + i + g.px * j + g.pxy * k;
+          for (int s = 0; s < 27; ++s) {
+            const int dz = s / 9 - 1, dy = (s / 3) % 3 - 1, dx = s % 3 - 1;
+            if (k + dz < 0 || k + dz >= nz || j + dy < 0 || j + dy >= ny || i + dx < 0 || i + dx >= nx) continue;
+            a[(size_t)v * n + (v + dz * nx * ny + dy * nx + dx)] = S[(size_t)s * g.total + pv];
+          }
+        }
+  }
   const OpParams op = make_op(D.h);
   std::vector<double> kk((size_t)n);
   for (int k = 0; k < nz; ++k)
     for (int j = 0; j < ny; ++j)
       for (int i = 0; i < nx; ++i) kk[(size_t)(i + nx * (j + ny * k))] = host_k(D, i, j, k);
-  std::vector<double> a((size_t)n * n, 0.0);
   auto K = [&](int i, int j, int k) { return kk[(size_t)(i + nx * (j + ny * k))]; };
-  for (int k = 0; k < nz; ++k)
+  for (int k = 0; k < nz && nd.S.p.empty(); ++k)
     for (int j = 0; j < ny; ++j)
       for (int i = 0; i < nx; ++i) {
         const int v = i + nx * (j + ny * k);

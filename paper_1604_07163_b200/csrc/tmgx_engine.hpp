@@ -145,6 +145,7 @@ struct MGDesc {
   int est_mode = 1;  // 0 reference, 1 lanczos
   std::vector<double> bounds;  // optional 2*nlevels
   std::vector<TeleStage> tele;
+  bool galerkin = false;  // levels below the finest: 2^-3 P^T A P (27-point)
 };
 
 enum NodeKind { SMOOTH = 0, TELESCOPE = 1, COARSE = 2 };
@@ -166,6 +167,7 @@ struct Node {
   std::shared_ptr<Dist> dist;
   std::vector<OpParams> op;  // per local box
   Field kcoef, b, x, r, d, d2;
+  Field S;  // Galerkin: per box 27 planes of `total` doubles (empty: 7-point operator)
   RegionPlan halo;
   double lo = 0.1, hi = 1.1;
   // telescope
@@ -239,6 +241,7 @@ class Solver {
 
  private:
   void build_nodes();
+  void build_galerkin();
   void setup_coarse(Node& nd);
   double host_k(const Dist& D, long long gi, long long gj, long long gk) const;
 };

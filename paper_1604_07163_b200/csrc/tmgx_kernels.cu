@@ -286,6 +286,118 @@ __global__ void __launch_bounds__(kBX* kBY)
   }
 }
 
+// 27-point (Galerkin) rows: columns ascending = slots (dz, dy, dx) lexicographic; every slot
+// is multiplied (out-of-grid slots hold exact zeros and read zero ghosts), which equals the
+// reference CSR row loop over the stored entries. Same functors and tiles as k_march.
+__device__ __forceinline__ double row27(const BoxGeo& g, const double* __restrict__ S, long long st,
+                                        const double* __restrict__ u, long long v) {
+  double acc = 0.0;
+#pragma unroll
+  for (int s = 0; s < 27; ++s) {
+    const long long o = (long long)(s / 9 - 1) * g.pxy + (long long)((s / 3) % 3 - 1) * g.px + (s % 3 - 1);
+    acc += __ldg(S + s * st + v) * __ldg(u + v + o);
+  }
+  return acc;
+}
+
+template <class F>
+__global__ void __launch_bounds__(kBX* kBY) k_march27(BoxGeo g, OpParams op, const double* __restrict__ u, F f) {
+  __shared__ double sh[32];
+  double acc0 = 0.0, acc1 = 0.0;
+  const int i0 = 2 * (blockIdx.x * kBX + threadIdx.x), j = blockIdx.y * kBY + threadIdx.y;
+  if (i0 < g.ex && j < g.ey) {
+    const bool two = i0 + 1 < g.ex;
+    const int k0 = blockIdx.z * g.zc, k1 = min(k0 + g.zc, g.ez);
+    for (int k = k0; k < k1; ++k) {
+      const long long v = vidx(g, i0, j, k);
+      const typename F::In in = f.load(v);
+      typename F::Out out{};
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        if (q == 1 && !two) break;
+        const double au = row27(g, op.S, op.S_stride, u, v + q);
+        const double invd = 1.0 / __ldg(op.S + 13 * op.S_stride + v + q);
+        f.point(q, au, invd, __ldg(u + v + q), in, out, acc0, acc1);
+      }
+      f.store(v, out, two);
+    }
+  }
+  if (F::kDots) {
+    const double s0 = block_sum(acc0, sh);
+    const double s1 = F::kDots > 1 ? block_sum(acc1, sh) : 0.0;
+    if (threadIdx.x == 0 && threadIdx.y == 0) f.partials(blk_linear(), s0, s1);
+  }
+}
+
+__device__ __forceinline__ double pw1(int d) { return d == 0 ? 1.0 : ((d == 1 || d == -1) ? 0.5 : 0.0); }
+
+// Galerkin product, one thread per coarse vertex I: for each fine row f of R's support
+// (ascending natural) and each column g of A's row f (ascending natural), add
+// (R(I,f) a(f,g)) P(g,J) to the coarse coefficient of column J (oracle galerkin_build order).
+template <bool FINE27, bool VAR>
+__global__ void __launch_bounds__(128) k_galerkin(BoxGeo F, OpParams fop, BoxGeo Cg, double* __restrict__ Sc,
+                                                   long long cst) {
+  const int I = blockIdx.x * blockDim.x + threadIdx.x, J = blockIdx.y * blockDim.y + threadIdx.y;
+  const int K = blockIdx.z;
+  if (I >= Cg.ex || J >= Cg.ey) return;
+  const int GI = Cg.gx + I, GJ = Cg.gy + J, GK = Cg.gz + K;
+  double acc[27];
+#pragma unroll
+  for (int t = 0; t < 27; ++t) acc[t] = 0.0;
+  for (int fk = 2 * GK - 1; fk <= 2 * GK + 1; ++fk) {
+    if (fk < 0 || fk >= F.Nz) continue;
+    for (int fj = 2 * GJ - 1; fj <= 2 * GJ + 1; ++fj) {
+      if (fj < 0 || fj >= F.Ny) continue;
+      for (int fi = 2 * GI - 1; fi <= 2 * GI + 1; ++fi) {
+        if (fi < 0 || fi >= F.Nx) continue;
+        const double wr = 0.125 * (pw1(fi - 2 * GI) * pw1(fj - 2 * GJ) * pw1(fk - 2 * GK));
+        const long long fv = vidx(F, fi - F.gx, fj - F.gy, fk - F.gz);
+        double a[27];
+        if (FINE27) {
+#pragma unroll
+          for (int s = 0; s < 27; ++s) a[s] = __ldg(fop.S + s * fop.S_stride + fv);
+        } else {
+#pragma unroll
+          for (int s = 0; s < 27; ++s) a[s] = 0.0;
+          const Pt p = make_pt(F, fi - F.gx, fj - F.gy, fk - F.gz);
+          Coef c;
+          if (VAR) {
+            const double* Kf = fop.k;
+            c = coef_at<true>(fop, p, Kf[fv], Kf[fv - 1], Kf[fv + 1], Kf[fv - F.px], Kf[fv + F.px], Kf[fv - F.pxy],
+                              Kf[fv + F.pxy]);
+          } else {
+            c = coef_at<false>(fop, p, 0, 0, 0, 0, 0, 0, 0);
+          }
+          a[13] = c.dg;
+          if (!p.bnd) {
+            if (p.czm) a[4] = c.azm;
+            if (p.cym) a[10] = c.aym;
+            if (p.cxm) a[12] = c.axm;
+            if (p.cxp) a[14] = c.axp;
+            if (p.cyp) a[16] = c.ayp;
+            if (p.czp) a[22] = c.azp;
+          }
+        }
+#pragma unroll
+        for (int s = 0; s < 27; ++s) {
+          const int gk = fk + s / 9 - 1, gj = fj + (s / 3) % 3 - 1, gi = fi + s % 3 - 1;
+          if (gk < 0 || gk >= F.Nz || gj < 0 || gj >= F.Ny || gi < 0 || gi >= F.Nx) continue;
+          const double ra = wr * a[s];
+#pragma unroll
+          for (int t = 0; t < 27; ++t) {
+            const int cK = GK + t / 9 - 1, cJ = GJ + (t / 3) % 3 - 1, cI = GI + t % 3 - 1;
+            const double wp = pw1(gi - 2 * cI) * pw1(gj - 2 * cJ) * pw1(gk - 2 * cK);
+            if (wp != 0.0) acc[t] += ra * wp;
+          }
+        }
+      }
+    }
+  }
+  const long long cv = vidx(Cg, I, J, K);
+#pragma unroll
+  for (int t = 0; t < 27; ++t) Sc[t * cst + cv] = acc[t];
+}
+
 struct NoIn {};
 
 // y = A u  (MODE 0) or  y = b - A u  (MODE 1)     (spmv dist_matrix.cpp:182-224; residual)
@@ -405,6 +517,7 @@ struct FSpmvDot {
 
 template <bool VAR>
 __device__ __forceinline__ double invd_at(const BoxGeo& g, const OpParams& op, int i, int j, int k, long long v) {
+  if (op.S) return 1.0 / op.S[13 * op.S_stride + v];
   if (!VAR) return op.cinvd;
   const Pt p = make_pt(g, i, j, k);
   const double* K = op.k;
@@ -781,7 +894,9 @@ int launch_cheb_start_zero(const BoxGeo& g, const OpParams& op, const double* b,
 
 template <class F>
 static void march(const BoxGeo& g, const OpParams& op, const double* u, const F& f, cudaStream_t s) {
-  if (op.k)
+  if (op.S)
+    k_march27<F><<<tile_grid(g), kBlock, 0, s>>>(g, op, u, f);
+  else if (op.k)
     k_march<true, F><<<tile_grid(g), kBlock, 0, s>>>(g, op, u, f);
   else
     k_march<false, F><<<tile_grid(g), kBlock, 0, s>>>(g, op, u, f);
@@ -817,6 +932,18 @@ int launch_restrict(const BoxGeo& fine, const BoxGeo& coarse, const double* rf, 
 
 int launch_prolong_add(const BoxGeo& fine, const BoxGeo& coarse, const double* xc, double* xf, cudaStream_t s) {
   k_prolong_add<<<plane_grid(fine, 0), dim3(32, 4), 0, s>>>(fine, coarse, xc, xf);
+  return 1;
+}
+
+int launch_galerkin(const BoxGeo& fine, const OpParams& fop, const BoxGeo& coarse, double* Sc, long long cst,
+                    cudaStream_t s) {
+  const dim3 gr(plane_grid(coarse, 0));
+  if (fop.S)
+    k_galerkin<true, false><<<gr, dim3(32, 4), 0, s>>>(fine, fop, coarse, Sc, cst);
+  else if (fop.k)
+    k_galerkin<false, true><<<gr, dim3(32, 4), 0, s>>>(fine, fop, coarse, Sc, cst);
+  else
+    k_galerkin<false, false><<<gr, dim3(32, 4), 0, s>>>(fine, fop, coarse, Sc, cst);
   return 1;
 }
 

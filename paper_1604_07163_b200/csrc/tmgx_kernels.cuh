@@ -43,6 +43,8 @@ struct OpParams {
   double cdiag;             // constant-coefficient diagonal (sum of the six face terms)
   double cinvd;             // 1.0 / cdiag (precond.cpp:179)
   const double* k;          // vertex coefficient (padded layout, ghosts filled); nullptr = k == 1
+  const double* S;          // Galerkin level: 27 row-coefficient planes (slot s at S + s*S_stride)
+  long long S_stride;
 };
 
 struct Sphere {
@@ -88,6 +90,12 @@ int launch_apply(const BoxGeo& g, const OpParams& op, const double* x, double* y
 int launch_restrict(const BoxGeo& fine, const BoxGeo& coarse, const double* rf, double* bc, cudaStream_t s);
 // xf += P xc (xc needs a box halo incl. corners).
 int launch_prolong_add(const BoxGeo& fine, const BoxGeo& coarse, const double* xc, double* xf, cudaStream_t s);
+
+// Galerkin coarse operator (ptap, dist_matrix.cpp:462-468; R = 2^-3 P^T): 27-point rows of the
+// coarse box from the fine operator `fop` (7-point from k/constants, or 27-point planes with a
+// filled halo). Output planes Sc + s*c_stride.
+int launch_galerkin(const BoxGeo& fine, const OpParams& fop, const BoxGeo& coarse, double* Sc, long long c_stride,
+                    cudaStream_t s);
 
 // CG / estimator pieces; partials: per-block fp64 partial sums (deterministic tree).
 int grid_blocks(const BoxGeo& g);

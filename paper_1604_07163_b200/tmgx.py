@@ -58,7 +58,7 @@ class _Stage(C.Structure):
 class _MG(C.Structure):
     _fields_ = [("nlevels", C.c_int), ("smooth_its", C.c_int), ("est_mode", C.c_int),
                 ("cheb_bounds", C.POINTER(C.c_double)), ("n_telescope", C.c_int),
-                ("telescope", _Stage * MAX_TELESCOPE)]
+                ("telescope", _Stage * MAX_TELESCOPE), ("galerkin", C.c_int)]
 
 
 class _Ksp(C.Structure):
@@ -349,6 +349,7 @@ class MGConfig:
     est_mode: int = EST_LANCZOS
     cheb_bounds: Optional[Sequence[float]] = None
     telescope: List[TelescopeStage] = field(default_factory=list)
+    galerkin: bool = False  # -pc_mg_galerkin: 2^-3 P^T A P coarse operators (27-point)
 
 
 def nccl_unique_id(parity=False):
@@ -397,6 +398,7 @@ def _c_problem(problem: Problem):
 def _c_mg(mg: MGConfig):
     m = _MG()
     m.nlevels, m.smooth_its, m.est_mode = mg.nlevels, mg.smooth_its, mg.est_mode
+    m.galerkin = int(mg.galerkin)
     bounds = None
     if mg.cheb_bounds is not None:
         bounds = np.ascontiguousarray(mg.cheb_bounds, dtype=np.float64)

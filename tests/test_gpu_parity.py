@@ -44,15 +44,15 @@ def check(a, b, parity):
 
 
 def make(np3, nlevels, kind=T.POISSON7, m=2, est=T.EST_LANCZOS, parity=False, n_ranks=1, bounds=None,
-         telescope=(), hint=None, seed_k=7):
+         telescope=(), hint=None, seed_k=7, galerkin=False):
     w = T.World(n_ranks=n_ranks, parity=parity)
     s = T.SolverNode(w, T.Problem(np3, kind, proc_grid_hint=hint, seed_k=seed_k),
-                     T.MGConfig(nlevels, m, est, cheb_bounds=bounds, telescope=list(telescope)))
+                     T.MGConfig(nlevels, m, est, cheb_bounds=bounds, telescope=list(telescope), galerkin=galerkin))
     return w, s
 
 
-def oracle_mg(np3, nlevels, kind=O.POISSON7, m=2, est=O.EST_LANCZOS, seed_k=7):
-    return O.MG(np3, nlevels, kind=kind, smooth_its=m, est_mode=est, seed_k=seed_k)
+def oracle_mg(np3, nlevels, kind=O.POISSON7, m=2, est=O.EST_LANCZOS, seed_k=7, galerkin=False):
+    return O.MG(np3, nlevels, kind=kind, smooth_its=m, est_mode=est, seed_k=seed_k, galerkin=galerkin)
 
 
 def oracle_bounds(mg, nlevels):
@@ -285,3 +285,66 @@ def test_telescope_gather_scatter_maps():
     assert np.array_equal(y, want)
     back = s.telescope_scatter(0, y, n1)
     assert np.array_equal(back, x_par)
+
+
+# ------------------------------------------------------------------------ Galerkin levels
+@pytest.mark.parametrize("parity", [True, False])
+@pytest.mark.parametrize("kind", KINDS)
+def test_galerkin_operator_and_vcycle(parity, kind):
+    """27-point Galerkin rows (2^-3 P^T A P) built on the device: operator, smoother and V-cycle
+    bitwise equal to the oracle's ptap-semantics rows in the parity build."""
+    np3, nl = (33, 17, 33), 4
+    om = oracle_mg(np3, nl, kind[1], galerkin=True)
+    w, s = make(np3, nl, kind[0], parity=parity, bounds=oracle_bounds(om, nl), galerkin=True)
+    rng = np.random.default_rng(5)
+    for level in range(nl):
+        x = rng.standard_normal(om.level_size(level))
+        check(s.level_apply(level, x), om.apply(level, x), parity)
+    b = rng.standard_normal(om.level_size(2))
+    check(s.level_smooth(2, b), om.smooth(2, b), parity)
+    bf = O.rhs(np3, 42)
+    got, want = s.pc_apply(bf), om.vcycle(nl - 1, bf)
+    if parity:
+        assert np.array_equal(got, want)
+    else:
+        assert rel(got, want) < 1e-11
+
+
+@pytest.mark.parametrize("parity", [True, False])
+@pytest.mark.parametrize("kind,np3,nl,m", [(KINDS[0], (65, 65, 65), 5, 2), (KINDS[1], (33, 33, 33), 4, 3),
+                                           (KINDS[1], (65, 65, 33), 5, 2)])
+def test_galerkin_solve(parity, kind, np3, nl, m):
+    om = oracle_mg(np3, nl, kind[1], m=m, galerkin=True)
+    b = O.rhs(np3, 1234)
+    xo, orep = om.solve(b, rtol=1e-8)
+    w, s = make(np3, nl, kind[0], m=m, parity=parity, galerkin=True)
+    x, rep = s.solve(b, cfg=T.KrylovConfig("cg", rtol=1e-8))
+    assert rep.converged()
+    if parity:
+        assert rep.iterations == orep["iterations"]
+        assert np.array_equal(x, xo)
+        return
+    assert abs(rep.iterations - orep["iterations"]) <= 1
+    if rep.iterations != orep["iterations"]:
+        xo, orep = om.solve(b, rtol=0.0, max_its=rep.iterations)
+    assert rel(x, xo) < TOL_SOLUTION
+
+
+def test_galerkin_decomposed_telescoped_bitwise():
+    """Galerkin rows computed box by box (halo-exchanged 27-plane operators) and moved by the
+    telescope gather (C3(i): P-hat^T A P-hat + row fusion) give the 1-rank V-cycle bitwise."""
+    np3, nl = (33, 33, 33), 4
+    om = oracle_mg(np3, nl, O.VARCOEF7, galerkin=True)
+    bounds = oracle_bounds(om, nl)
+    b_nat = O.rhs(np3, 42)
+    w1, s1 = make(np3, nl, T.VARCOEF7_HARMONIC, parity=True, bounds=bounds, galerkin=True)
+    y1 = s1.pc_apply(b_nat)
+    assert np.array_equal(y1, om.vcycle(nl - 1, b_nat))
+    w8, s8 = make(np3, nl, T.VARCOEF7_HARMONIC, parity=True, n_ranks=8, bounds=bounds, galerkin=True,
+                  telescope=[T.TelescopeStage(2, 4), T.TelescopeStage(1, 2)])
+    h, _ = s8.level_info(nl - 1)
+    perm = T.rank_block_to_natural(h)
+    y8 = s8.pc_apply(b_nat[perm])
+    y8n = np.empty_like(y8)
+    y8n[perm] = y8
+    assert np.array_equal(y8n, y1)

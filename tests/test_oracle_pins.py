@@ -170,3 +170,39 @@ def test_interp_1d_and_lu_known_answers():
     # LU coarse solve exact: x = A ones -> ones
     A1 = mg.apply(0, np.ones(27))
     assert np.max(np.abs(mg.coarse_solve(A1) - 1.0)) < 1e-13
+
+
+def test_galerkin_pins():
+    # Galerkin coarse operators on cfg1 (65^3, 5 levels, V(2,2)) need 8 CG
+    # iterations with the fixed estimator and 21 with the shipped one.
+    b = O.rhs((65,) * 3, 42)
+    for est, its in ((O.EST_LANCZOS, 8), (O.EST_REFERENCE, 21)):
+        mg = O.MG((65,) * 3, 5, est_mode=est, galerkin=True)
+        _, rep = mg.solve(b, rtol=1e-8)
+        assert rep["iterations"] == its
+
+
+def test_galerkin_equals_dense_triple_product():
+    # SPEC.md ptap "[DERIVED: dense oracle]": the 27-point rows equal 2^-3 P^T A P formed densely
+    for kind in (O.POISSON7, O.VARCOEF7):
+        mg = O.MG((9, 9, 17), 3, kind=kind, galerkin=True, seed_k=3)
+        for fine in (2, 1):
+            nf, nc = mg.level_size(fine), mg.level_size(fine - 1)
+            A = np.zeros((nf, nf))
+            for c in range(nf):
+                e = np.zeros(nf)
+                e[c] = 1.0
+                A[:, c] = mg.apply(fine, e)
+            P = np.zeros((nf, nc))
+            for c in range(nc):
+                e = np.zeros(nc)
+                e[c] = 1.0
+                P[:, c] = mg.prolong_add(fine, e, np.zeros(nf))
+            Ac = 0.125 * P.T @ A @ P
+            Bc = np.zeros((nc, nc))
+            for c in range(nc):
+                e = np.zeros(nc)
+                e[c] = 1.0
+                Bc[:, c] = mg.apply(fine - 1, e)
+            assert np.max(np.abs(Ac - Bc)) <= 1e-13 * np.max(np.abs(Ac))
+            assert np.max(np.abs(Bc - Bc.T)) <= 1e-13 * np.max(np.abs(Bc))
