@@ -31,6 +31,10 @@ CONFIGS = {
     "cfg3": ((513, 513, 513), 8, 3, 1, 4, 1e-8),
     "cfg4w": ((257, 257, 257), 7, 2, 0, 4, 1e-8),
 }
+# Coarse operators: rediscretised (reference default) for constant k;
+# Galerkin 2^-3 P^T A P for the 1e4-contrast problem (with rediscretisation the reference
+# algorithm needs ~500 CG iterations at 513^3).
+GALERKIN = {"cfg3": True}
 SEED_F = 1234
 SEED_K = 7
 
@@ -168,6 +172,7 @@ def main():
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--est", default="lanczos", choices=["lanczos", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--galerkin", choices=["on", "off"], default=None)
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -205,7 +210,9 @@ def main():
     w = T.World(n_ranks=world, nproc=world, proc=rank, device=local, nccl_id=nccl_id)
     tele = [T.TelescopeStage(tele_level, world)] if (world > 1 and tele_level is not None) else []
     t0 = time.perf_counter()
-    s = T.SolverNode(w, T.Problem(np3, kind, seed_k=SEED_K), T.MGConfig(nlevels, m, est, telescope=tele))
+    galerkin = GALERKIN.get(args.config, False) if args.galerkin is None else args.galerkin == "on"
+    s = T.SolverNode(w, T.Problem(np3, kind, seed_k=SEED_K),
+                     T.MGConfig(nlevels, m, est, telescope=tele, galerkin=galerkin))
     t_setup = time.perf_counter() - t0
     cfg = T.KrylovConfig("cg", rtol=rtol)
     n_local = s.local_size()
@@ -286,7 +293,8 @@ def main():
             "data": "synthetic (seeded RHS, natural-index hash; BASELINE configs are synthetic)",
             "config": {"workload": f"{args.config}: {np3[0]}x{np3[1]}x{np3[2]} "
                                    f"{'var-coef' if kind else 'Poisson'} {nlevels}-level MG V({m},{m}) "
-                                   f"Cheb-Jacobi CG rtol {rtol:g}, est={args.est}",
+                                   f"Cheb-Jacobi CG rtol {rtol:g}, est={args.est}, "
+                                   f"coarse={'galerkin' if galerkin else 'rediscretised'}",
                        "global_batch": 1, "seq_len": np3[0],
                        "parallelism": f"box{world}" + (f"+telescope(L{tele_level},r{world})" if tele else ""),
                        "l2": "inputs larger than L2 (one fine vector = %.0f MB)" % (n_dof * 8 / 1e6),

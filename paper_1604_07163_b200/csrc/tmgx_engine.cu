@@ -478,7 +478,14 @@ void Solver::build_nodes() {
     }
     for (size_t q = 0; q < D.local.size(); ++q) {
       OpParams op = make_op(D.h);
-      if (prob.kind == 1) op.k = nd.kcoef.p[q];
+      if (prob.kind == 1) {
+        op.k = nd.kcoef.p[q];
+        // precomputed rows (D, FX, FY, FZ) used by the stencil passes of this level
+        double* fc = arena.alloc(4 * D.geo[q].total);
+        W.cnt.launches += launch_fill_faces(D.geo[q], op, fc, D.geo[q].total, W.stream);
+        op.fc = fc;
+        op.fc_stride = D.geo[q].total;
+      }
       nd.op.push_back(op);
       nblk_max = std::max(nblk_max, grid_blocks(D.geo[q]));
       staging_n = std::max<long long>(staging_n, D.local_unknowns());
@@ -549,7 +556,8 @@ void Solver::build_galerkin() {
       if (!up.S.p.empty())
         for (int s = 0; s < 27; ++s) run_plan(W, up.halo, planes(up, s), planes(up, s), false);
       for (size_t q = 0; q < D.local.size(); ++q)
-        W.cnt.launches += launch_galerkin(up.dist->geo[q], up.op[q], D.geo[q], nd.S.p[q], D.geo[q].total, W.stream);
+        W.cnt.launches += launch_galerkin(up.dist->geo[q], up.op[q], D.geo[q], nd.S.p[q], D.geo[q].total,
+                                          spheres_dev, (int)spheres.size(), prob.k_in, W.stream);
     }
     for (size_t q = 0; q < D.local.size(); ++q) {
       nd.op[q].S = nd.S.p[q];

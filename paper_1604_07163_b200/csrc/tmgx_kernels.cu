@@ -174,6 +174,19 @@ __device__ __forceinline__ double hashed_uniform(unsigned long long seed, unsign
 // k at every in-grid position of the padded box (incl. the ghost ring): the coefficient is a
 // pure function of the global vertex, so no exchange is needed (rediscretisation by injection,
 // SURVEY App. A-C7). The inside test uses explicitly unfused products (bit-exact with the oracle).
+__device__ double sphere_k(const BoxGeo& g, const Sphere* __restrict__ sph, int ns, double k_in, int gi, int gj,
+                           int gk) {
+  const double x = __dmul_rn((double)gi, 1.0 / (double)(g.Nx - 1));
+  const double y = __dmul_rn((double)gj, 1.0 / (double)(g.Ny - 1));
+  const double z = __dmul_rn((double)gk, 1.0 / (double)(g.Nz - 1));
+  for (int s = 0; s < ns; ++s) {
+    const double dx = __dadd_rn(x, -sph[s].cx), dy = __dadd_rn(y, -sph[s].cy), dz = __dadd_rn(z, -sph[s].cz);
+    const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+    if (d2 <= __dmul_rn(sph[s].r, sph[s].r)) return k_in;
+  }
+  return 1.0;
+}
+
 __global__ void k_fill_coeff(BoxGeo g, double* __restrict__ kf, const Sphere* __restrict__ sph, int ns,
                              double k_in, int varcoef) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x - 1;
@@ -182,21 +195,28 @@ __global__ void k_fill_coeff(BoxGeo g, double* __restrict__ kf, const Sphere* __
   if (i > g.ex || j > g.ey) return;
   const int gi = g.gx + i, gj = g.gy + j, gk = g.gz + k;
   if (gi < 0 || gj < 0 || gk < 0 || gi >= g.Nx || gj >= g.Ny || gk >= g.Nz) return;
-  double val = 1.0;
-  if (varcoef) {
-    const double x = __dmul_rn((double)gi, 1.0 / (double)(g.Nx - 1));
-    const double y = __dmul_rn((double)gj, 1.0 / (double)(g.Ny - 1));
-    const double z = __dmul_rn((double)gk, 1.0 / (double)(g.Nz - 1));
-    for (int s = 0; s < ns; ++s) {
-      const double dx = __dadd_rn(x, -sph[s].cx), dy = __dadd_rn(y, -sph[s].cy), dz = __dadd_rn(z, -sph[s].cz);
-      const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
-      if (d2 <= __dmul_rn(sph[s].r, sph[s].r)) {
-        val = k_in;
-        break;
-      }
-    }
+  kf[vidx(g, i, j, k)] = varcoef ? sphere_k(g, sph, ns, k_in, gi, gj, gk) : 1.0;
+}
+
+// FX/FY/FZ on [-1, e-1]^3 (the +face of every vertex whose row or whose +neighbour's row is
+// owned) and D on the owned box; every k read stays inside the filled ring.
+__global__ void k_fill_faces(BoxGeo g, OpParams op, double* __restrict__ fc, long long st) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x - 1;
+  const int j = blockIdx.y * blockDim.y + threadIdx.y - 1;
+  const int k = blockIdx.z - 1;
+  if (i >= g.ex || j >= g.ey || k >= g.ez) return;
+  const int gi = g.gx + i, gj = g.gy + j, gk = g.gz + k;
+  if (gi < 0 || gj < 0 || gk < 0) return;
+  const long long v = vidx(g, i, j, k);
+  const double* K = op.k;
+  const double kc = K[v];
+  fc[1 * st + v] = gi + 1 < g.Nx ? harm(kc, K[v + 1]) * op.ih2x : 0.0;
+  fc[2 * st + v] = gj + 1 < g.Ny ? harm(kc, K[v + g.px]) * op.ih2y : 0.0;
+  fc[3 * st + v] = gk + 1 < g.Nz ? harm(kc, K[v + g.pxy]) * op.ih2z : 0.0;
+  if (i >= 0 && j >= 0 && k >= 0) {
+    const Pt p = make_pt(g, i, j, k);
+    fc[v] = coef_at<true>(op, p, kc, K[v - 1], K[v + 1], K[v - g.px], K[v + g.px], K[v - g.pxy], K[v + g.pxy]).dg;
   }
-  kf[vidx(g, i, j, k)] = val;
 }
 
 __global__ void k_fill_rhs(BoxGeo g, double* __restrict__ b, unsigned long long seed, int bzero) {
@@ -231,38 +251,49 @@ __global__ void __launch_bounds__(kBX* kBY)
     const int k0 = blockIdx.z * g.zc, k1 = min(k0 + g.zc, g.ez);
     long long v = vidx(g, i0, j, k0);
     double2 um = ld2(u + v - g.pxy), uc = ld2(u + v), un = ld2(u + v + g.pxy);
-    double2 km{1.0, 1.0}, kc{1.0, 1.0}, kn{1.0, 1.0};
-    if (VAR) {
-      km = ld2(op.k + v - g.pxy);
-      kc = ld2(op.k + v);
-      kn = ld2(op.k + v + g.pxy);
-    }
+    // VAR: precomputed rows (fc planes D, FX, FY, FZ); the -z face comes from a z queue
+    const double *fD = op.fc, *fX = op.fc + op.fc_stride, *fY = op.fc + 2 * op.fc_stride,
+                 *fZ = op.fc + 3 * op.fc_stride;
+    double2 fzm{0.0, 0.0};
+    if (VAR) fzm = ld2(fZ + v - g.pxy);
     typename F::In in = f.load(v);
     for (int k = k0; k < k1; ++k, v += g.pxy) {
-      double2 unn{0.0, 0.0}, knn{1.0, 1.0};
+      double2 unn{0.0, 0.0};
       typename F::In inn{};
       if (k + 1 < k1) {  // prefetch the next plane
         unn = ld2(u + v + 2 * g.pxy);
-        if (VAR) knn = ld2(op.k + v + 2 * g.pxy);
         inn = f.load(v + g.pxy);
       }
       const double2 uym = ld2(u + v - g.px), uyp = ld2(u + v + g.px);
       const double uxl = __ldg(u + v - 1), uxr = __ldg(u + v + 2);
-      double2 kym{1.0, 1.0}, kyp{1.0, 1.0};
-      double kxl = 1.0, kxr = 1.0;
+      double2 dd{0.0, 0.0}, fx{0.0, 0.0}, fy{0.0, 0.0}, fym{0.0, 0.0}, fz{0.0, 0.0};
+      double fxl = 0.0;
       if (VAR) {
-        kym = ld2(op.k + v - g.px);
-        kyp = ld2(op.k + v + g.px);
-        kxl = __ldg(op.k + v - 1);
-        kxr = __ldg(op.k + v + 2);
+        dd = ld2(fD + v);
+        fx = ld2(fX + v);
+        fy = ld2(fY + v);
+        fym = ld2(fY + v - g.px);
+        fz = ld2(fZ + v);
+        fxl = __ldg(fX + v - 1);
       }
       typename F::Out out{};
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
         if (q == 1 && !two) break;
         const Pt p = make_pt(g, i0 + q, j, k);
-        const double kxm = q ? kc.x : kxl, kxp = q ? kxr : kc.y;
-        const Coef c = coef_at<VAR>(op, p, get(kc, q), kxm, kxp, get(kym, q), get(kyp, q), get(km, q), get(kn, q));
+        Coef c;
+        if (VAR) {
+          c.dg = get(dd, q);
+          c.invd = 1.0 / c.dg;
+          c.azm = -get(fzm, q);
+          c.aym = -get(fym, q);
+          c.axm = -(q ? fx.x : fxl);
+          c.axp = -get(fx, q);
+          c.ayp = -get(fy, q);
+          c.azp = -get(fz, q);
+        } else {
+          c = coef_at<false>(op, p, 0, 0, 0, 0, 0, 0, 0);
+        }
         const double uxm = q ? uc.x : uxl, uxp = q ? uxr : uc.y;
         const double au = row_apply(p, c, get(um, q), get(uym, q), uxm, get(uc, q), uxp, get(uyp, q), get(un, q));
         f.point(q, au, c.invd, get(uc, q), in, out, acc0, acc1);
@@ -271,11 +302,7 @@ __global__ void __launch_bounds__(kBX* kBY)
       um = uc;
       uc = un;
       un = unn;
-      if (VAR) {
-        km = kc;
-        kc = kn;
-        kn = knn;
-      }
+      if (VAR) fzm = fz;
       in = inn;
     }
   }
@@ -336,7 +363,14 @@ __device__ __forceinline__ double pw1(int d) { return d == 0 ? 1.0 : ((d == 1 ||
 // (R(I,f) a(f,g)) P(g,J) to the coarse coefficient of column J (oracle galerkin_build order).
 template <bool FINE27, bool VAR>
 __global__ void __launch_bounds__(128) k_galerkin(BoxGeo F, OpParams fop, BoxGeo Cg, double* __restrict__ Sc,
-                                                   long long cst) {
+                                                   long long cst, const Sphere* __restrict__ sph, int ns,
+                                                   double k_in) {
+  // k at a fine vertex given by local indices: stored ring, or (two cells out, for rows of
+  // ghost-ring vertices) evaluated from the coefficient function itself
+  auto Kat = [&](int li, int lj, int lk) -> double {
+    if (li >= -1 && li <= F.ex && lj >= -1 && lj <= F.ey && lk >= -1 && lk <= F.ez) return fop.k[vidx(F, li, lj, lk)];
+    return sphere_k(F, sph, ns, k_in, F.gx + li, F.gy + lj, F.gz + lk);
+  };
   const int I = blockIdx.x * blockDim.x + threadIdx.x, J = blockIdx.y * blockDim.y + threadIdx.y;
   const int K = blockIdx.z;
   if (I >= Cg.ex || J >= Cg.ey) return;
@@ -362,9 +396,9 @@ __global__ void __launch_bounds__(128) k_galerkin(BoxGeo F, OpParams fop, BoxGeo
           const Pt p = make_pt(F, fi - F.gx, fj - F.gy, fk - F.gz);
           Coef c;
           if (VAR) {
-            const double* Kf = fop.k;
-            c = coef_at<true>(fop, p, Kf[fv], Kf[fv - 1], Kf[fv + 1], Kf[fv - F.px], Kf[fv + F.px], Kf[fv - F.pxy],
-                              Kf[fv + F.pxy]);
+            const int li = fi - F.gx, lj = fj - F.gy, lk = fk - F.gz;
+            c = coef_at<true>(fop, p, Kat(li, lj, lk), Kat(li - 1, lj, lk), Kat(li + 1, lj, lk), Kat(li, lj - 1, lk),
+                              Kat(li, lj + 1, lk), Kat(li, lj, lk - 1), Kat(li, lj, lk + 1));
           } else {
             c = coef_at<false>(fop, p, 0, 0, 0, 0, 0, 0, 0);
           }
@@ -518,6 +552,7 @@ struct FSpmvDot {
 template <bool VAR>
 __device__ __forceinline__ double invd_at(const BoxGeo& g, const OpParams& op, int i, int j, int k, long long v) {
   if (op.S) return 1.0 / op.S[13 * op.S_stride + v];
+  if (op.fc) return 1.0 / op.fc[v];
   if (!VAR) return op.cinvd;
   const Pt p = make_pt(g, i, j, k);
   const double* K = op.k;
@@ -878,6 +913,11 @@ int launch_fill_coeff(const BoxGeo& g, double* k, const Sphere* sph, int ns, dou
   return 1;
 }
 
+int launch_fill_faces(const BoxGeo& g, const OpParams& op, double* fc, long long st, cudaStream_t s) {
+  k_fill_faces<<<plane_grid(g, 1), dim3(32, 4), 0, s>>>(g, op, fc, st);
+  return 1;
+}
+
 int launch_fill_rhs(const BoxGeo& g, double* b, unsigned long long seed, bool bzero, cudaStream_t s) {
   k_fill_rhs<<<plane_grid(g, 0), dim3(32, 4), 0, s>>>(g, b, seed, bzero ? 1 : 0);
   return 1;
@@ -896,7 +936,7 @@ template <class F>
 static void march(const BoxGeo& g, const OpParams& op, const double* u, const F& f, cudaStream_t s) {
   if (op.S)
     k_march27<F><<<tile_grid(g), kBlock, 0, s>>>(g, op, u, f);
-  else if (op.k)
+  else if (op.fc)
     k_march<true, F><<<tile_grid(g), kBlock, 0, s>>>(g, op, u, f);
   else
     k_march<false, F><<<tile_grid(g), kBlock, 0, s>>>(g, op, u, f);
@@ -936,14 +976,14 @@ int launch_prolong_add(const BoxGeo& fine, const BoxGeo& coarse, const double* x
 }
 
 int launch_galerkin(const BoxGeo& fine, const OpParams& fop, const BoxGeo& coarse, double* Sc, long long cst,
-                    cudaStream_t s) {
+                    const Sphere* sph, int ns, double k_in, cudaStream_t s) {
   const dim3 gr(plane_grid(coarse, 0));
   if (fop.S)
-    k_galerkin<true, false><<<gr, dim3(32, 4), 0, s>>>(fine, fop, coarse, Sc, cst);
+    k_galerkin<true, false><<<gr, dim3(32, 4), 0, s>>>(fine, fop, coarse, Sc, cst, sph, ns, k_in);
   else if (fop.k)
-    k_galerkin<false, true><<<gr, dim3(32, 4), 0, s>>>(fine, fop, coarse, Sc, cst);
+    k_galerkin<false, true><<<gr, dim3(32, 4), 0, s>>>(fine, fop, coarse, Sc, cst, sph, ns, k_in);
   else
-    k_galerkin<false, false><<<gr, dim3(32, 4), 0, s>>>(fine, fop, coarse, Sc, cst);
+    k_galerkin<false, false><<<gr, dim3(32, 4), 0, s>>>(fine, fop, coarse, Sc, cst, sph, ns, k_in);
   return 1;
 }
 

@@ -45,6 +45,11 @@ struct OpParams {
   const double* k;          // vertex coefficient (padded layout, ghosts filled); nullptr = k == 1
   const double* S;          // Galerkin level: 27 row-coefficient planes (slot s at S + s*S_stride)
   long long S_stride;
+  // Variable k, precomputed rows: planes D (diagonal), FX, FY, FZ (+x/+y/+z face terms
+  // harm(k_v, k_nb)/h^2) at fc + {0,1,2,3}*fc_stride; the -x/-y/-z faces are the neighbours'
+  // +faces. Same values as evaluating from k, without the six divisions per row.
+  const double* fc;
+  long long fc_stride;
 };
 
 struct Sphere {
@@ -70,6 +75,8 @@ struct PtrTable {
 // ---- launchers (all asynchronous on `s`; return number of kernels launched) ----
 int launch_fill_coeff(const BoxGeo& g, double* k, const Sphere* spheres_dev, int n_spheres, double k_in,
                       bool varcoef, cudaStream_t s);
+// Face/diagonal planes of the variable-coefficient rows from op.k (ring filled) into fc.
+int launch_fill_faces(const BoxGeo& g, const OpParams& op, double* fc, long long fc_stride, cudaStream_t s);
 int launch_fill_rhs(const BoxGeo& g, double* b, unsigned long long seed, bool boundary_zero, cudaStream_t s);
 
 // Chebyshev(Jacobi) smoother pieces (solver.cpp:79-110 + precond.cpp:183-185).
@@ -95,7 +102,7 @@ int launch_prolong_add(const BoxGeo& fine, const BoxGeo& coarse, const double* x
 // coarse box from the fine operator `fop` (7-point from k/constants, or 27-point planes with a
 // filled halo). Output planes Sc + s*c_stride.
 int launch_galerkin(const BoxGeo& fine, const OpParams& fop, const BoxGeo& coarse, double* Sc, long long c_stride,
-                    cudaStream_t s);
+                    const Sphere* sph, int n_spheres, double k_in, cudaStream_t s);
 
 // CG / estimator pieces; partials: per-block fp64 partial sums (deterministic tree).
 int grid_blocks(const BoxGeo& g);

@@ -9,18 +9,20 @@ sys.path.insert(0, ROOT)
 
 import torch  # noqa: E402
 
-from bench import CONFIGS, SEED_F, SEED_K  # noqa: E402
+from bench import CONFIGS, GALERKIN, SEED_F, SEED_K  # noqa: E402
 from paper_1604_07163_b200 import tmgx as T  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="cfg2")
 ap.add_argument("--warmup", type=int, default=2)
+ap.add_argument("--max-its", type=int, default=10000)
 args = ap.parse_args()
 np3, nl, m, kind, tele, rtol = CONFIGS[args.config]
 torch.cuda.set_device(0)
 w = T.World(1)
-s = T.SolverNode(w, T.Problem(np3, kind, seed_k=SEED_K), T.MGConfig(nl, m, T.EST_LANCZOS))
-cfg = T.KrylovConfig("cg", rtol=rtol)
+s = T.SolverNode(w, T.Problem(np3, kind, seed_k=SEED_K),
+                 T.MGConfig(nl, m, T.EST_LANCZOS, galerkin=GALERKIN.get(args.config, False)))
+cfg = T.KrylovConfig("cg", rtol=rtol, max_its=args.max_its)
 for _ in range(args.warmup):
     s.solve_seeded(SEED_F, cfg=cfg)
 torch.cuda.synchronize()
