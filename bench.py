@@ -139,8 +139,10 @@ def cpu_reference_sample(steps=1, warmup=0, np3=(129, 129, 129), nlevels=6, m=2)
         t = sum(ts) / len(ts)
         kind = "port"
         its = rep["iterations"]
+    impl = ("reference translation units + SPEC glue (oracle/_ref/tmg_ref_bench)" if kind == "reference"
+            else "oracle C restatement (oracle/liboracle.so)")
     desc = (f"{np3[0]}x{np3[1]}x{np3[2]} Poisson, {nlevels}-level MG V({m},{m}) Cheb-Jacobi CG rtol 1e-8, "
-            f"{its} its, 1 core, solve only (setup excluded)")
+            f"{its} its, 1 core, solve only (setup excluded), {impl}")
     return n / t, t, kind, desc
 
 
