@@ -360,6 +360,7 @@ static OpParams make_op(const tmg::GridHeader& h) {
 Solver::Solver(World& W_, const ProblemDesc& P, const MGDesc& M) : W(W_), prob(P), mgd(M) {
   CK(cudaSetDevice(W.device));
   if (const char* e = std::getenv("TMGX_GRAPHS")) use_graphs = std::string(e) != "0";
+  if (const char* e = std::getenv("TMGX_TB")) tb_enabled = std::string(e) != "0";
   if (mgd.nlevels < 1) throw tmg::ConfigError("mg: number of levels must be >= 1");
   if (mgd.m < 1) throw tmg::ConfigError("mg: smoother iterations must be >= 1");
   if (prob.kind == 1) {
@@ -721,6 +722,16 @@ void Solver::smooth(int i, bool zero_x) {
   double rho = 1.0 / sigma;
   const double s_theta = 1.0 / theta;
   const size_t nb = D.local.size();
+  if (use_tb(i)) {  // one temporally blocked kernel per side (bitwise identical arithmetic)
+    const double rho_new = 1.0 / (2.0 * sigma - rho);
+    const ChebStep cs{rho_new * rho, 2.0 * rho_new / delta};
+    if (!zero_x)  // the kernel reads x out of place; V-cycles hand it the prolongated x in r
+      for (size_t q = 0; q < nb; ++q) W.cnt.launches += launch_copy_interior(D.geo[q], nd.x.p[q], nd.r.p[q], W.stream);
+    for (size_t q = 0; q < nb; ++q)
+      W.cnt.launches += launch_cheb2_tb(D.geo[q], nd.op[q], nd.b.p[q], nd.r.p[q], nd.x.p[q], s_theta, cs, zero_x,
+                                        W.stream);
+    return;
+  }
   if (zero_x) {
     for (size_t q = 0; q < nb; ++q)
       W.cnt.launches += launch_cheb_start_zero(D.geo[q], nd.op[q], nd.b.p[q], m == 1 ? nd.x.p[q] : nd.d.p[q], s_theta,
@@ -775,9 +786,28 @@ void Solver::vcycle(int i) {
     W.cnt.launches += launch_restrict(D.geo[q], cn.dist->geo[q], nd.r.p[q], cn.b.p[q], W.stream);
   vcycle(i + 1);
   halo(i + 1, cn.x);
+  if (use_tb(i)) {  // prolongate out of place into r, then the blocked post-smooth r -> x
+    for (size_t q = 0; q < D.local.size(); ++q)
+      W.cnt.launches += launch_prolong_to(D.geo[q], cn.dist->geo[q], cn.x.p[q], nd.x.p[q], nd.r.p[q], W.stream);
+    const double theta = 0.5 * (nd.hi + nd.lo), delta = 0.5 * (nd.hi - nd.lo), sigma = theta / delta;
+    const double rho = 1.0 / sigma, rho_new = 1.0 / (2.0 * sigma - rho);
+    const ChebStep cs{rho_new * rho, 2.0 * rho_new / delta};
+    for (size_t q = 0; q < D.local.size(); ++q)
+      W.cnt.launches += launch_cheb2_tb(D.geo[q], nd.op[q], nd.b.p[q], nd.r.p[q], nd.x.p[q], 1.0 / theta, cs, false,
+                                        W.stream);
+    return;
+  }
   for (size_t q = 0; q < D.local.size(); ++q)
     W.cnt.launches += launch_prolong_add(D.geo[q], cn.dist->geo[q], cn.x.p[q], nd.x.p[q], W.stream);
   smooth(i, false);
+}
+
+// The temporally blocked m = 2 smoother runs on single-box levels of 7-point operators
+// (TMGX_TB=0 disables it).
+bool Solver::use_tb(int i) const {
+  const Node& nd = nodes[i];
+  return tb_enabled && mgd.m == 2 && nd.kind == SMOOTH && nd.dist->h.n_ranks() == 1 && !nd.dist->local.empty() &&
+         nd.op[0].S == nullptr;
 }
 
 void Solver::device_allreduce_ranksums(int nslots) {

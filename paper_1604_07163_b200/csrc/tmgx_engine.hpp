@@ -233,6 +233,8 @@ class Solver {
 
   // CG iteration as one CUDA graph (TMGX_GRAPHS=0 disables capture)
   bool use_graphs = true;
+  bool tb_enabled = true;  // temporally blocked V(2,2) smoother (TMGX_TB=0 disables)
+  bool use_tb(int i) const;
   cudaGraphExec_t iter_exec = nullptr;
   long long iter_launches = 0;
   void cg_dots(int op);

@@ -432,6 +432,145 @@ __global__ void __launch_bounds__(128) k_galerkin(BoxGeo F, OpParams fop, BoxGeo
   for (int t = 0; t < 27; ++t) Sc[t * cst + cv] = acc[t];
 }
 
+// ------------------------------------------------------------------------------------------
+// Temporally blocked Chebyshev, m = 2 (one kernel per smoothing side, solver.cpp:88-110):
+//   pass 1 on the tile grown by one vertex:  d0 = D^-1 (b - A x) / theta   (PRE: x = 0, r = b)
+//   pass 2 on the tile:                      x' = (x + d0) + (c1 d0 + c2 D^-1 (r - A d0))
+// x planes are staged in a 3-plane shared ring over the tile grown by two, d0 in a 3-plane
+// ring over the tile grown by one; the z direction is pipelined (pass 1 runs one plane ahead of
+// pass 2). Arithmetic is exactly that of k_cheb_start_res/_zero + k_cheb_step(last), so results
+// are bitwise identical; DRAM traffic is x, b in and x' out (24 B/pt; PRE 16 B/pt) instead of
+// 64 (PRE 40). Valid on single-box levels (pass 1 on the ring reads only in-grid vertices there).
+// ------------------------------------------------------------------------------------------
+constexpr int kTBX = 32, kTBY = 8;
+
+template <bool VAR>
+__device__ __forceinline__ Coef coef_fc(const BoxGeo& g, const OpParams& op, const Pt& p, long long v) {
+  if (!VAR) return coef_at<false>(op, p, 0, 0, 0, 0, 0, 0, 0);
+  const long long st = op.fc_stride;
+  Coef c;
+  c.dg = __ldg(op.fc + v);
+  c.invd = 1.0 / c.dg;
+  c.azm = -__ldg(op.fc + 3 * st + v - g.pxy);
+  c.aym = -__ldg(op.fc + 2 * st + v - g.px);
+  c.axm = -__ldg(op.fc + 1 * st + v - 1);
+  c.axp = -__ldg(op.fc + 1 * st + v);
+  c.ayp = -__ldg(op.fc + 2 * st + v);
+  c.azp = -__ldg(op.fc + 3 * st + v);
+  return c;
+}
+
+template <bool VAR, bool PRE>
+__global__ void __launch_bounds__(kTBX* kTBY)
+    k_cheb2_tb(BoxGeo g, OpParams op, const double* __restrict__ b, const double* __restrict__ xin,
+               double* __restrict__ xout, double s_theta, double c1, double c2) {
+  constexpr int RX = kTBX + 4, RY = kTBY + 4;  // x ring: tile + 2
+  constexpr int DX = kTBX + 2, DY = kTBY + 2;  // d0 ring: tile + 1
+  __shared__ double xs[PRE ? 1 : 3][PRE ? 1 : RY][PRE ? 1 : RX];
+  __shared__ double ds[3][DY][DX];
+  __shared__ double rs[PRE ? 1 : 2][kTBY][kTBX];
+  const int tid = threadIdx.x + kTBX * threadIdx.y;
+  const int ox = blockIdx.x * kTBX, oy = blockIdx.y * kTBY;
+  const int k0 = blockIdx.z * g.zc, k1 = min(k0 + g.zc, g.ez);
+  auto in_grid = [&](int i, int j, int k) {
+    const int gi = g.gx + i, gj = g.gy + j, gk = g.gz + k;
+    return gi >= 0 && gj >= 0 && gk >= 0 && gi < g.Nx && gj < g.Ny && gk < g.Nz;
+  };
+  auto load_x = [&](int k) {  // x plane k into ring slot k mod 3 (tile + 2)
+    if (PRE) return;
+    const int sl = (k + 3) % 3;
+    for (int e = tid; e < RX * RY; e += kTBX * kTBY) {
+      const int lx = e % RX - 2, ly = e / RX - 2;
+      const int i = ox + lx, j = oy + ly;
+      double val = 0.0;
+      if (in_grid(i, j, k) && i >= -1 && i <= g.ex && j >= -1 && j <= g.ey && k >= -1 && k <= g.ez)
+        val = xin[vidx(g, i, j, k)];
+      xs[sl][ly + 2][lx + 2] = val;
+    }
+  };
+  auto xv = [&](int k, int lx, int ly) { return xs[(k + 3) % 3][ly + 2][lx + 2]; };
+  auto pass1 = [&](int k) {  // d0 plane k on tile + 1 (and r on the tile)
+    const int sl = (k + 3) % 3;
+    for (int e = tid; e < DX * DY; e += kTBX * kTBY) {
+      const int lx = e % DX - 1, ly = e / DX - 1;
+      const int i = ox + lx, j = oy + ly;
+      double d0 = 0.0;
+      if (in_grid(i, j, k) && i >= -1 && i <= g.ex && j >= -1 && j <= g.ey && k >= -1 && k <= g.ez) {
+        const long long v = vidx(g, i, j, k);
+        const Pt p = make_pt(g, i, j, k);
+        const Coef c = coef_fc<VAR>(g, op, p, v);
+        if (PRE) {
+          d0 = (b[v] * c.invd) * s_theta;
+        } else {
+          const double ax = row_apply(p, c, xv(k - 1, lx, ly), xv(k, lx, ly - 1), xv(k, lx - 1, ly), xv(k, lx, ly),
+                                      xv(k, lx + 1, ly), xv(k, lx, ly + 1), xv(k + 1, lx, ly));
+          const double rr = b[v] - ax;
+          d0 = (rr * c.invd) * s_theta;
+          if (lx >= 0 && ly >= 0 && lx < kTBX && ly < kTBY) rs[(k + 2) % 2][ly][lx] = rr;
+        }
+      }
+      ds[sl][ly + 1][lx + 1] = d0;
+    }
+  };
+  auto dv = [&](int k, int lx, int ly) { return ds[(k + 3) % 3][ly + 1][lx + 1]; };
+  // prologue: d0 planes k0-1 and k0
+  load_x(k0 - 2);
+  load_x(k0 - 1);
+  load_x(k0);
+  __syncthreads();
+  pass1(k0 - 1);
+  __syncthreads();
+  load_x(k0 + 1);
+  __syncthreads();
+  pass1(k0);
+  for (int k = k0; k < k1; ++k) {
+    __syncthreads();
+    load_x(k + 2);
+    __syncthreads();
+    pass1(k + 1);
+    __syncthreads();
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int i = ox + tx, j = oy + ty;
+    if (i < g.ex && j < g.ey) {
+      const long long v = vidx(g, i, j, k);
+      const Pt p = make_pt(g, i, j, k);
+      const Coef c = coef_fc<VAR>(g, op, p, v);
+      const double d0 = dv(k, tx, ty);
+      const double x1 = PRE ? d0 : xv(k, tx, ty) + d0;
+      const double ad = row_apply(p, c, dv(k - 1, tx, ty), dv(k, tx, ty - 1), dv(k, tx - 1, ty), d0, dv(k, tx + 1, ty),
+                                  dv(k, tx, ty + 1), dv(k + 1, tx, ty));
+      const double r0 = PRE ? b[v] : rs[(k + 2) % 2][ty][tx];
+      const double r1 = r0 - ad;
+      const double z = r1 * c.invd;
+      const double dn = c1 * d0 + c2 * z;
+      xout[v] = x1 + dn;
+    }
+  }
+}
+
+// out-of-place prolongation: xo = xf + P xc
+__global__ void k_prolong_to(BoxGeo F, BoxGeo Cg, const double* __restrict__ xc, const double* __restrict__ xf,
+                             double* __restrict__ xo) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y * blockDim.y + threadIdx.y;
+  const int k = blockIdx.z;
+  if (i >= F.ex || j >= F.ey) return;
+  const int fx = F.gx + i, fy = F.gy + j, fz = F.gz + k;
+  const int nx = 1 + (fx & 1), ny = 1 + (fy & 1), nz = 1 + (fz & 1);
+  const int cx0 = (fx >> 1) - Cg.gx, cy0 = (fy >> 1) - Cg.gy, cz0 = (fz >> 1) - Cg.gz;
+  const double wx = nx == 2 ? 0.5 : 1.0, wy = ny == 2 ? 0.5 : 1.0, wz = nz == 2 ? 0.5 : 1.0;
+  double acc = 0.0;
+  for (int tz = 0; tz < nz; ++tz)
+    for (int ty = 0; ty < ny; ++ty) {
+      const double* row = xc + vidx(Cg, cx0, cy0 + ty, cz0 + tz);
+      for (int tx = 0; tx < nx; ++tx) {
+        const double ww = wx * wy * wz;
+        acc += ww * __ldg(row + tx);
+      }
+    }
+  const long long v = vidx(F, i, j, k);
+  xo[v] = xf[v] + acc;
+}
+
 struct NoIn {};
 
 // y = A u  (MODE 0) or  y = b - A u  (MODE 1)     (spmv dist_matrix.cpp:182-224; residual)
@@ -962,6 +1101,30 @@ int launch_residual(const BoxGeo& g, const OpParams& op, const double* b, const 
 
 int launch_apply(const BoxGeo& g, const OpParams& op, const double* x, double* y, cudaStream_t s) {
   march(g, op, x, FApply<0>{nullptr, y}, s);
+  return 1;
+}
+
+int launch_cheb2_tb(const BoxGeo& g, const OpParams& op, const double* b, const double* xin, double* xout,
+                    double s_theta, ChebStep c, bool pre, cudaStream_t s) {
+  const dim3 gr((g.ex + kTBX - 1) / kTBX, (g.ey + kTBY - 1) / kTBY, (g.ez + g.zc - 1) / g.zc);
+  const dim3 bl(kTBX, kTBY);
+  if (op.fc) {
+    if (pre)
+      k_cheb2_tb<true, true><<<gr, bl, 0, s>>>(g, op, b, xin, xout, s_theta, c.c1, c.c2);
+    else
+      k_cheb2_tb<true, false><<<gr, bl, 0, s>>>(g, op, b, xin, xout, s_theta, c.c1, c.c2);
+  } else {
+    if (pre)
+      k_cheb2_tb<false, true><<<gr, bl, 0, s>>>(g, op, b, xin, xout, s_theta, c.c1, c.c2);
+    else
+      k_cheb2_tb<false, false><<<gr, bl, 0, s>>>(g, op, b, xin, xout, s_theta, c.c1, c.c2);
+  }
+  return 1;
+}
+
+int launch_prolong_to(const BoxGeo& fine, const BoxGeo& coarse, const double* xc, const double* xf, double* xo,
+                      cudaStream_t s) {
+  k_prolong_to<<<plane_grid(fine, 0), dim3(32, 4), 0, s>>>(fine, coarse, xc, xf, xo);
   return 1;
 }
 
