@@ -723,13 +723,12 @@ void Solver::smooth(int i, bool zero_x) {
   const double s_theta = 1.0 / theta;
   const size_t nb = D.local.size();
   if (use_tb(i)) {  // one temporally blocked kernel per side (bitwise identical arithmetic)
-    const double rho_new = 1.0 / (2.0 * sigma - rho);
-    const ChebStep cs{rho_new * rho, 2.0 * rho_new / delta};
-    if (!zero_x)  // the kernel reads x out of place; V-cycles hand it the prolongated x in r
-      for (size_t q = 0; q < nb; ++q) W.cnt.launches += launch_copy_interior(D.geo[q], nd.x.p[q], nd.r.p[q], W.stream);
+    const ChebStep cs = cheb_first_step(nd);
+    if (!zero_x)  // the kernel reads x out of place
+      for (size_t q = 0; q < nb; ++q) W.cnt.launches += launch_copy_interior(D.geo[q], nd.x.p[q], nd.d.p[q], W.stream);
     for (size_t q = 0; q < nb; ++q)
-      W.cnt.launches += launch_cheb2_tb(D.geo[q], nd.op[q], nd.b.p[q], nd.r.p[q], nd.x.p[q], s_theta, cs, zero_x,
-                                        W.stream);
+      W.cnt.launches += launch_cheb2_tb(D.geo[q], nd.op[q], nd.b.p[q], nd.d.p[q], nd.x.p[q], s_theta, cs, zero_x,
+                                        nullptr, nullptr, W.stream);
     return;
   }
   if (zero_x) {
@@ -777,6 +776,25 @@ void Solver::vcycle(int i) {
   }
   const Dist& D = *nd.dist;
   Node& cn = nodes[i + 1];
+  if (use_tb(i)) {
+    // blocked pre-smooth b -> d (x after pre-smoothing), residual, restriction, coarse
+    // correction, then the blocked post-smooth reads d + P x_c (prolongation fused) -> x
+    const ChebStep cs = cheb_first_step(nd);
+    const double s_theta = 1.0 / (0.5 * (nd.hi + nd.lo));
+    for (size_t q = 0; q < D.local.size(); ++q)
+      W.cnt.launches += launch_cheb2_tb(D.geo[q], nd.op[q], nd.b.p[q], nullptr, nd.d.p[q], s_theta, cs, true, nullptr,
+                                        nullptr, W.stream);
+    for (size_t q = 0; q < D.local.size(); ++q)
+      W.cnt.launches += launch_residual(D.geo[q], nd.op[q], nd.b.p[q], nd.d.p[q], nd.r.p[q], W.stream);
+    for (size_t q = 0; q < D.local.size(); ++q)
+      W.cnt.launches += launch_restrict(D.geo[q], cn.dist->geo[q], nd.r.p[q], cn.b.p[q], W.stream);
+    vcycle(i + 1);
+    halo(i + 1, cn.x);
+    for (size_t q = 0; q < D.local.size(); ++q)
+      W.cnt.launches += launch_cheb2_tb(D.geo[q], nd.op[q], nd.b.p[q], nd.d.p[q], nd.x.p[q], s_theta, cs, false,
+                                        cn.x.p[q], &cn.dist->geo[q], W.stream);
+    return;
+  }
   smooth(i, true);
   halo(i, nd.x);
   for (size_t q = 0; q < D.local.size(); ++q)
@@ -786,20 +804,19 @@ void Solver::vcycle(int i) {
     W.cnt.launches += launch_restrict(D.geo[q], cn.dist->geo[q], nd.r.p[q], cn.b.p[q], W.stream);
   vcycle(i + 1);
   halo(i + 1, cn.x);
-  if (use_tb(i)) {  // prolongate out of place into r, then the blocked post-smooth r -> x
-    for (size_t q = 0; q < D.local.size(); ++q)
-      W.cnt.launches += launch_prolong_to(D.geo[q], cn.dist->geo[q], cn.x.p[q], nd.x.p[q], nd.r.p[q], W.stream);
-    const double theta = 0.5 * (nd.hi + nd.lo), delta = 0.5 * (nd.hi - nd.lo), sigma = theta / delta;
-    const double rho = 1.0 / sigma, rho_new = 1.0 / (2.0 * sigma - rho);
-    const ChebStep cs{rho_new * rho, 2.0 * rho_new / delta};
-    for (size_t q = 0; q < D.local.size(); ++q)
-      W.cnt.launches += launch_cheb2_tb(D.geo[q], nd.op[q], nd.b.p[q], nd.r.p[q], nd.x.p[q], 1.0 / theta, cs, false,
-                                        W.stream);
-    return;
-  }
   for (size_t q = 0; q < D.local.size(); ++q)
     W.cnt.launches += launch_prolong_add(D.geo[q], cn.dist->geo[q], cn.x.p[q], nd.x.p[q], W.stream);
   smooth(i, false);
+}
+
+// First Chebyshev step coefficients (solver.cpp:90-93, 106-108) for the m = 2 blocked kernel.
+ChebStep Solver::cheb_first_step(const Node& nd) const {
+  const double theta = 0.5 * (nd.hi + nd.lo);
+  const double delta = 0.5 * (nd.hi - nd.lo);
+  const double sigma = theta / delta;
+  const double rho = 1.0 / sigma;
+  const double rho_new = 1.0 / (2.0 * sigma - rho);
+  return ChebStep{rho_new * rho, 2.0 * rho_new / delta};
 }
 
 // The temporally blocked m = 2 smoother runs on single-box levels of 7-point operators

@@ -235,6 +235,7 @@ class Solver {
   bool use_graphs = true;
   bool tb_enabled = true;  // temporally blocked V(2,2) smoother (TMGX_TB=0 disables)
   bool use_tb(int i) const;
+  ChebStep cheb_first_step(const Node& nd) const;
   cudaGraphExec_t iter_exec = nullptr;
   long long iter_launches = 0;
   void cg_dots(int op);

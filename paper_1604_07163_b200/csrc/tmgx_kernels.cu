@@ -463,10 +463,13 @@ __device__ __forceinline__ Coef coef_fc(const BoxGeo& g, const OpParams& op, con
 template <bool VAR, bool PRE>
 __global__ void __launch_bounds__(kTBX* kTBY)
     k_cheb2_tb(BoxGeo g, OpParams op, const double* __restrict__ b, const double* __restrict__ xin,
-               double* __restrict__ xout, double s_theta, double c1, double c2) {
+               double* __restrict__ xout, double s_theta, double c1, double c2, const double* __restrict__ xc,
+               BoxGeo Cg) {
   constexpr int RX = kTBX + 4, RY = kTBY + 4;  // x ring: tile + 2
   constexpr int DX = kTBX + 2, DY = kTBY + 2;  // d0 ring: tile + 1
-  __shared__ double xs[PRE ? 1 : 3][PRE ? 1 : RY][PRE ? 1 : RX];
+  constexpr int NT = kTBX * kTBY;
+  constexpr int XPER = (RX * RY + NT - 1) / NT;  // x-plane points staged per thread
+  __shared__ double xs[PRE ? 1 : 4][PRE ? 1 : RY][PRE ? 1 : RX];
   __shared__ double ds[3][DY][DX];
   __shared__ double rs[PRE ? 1 : 2][kTBY][kTBX];
   const int tid = threadIdx.x + kTBX * threadIdx.y;
@@ -476,26 +479,42 @@ __global__ void __launch_bounds__(kTBX* kTBY)
     const int gi = g.gx + i, gj = g.gy + j, gk = g.gz + k;
     return gi >= 0 && gj >= 0 && gk >= 0 && gi < g.Nx && gj < g.Ny && gk < g.Nz;
   };
-  auto load_x = [&](int k) {  // x plane k into ring slot k mod 3 (tile + 2)
-    if (PRE) return;
-    const int sl = (k + 3) % 3;
-    for (int e = tid; e < RX * RY; e += kTBX * kTBY) {
+  // x value staged for (i,j,k): xin (+ P xc when the V-cycle hands over the coarse correction,
+  // i.e. the prolongation x += P x_c fused into the staging; 0 outside the grid)
+  auto x_fetch = [&](int i, int j, int k) -> double {
+    if (!in_grid(i, j, k)) return 0.0;
+    const double xo = xin[vidx(g, i, j, k)];
+    if (!xc) return xo;
+    const int fx = g.gx + i, fy = g.gy + j, fz = g.gz + k;
+    const int nx = 1 + (fx & 1), ny = 1 + (fy & 1), nz = 1 + (fz & 1);
+    const int cx0 = (fx >> 1) - Cg.gx, cy0 = (fy >> 1) - Cg.gy, cz0 = (fz >> 1) - Cg.gz;
+    const double wx = nx == 2 ? 0.5 : 1.0, wy = ny == 2 ? 0.5 : 1.0, wz = nz == 2 ? 0.5 : 1.0;
+    double acc = 0.0;
+    for (int tz = 0; tz < nz; ++tz)
+      for (int ty = 0; ty < ny; ++ty) {
+        const double* row = xc + vidx(Cg, cx0, cy0 + ty, cz0 + tz);
+        for (int tx = 0; tx < nx; ++tx) {
+          const double ww = wx * wy * wz;
+          acc += ww * __ldg(row + tx);
+        }
+      }
+    return xo + acc;
+  };
+  auto stage_x = [&](int k) {  // direct (prologue)
+    const int sl = (k + 4) & 3;
+    for (int e = tid; e < RX * RY; e += NT) {
       const int lx = e % RX - 2, ly = e / RX - 2;
-      const int i = ox + lx, j = oy + ly;
-      double val = 0.0;
-      if (in_grid(i, j, k) && i >= -1 && i <= g.ex && j >= -1 && j <= g.ey && k >= -1 && k <= g.ez)
-        val = xin[vidx(g, i, j, k)];
-      xs[sl][ly + 2][lx + 2] = val;
+      xs[sl][ly + 2][lx + 2] = x_fetch(ox + lx, oy + ly, k);
     }
   };
-  auto xv = [&](int k, int lx, int ly) { return xs[(k + 3) % 3][ly + 2][lx + 2]; };
+  auto xv = [&](int k, int lx, int ly) { return xs[(k + 4) & 3][ly + 2][lx + 2]; };
   auto pass1 = [&](int k) {  // d0 plane k on tile + 1 (and r on the tile)
     const int sl = (k + 3) % 3;
-    for (int e = tid; e < DX * DY; e += kTBX * kTBY) {
+    for (int e = tid; e < DX * DY; e += NT) {
       const int lx = e % DX - 1, ly = e / DX - 1;
       const int i = ox + lx, j = oy + ly;
       double d0 = 0.0;
-      if (in_grid(i, j, k) && i >= -1 && i <= g.ex && j >= -1 && j <= g.ey && k >= -1 && k <= g.ez) {
+      if (in_grid(i, j, k)) {
         const long long v = vidx(g, i, j, k);
         const Pt p = make_pt(g, i, j, k);
         const Coef c = coef_fc<VAR>(g, op, p, v);
@@ -506,29 +525,41 @@ __global__ void __launch_bounds__(kTBX* kTBY)
                                       xv(k, lx + 1, ly), xv(k, lx, ly + 1), xv(k + 1, lx, ly));
           const double rr = b[v] - ax;
           d0 = (rr * c.invd) * s_theta;
-          if (lx >= 0 && ly >= 0 && lx < kTBX && ly < kTBY) rs[(k + 2) % 2][ly][lx] = rr;
+          if (lx >= 0 && ly >= 0 && lx < kTBX && ly < kTBY) rs[(k + 2) & 1][ly][lx] = rr;
         }
       }
       ds[sl][ly + 1][lx + 1] = d0;
     }
   };
   auto dv = [&](int k, int lx, int ly) { return ds[(k + 3) % 3][ly + 1][lx + 1]; };
-  // prologue: d0 planes k0-1 and k0
-  load_x(k0 - 2);
-  load_x(k0 - 1);
-  load_x(k0);
+  // prologue: x planes k0-2 .. k0+2, d0 planes k0-1, k0
+  if (!PRE) {
+    stage_x(k0 - 2);
+    stage_x(k0 - 1);
+    stage_x(k0);
+    stage_x(k0 + 1);
+  }
   __syncthreads();
   pass1(k0 - 1);
   __syncthreads();
-  load_x(k0 + 1);
-  __syncthreads();
+  if (!PRE) stage_x(k0 + 2);
   pass1(k0);
+  __syncthreads();
   for (int k = k0; k < k1; ++k) {
-    __syncthreads();
-    load_x(k + 2);
-    __syncthreads();
+    // (A) issue the loads of x plane k+3 into registers; they complete behind (B) and (C)
+    double pre[XPER];
+    if (!PRE) {
+#pragma unroll
+      for (int t = 0; t < XPER; ++t) {
+        const int e = tid + t * NT;
+        pre[t] = 0.0;
+        if (e < RX * RY && k + 3 < k1 + 2) pre[t] = x_fetch(ox + e % RX - 2, oy + e / RX - 2, k + 3);
+      }
+    }
+    // (B) pass 1 one plane ahead
     pass1(k + 1);
     __syncthreads();
+    // (C) pass 2 on the tile, plane k
     const int tx = threadIdx.x, ty = threadIdx.y;
     const int i = ox + tx, j = oy + ty;
     if (i < g.ex && j < g.ey) {
@@ -539,12 +570,21 @@ __global__ void __launch_bounds__(kTBX* kTBY)
       const double x1 = PRE ? d0 : xv(k, tx, ty) + d0;
       const double ad = row_apply(p, c, dv(k - 1, tx, ty), dv(k, tx, ty - 1), dv(k, tx - 1, ty), d0, dv(k, tx + 1, ty),
                                   dv(k, tx, ty + 1), dv(k + 1, tx, ty));
-      const double r0 = PRE ? b[v] : rs[(k + 2) % 2][ty][tx];
+      const double r0 = PRE ? b[v] : rs[(k + 2) & 1][ty][tx];
       const double r1 = r0 - ad;
       const double z = r1 * c.invd;
       const double dn = c1 * d0 + c2 * z;
       xout[v] = x1 + dn;
     }
+    // (D) x plane k+3 into the ring slot of plane k-1
+    if (!PRE) {
+#pragma unroll
+      for (int t = 0; t < XPER; ++t) {
+        const int e = tid + t * NT;
+        if (e < RX * RY) xs[(k + 3 + 4) & 3][e / RX][e % RX] = pre[t];
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -1105,19 +1145,20 @@ int launch_apply(const BoxGeo& g, const OpParams& op, const double* x, double* y
 }
 
 int launch_cheb2_tb(const BoxGeo& g, const OpParams& op, const double* b, const double* xin, double* xout,
-                    double s_theta, ChebStep c, bool pre, cudaStream_t s) {
+                    double s_theta, ChebStep c, bool pre, const double* xc, const BoxGeo* coarse, cudaStream_t s) {
+  const BoxGeo cg = coarse ? *coarse : g;
   const dim3 gr((g.ex + kTBX - 1) / kTBX, (g.ey + kTBY - 1) / kTBY, (g.ez + g.zc - 1) / g.zc);
   const dim3 bl(kTBX, kTBY);
   if (op.fc) {
     if (pre)
-      k_cheb2_tb<true, true><<<gr, bl, 0, s>>>(g, op, b, xin, xout, s_theta, c.c1, c.c2);
+      k_cheb2_tb<true, true><<<gr, bl, 0, s>>>(g, op, b, xin, xout, s_theta, c.c1, c.c2, xc, cg);
     else
-      k_cheb2_tb<true, false><<<gr, bl, 0, s>>>(g, op, b, xin, xout, s_theta, c.c1, c.c2);
+      k_cheb2_tb<true, false><<<gr, bl, 0, s>>>(g, op, b, xin, xout, s_theta, c.c1, c.c2, xc, cg);
   } else {
     if (pre)
-      k_cheb2_tb<false, true><<<gr, bl, 0, s>>>(g, op, b, xin, xout, s_theta, c.c1, c.c2);
+      k_cheb2_tb<false, true><<<gr, bl, 0, s>>>(g, op, b, xin, xout, s_theta, c.c1, c.c2, xc, cg);
     else
-      k_cheb2_tb<false, false><<<gr, bl, 0, s>>>(g, op, b, xin, xout, s_theta, c.c1, c.c2);
+      k_cheb2_tb<false, false><<<gr, bl, 0, s>>>(g, op, b, xin, xout, s_theta, c.c1, c.c2, xc, cg);
   }
   return 1;
 }
