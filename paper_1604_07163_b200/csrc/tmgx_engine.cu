@@ -823,8 +823,11 @@ ChebStep Solver::cheb_first_step(const Node& nd) const {
 // (TMGX_TB=0 disables it).
 bool Solver::use_tb(int i) const {
   const Node& nd = nodes[i];
-  return tb_enabled && mgd.m == 2 && nd.kind == SMOOTH && nd.dist->h.n_ranks() == 1 && !nd.dist->local.empty() &&
-         nd.op[0].S == nullptr;
+  if (!(tb_enabled && mgd.m == 2 && nd.kind == SMOOTH && nd.dist->h.n_ranks() == 1 && !nd.dist->local.empty() &&
+        nd.op[0].S == nullptr))
+    return false;
+  const bool coarse_ok = i + 1 < (int)nodes.size() && nodes[i + 1].kind != TELESCOPE && !nodes[i + 1].dist->geo.empty();
+  return cheb2_tb_supported(nd.dist->geo[0], coarse_ok ? &nodes[i + 1].dist->geo[0] : nullptr) && coarse_ok;
 }
 
 void Solver::device_allreduce_ranksums(int nslots) {

@@ -21,6 +21,17 @@
 
 #include <math.h>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <tuple>
+
 namespace tmgx {
 
 namespace {
@@ -434,21 +445,96 @@ __global__ void __launch_bounds__(128) k_galerkin(BoxGeo F, OpParams fop, BoxGeo
 
 // ------------------------------------------------------------------------------------------
 // Temporally blocked Chebyshev, m = 2 (one kernel per smoothing side, solver.cpp:88-110):
-//   pass 1 on the tile grown by one vertex:  d0 = D^-1 (b - A x) / theta   (PRE: x = 0, r = b)
-//   pass 2 on the tile:                      x' = (x + d0) + (c1 d0 + c2 D^-1 (r - A d0))
-// x planes are staged in a 3-plane shared ring over the tile grown by two, d0 in a 3-plane
-// ring over the tile grown by one; the z direction is pipelined (pass 1 runs one plane ahead of
-// pass 2). Arithmetic is exactly that of k_cheb_start_res/_zero + k_cheb_step(last), so results
-// are bitwise identical; DRAM traffic is x, b in and x' out (24 B/pt; PRE 16 B/pt) instead of
-// 64 (PRE 40). Valid on single-box levels (pass 1 on the ring reads only in-grid vertices there).
+//   pass 1:  d0 = D^-1 (b - A x~) / theta          (PRE, x = 0: d0 = D^-1 b / theta)
+//   pass 2:  x' = (x~ + d0) + (c1 d0 + c2 D^-1 (r0 - A d0))   (PRE: x~ = 0, r0 = b)
+// with x~ = x + P x_c when the V-cycle hands over the coarse correction (the prolongation
+// x += P x_c of grid.cpp:373-428 fused in) and x~ = x otherwise.
+//
+// Mapping: a 32 x 16 thread block is the pass-1 ring; each thread owns one (i, j) column of
+// it and marches z, so the z-neighbours of x~, d0 and r0 live in per-thread register queues
+// and only in-plane neighbours go through shared memory (one plane of x~ and one of d0, double
+// buffered: one __syncthreads per plane). The interior 30 x 14 threads also run pass 2 and
+// write x'. Pass 1 runs one plane behind the x~ staging, pass 2 one plane behind pass 1.
+// Loads are TMA box copies (cp.async.bulk.tensor.3d, one elected thread, mbarrier completion)
+// of the b plane over the ring, the raw x plane over the ring grown by one and the coarse x_c
+// plane under it, kTBPF planes ahead of use; out-of-array boxes are zero-filled by the TMA unit.
+// Arithmetic is exactly that of k_cheb_start_res/_zero + (k_prolong_add) + k_cheb_step(last),
+// so results are bitwise identical to the unfused path. Algorithmic DRAM traffic: x, b in,
+// x' out (24 B/pt, + 1 B/pt of x_c); PRE: b in, x' out (16 B/pt) -- instead of 64 + 17
+// (PRE 40) for the unfused passes. Valid on single-box levels: the ring's out-of-box vertices
+// are out of the grid and never enter the arithmetic (row_apply reads coupled neighbours only).
 // ------------------------------------------------------------------------------------------
-constexpr int kTBX = 32, kTBY = 8;
+constexpr int kTBX = 32, kTBY = 16, kTBNT = kTBX * kTBY;  // threads = pass-1 ring
+constexpr int kTBOX = kTBX - 2, kTBOY = kTBY - 2;          // output tile 30 x 14
+constexpr int kTBSX = kTBX + 2, kTBSY = kTBY + 2;          // staged x~ ring 34 x 18
+#ifndef TMGX_TB_PF
+#define TMGX_TB_PF 3
+#endif
+constexpr int kTBPF = TMGX_TB_PF;  // plane groups in flight
+constexpr int kTBNS = kTBPF + 1;   // plane slots
+constexpr int kTBCW = 20, kTBCH = 10, kTBNC = 4;  // coarse box: columns, rows; plane slots
+static_assert(kTBPF >= 1 && kTBPF <= 4, "the 4-slot coarse ring covers at most 4 planes in flight");
+// TMA box starts must be 16-byte aligned in x (even fp64 column): b is staged 34 wide from the
+// ring's column -1 (rows of the ring only), x from -1 with one extra row above/below.
+constexpr int kTBRawB = kTBSX * kTBSY * 8, kTBBB = kTBSX * kTBY * 8, kTBCB = kTBCW * kTBCH * 8;  // box bytes
+constexpr int tb_al128(int b) { return (b + 127) / 128 * 128; }
+
+template <bool PRE>
+struct alignas(128) TBSmem {
+  alignas(128) unsigned char b[kTBNS][tb_al128(kTBBB)];
+  alignas(128) unsigned char raw[PRE ? 1 : kTBNS][tb_al128(kTBRawB)];
+  alignas(128) unsigned char c[PRE ? 1 : kTBNC][tb_al128(kTBCB)];
+  double xt[PRE ? 1 : 2][kTBSY][kTBSX];
+  double d[2][kTBY][kTBX];
+  unsigned long long bar[kTBNS];
+};
+
+struct TBMaps {  // TMA descriptors (host-encoded, passed as __grid_constant__ parameters)
+  CUtensorMap b, x, c;
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "TB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra TB_DONE;\n"
+      "bra TB_WAIT;\n"
+      "TB_DONE:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load3(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                          unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::
+          "r"(smem_u32(dst)),
+      "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
 
 template <bool VAR>
-__device__ __forceinline__ Coef coef_fc(const BoxGeo& g, const OpParams& op, const Pt& p, long long v) {
-  if (!VAR) return coef_at<false>(op, p, 0, 0, 0, 0, 0, 0, 0);
-  const long long st = op.fc_stride;
+__device__ __forceinline__ Coef coef_fc(const BoxGeo& g, const OpParams& op, long long v) {
   Coef c;
+  if (!VAR) {
+    c.dg = op.cdiag;
+    c.invd = op.cinvd;
+    c.azm = c.azp = -op.ih2z;
+    c.aym = c.ayp = -op.ih2y;
+    c.axm = c.axp = -op.ih2x;
+    return c;
+  }
+  const long long st = op.fc_stride;
   c.dg = __ldg(op.fc + v);
   c.invd = 1.0 / c.dg;
   c.azm = -__ldg(op.fc + 3 * st + v - g.pxy);
@@ -460,131 +546,189 @@ __device__ __forceinline__ Coef coef_fc(const BoxGeo& g, const OpParams& op, con
   return c;
 }
 
+// Interior row (every coupling present): the same accumulation sequence as row_apply.
+__device__ __forceinline__ double row_full(const Coef& c, double uzm, double uym, double uxm, double uc, double uxp,
+                                           double uyp, double uzp) {
+  double acc = 0.0;
+  acc += c.azm * uzm;
+  acc += c.aym * uym;
+  acc += c.axm * uxm;
+  acc += c.dg * uc;
+  acc += c.axp * uxp;
+  acc += c.ayp * uyp;
+  acc += c.azp * uzp;
+  return acc;
+}
+
 template <bool VAR, bool PRE>
-__global__ void __launch_bounds__(kTBX* kTBY)
-    k_cheb2_tb(BoxGeo g, OpParams op, const double* __restrict__ b, const double* __restrict__ xin,
-               double* __restrict__ xout, double s_theta, double c1, double c2, const double* __restrict__ xc,
-               BoxGeo Cg) {
-  constexpr int RX = kTBX + 4, RY = kTBY + 4;  // x ring: tile + 2
-  constexpr int DX = kTBX + 2, DY = kTBY + 2;  // d0 ring: tile + 1
-  constexpr int NT = kTBX * kTBY;
-  constexpr int XPER = (RX * RY + NT - 1) / NT;  // x-plane points staged per thread
-  __shared__ double xs[PRE ? 1 : 4][PRE ? 1 : RY][PRE ? 1 : RX];
-  __shared__ double ds[3][DY][DX];
-  __shared__ double rs[PRE ? 1 : 2][kTBY][kTBX];
-  const int tid = threadIdx.x + kTBX * threadIdx.y;
-  const int ox = blockIdx.x * kTBX, oy = blockIdx.y * kTBY;
+__global__ void __launch_bounds__(kTBNT, 2)
+    k_cheb2_tb(const __grid_constant__ TBMaps maps, BoxGeo g, OpParams op, double* __restrict__ xout, double s_theta,
+               double c1, double c2, int fuse_p, BoxGeo Cg) {
+  extern __shared__ __align__(1024) unsigned char tb_smem_raw[];
+  TBSmem<PRE>& S = *reinterpret_cast<TBSmem<PRE>*>(tb_smem_raw);
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = tx + kTBX * ty;
+  const int ox = blockIdx.x * kTBOX, oy = blockIdx.y * kTBOY;
   const int k0 = blockIdx.z * g.zc, k1 = min(k0 + g.zc, g.ez);
-  auto in_grid = [&](int i, int j, int k) {
-    const int gi = g.gx + i, gj = g.gy + j, gk = g.gz + k;
-    return gi >= 0 && gj >= 0 && gk >= 0 && gi < g.Nx && gj < g.Ny && gk < g.Nz;
+  const int i = ox - 1 + tx, j = oy - 1 + ty;  // this thread's ring column
+  const int gi = g.gx + i, gj = g.gy + j;
+  const bool in_xy = gi >= 0 && gj >= 0 && gi < g.Nx && gj < g.Ny;
+  const bool fast_xy = gi >= 2 && gj >= 2 && gi <= g.Nx - 3 && gj <= g.Ny - 3;
+  const bool out_xy = tx >= 1 && ty >= 1 && tx <= kTBOX && ty <= kTBOY && i < g.ex && j < g.ey;
+  const long long vij = g.base + i + g.px * (long long)j;
+  auto in_z = [&](int k) { return g.gz + k >= 0 && g.gz + k < g.Nz; };
+  auto fast_z = [&](int k) { return g.gz + k >= 2 && g.gz + k <= g.Nz - 3; };
+
+  // plane schedule: step t stages x~(t) (POST), runs pass 1 on plane t - LAG1 and pass 2 on
+  // t - LAG1 - 1. Group t = {b(t - LAG1), raw x(t), coarse planes first needed by x~(t)}.
+  constexpr int LAG1 = PRE ? 0 : 1;
+  const int T0 = k0 - 1 - LAG1, T1 = k1 + LAG1;
+  const int cxs = (((g.gx + ox - 2) >> 1) - Cg.gx) & ~1;  // first staged coarse column (even) / row
+  const int cys = ((g.gy + oy - 2) >> 1) - Cg.gy;
+  auto slot = [&](int t) { return (t - T0) % kTBNS; };
+  auto parity = [&](int t) { return (unsigned)(((t - T0) / kTBNS) & 1); };
+  auto issue = [&](int t) {  // elected thread only
+    if (t > T1) return;
+    unsigned long long* bar = &S.bar[slot(t)];
+    const int pb = t - LAG1;
+    unsigned bytes = kTBBB;
+    int q0 = 0, nq = 0;
+    if (!PRE) {
+      bytes += kTBRawB;
+      if (fuse_p) {
+        const int fz = g.gz + t;
+        if (t == T0) q0 = (fz >> 1) - Cg.gz, nq = (fz & 1) ? 2 : 1;
+        else if (fz & 1) q0 = (fz >> 1) + 1 - Cg.gz, nq = 1;
+        bytes += nq * kTBCB;
+      }
+    }
+    mbar_expect_tx(bar, bytes);
+    tma_load3(S.b[slot(t)], &maps.b, kXO + ox - 2, oy, pb + 1, bar);
+    if (!PRE) {
+      tma_load3(S.raw[slot(t)], &maps.x, kXO + ox - 2, oy - 1, t + 1, bar);
+      for (int q = q0; q < q0 + nq; ++q) tma_load3(S.c[q & (kTBNC - 1)], &maps.c, kXO + cxs, cys + 1, q + 1, bar);
+    }
   };
-  // x value staged for (i,j,k): xin (+ P xc when the V-cycle hands over the coarse correction,
-  // i.e. the prolongation x += P x_c fused into the staging; 0 outside the grid)
-  auto x_fetch = [&](int i, int j, int k) -> double {
-    if (!in_grid(i, j, k)) return 0.0;
-    const double xo = xin[vidx(g, i, j, k)];
-    if (!xc) return xo;
-    const int fx = g.gx + i, fy = g.gy + j, fz = g.gz + k;
+  // x~ at staged ring position (lx, ly) of plane p: raw + P x_c in grid (k_prolong_add order), else 0
+  auto xtilde = [&](int p, int lx, int ly) -> double {
+    const int fx = g.gx + ox - 2 + lx, fy = g.gy + oy - 2 + ly, fz = g.gz + p;
+    if (fx < 0 || fy < 0 || fz < 0 || fx >= g.Nx || fy >= g.Ny || fz >= g.Nz) return 0.0;
+    const double* raw = reinterpret_cast<const double*>(S.raw[slot(p)]);
+    const double xo = raw[ly * kTBSX + lx];
+    if (!fuse_p) return xo;
     const int nx = 1 + (fx & 1), ny = 1 + (fy & 1), nz = 1 + (fz & 1);
-    const int cx0 = (fx >> 1) - Cg.gx, cy0 = (fy >> 1) - Cg.gy, cz0 = (fz >> 1) - Cg.gz;
+    const int cx0 = (fx >> 1) - Cg.gx - cxs, cy0 = (fy >> 1) - Cg.gy - cys, cz0 = (fz >> 1) - Cg.gz;
     const double wx = nx == 2 ? 0.5 : 1.0, wy = ny == 2 ? 0.5 : 1.0, wz = nz == 2 ? 0.5 : 1.0;
     double acc = 0.0;
-    for (int tz = 0; tz < nz; ++tz)
-      for (int ty = 0; ty < ny; ++ty) {
-        const double* row = xc + vidx(Cg, cx0, cy0 + ty, cz0 + tz);
-        for (int tx = 0; tx < nx; ++tx) {
-          const double ww = wx * wy * wz;
-          acc += ww * __ldg(row + tx);
+#pragma unroll
+    for (int tz = 0; tz < 2; ++tz) {
+      if (tz < nz) {
+        const double* cp = reinterpret_cast<const double*>(S.c[(cz0 + tz) & (kTBNC - 1)]);
+#pragma unroll
+        for (int uy = 0; uy < 2; ++uy) {
+          if (uy < ny) {
+#pragma unroll
+            for (int ux = 0; ux < 2; ++ux) {
+              if (ux < nx) {
+                const double ww = wx * wy * wz;
+                acc += ww * cp[(cy0 + uy) * kTBCW + cx0 + ux];
+              }
+            }
+          }
         }
       }
+    }
     return xo + acc;
   };
-  auto stage_x = [&](int k) {  // direct (prologue)
-    const int sl = (k + 4) & 3;
-    for (int e = tid; e < RX * RY; e += NT) {
-      const int lx = e % RX - 2, ly = e / RX - 2;
-      xs[sl][ly + 2][lx + 2] = x_fetch(ox + lx, oy + ly, k);
-    }
-  };
-  auto xv = [&](int k, int lx, int ly) { return xs[(k + 4) & 3][ly + 2][lx + 2]; };
-  auto pass1 = [&](int k) {  // d0 plane k on tile + 1 (and r on the tile)
-    const int sl = (k + 3) % 3;
-    for (int e = tid; e < DX * DY; e += NT) {
-      const int lx = e % DX - 1, ly = e / DX - 1;
-      const int i = ox + lx, j = oy + ly;
-      double d0 = 0.0;
-      if (in_grid(i, j, k)) {
-        const long long v = vidx(g, i, j, k);
-        const Pt p = make_pt(g, i, j, k);
-        const Coef c = coef_fc<VAR>(g, op, p, v);
-        if (PRE) {
-          d0 = (b[v] * c.invd) * s_theta;
-        } else {
-          const double ax = row_apply(p, c, xv(k - 1, lx, ly), xv(k, lx, ly - 1), xv(k, lx - 1, ly), xv(k, lx, ly),
-                                      xv(k, lx + 1, ly), xv(k, lx, ly + 1), xv(k + 1, lx, ly));
-          const double rr = b[v] - ax;
-          d0 = (rr * c.invd) * s_theta;
-          if (lx >= 0 && ly >= 0 && lx < kTBX && ly < kTBY) rs[(k + 2) & 1][ly][lx] = rr;
-        }
-      }
-      ds[sl][ly + 1][lx + 1] = d0;
-    }
-  };
-  auto dv = [&](int k, int lx, int ly) { return ds[(k + 3) % 3][ly + 1][lx + 1]; };
-  // prologue: x planes k0-2 .. k0+2, d0 planes k0-1, k0
-  if (!PRE) {
-    stage_x(k0 - 2);
-    stage_x(k0 - 1);
-    stage_x(k0);
-    stage_x(k0 + 1);
+
+  if (tid == 0) {
+    for (int s = 0; s < kTBNS; ++s) mbar_init(&S.bar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
-  pass1(k0 - 1);
-  __syncthreads();
-  if (!PRE) stage_x(k0 + 2);
-  pass1(k0);
-  __syncthreads();
-  for (int k = k0; k < k1; ++k) {
-    // (A) issue the loads of x plane k+3 into registers; they complete behind (B) and (C)
-    double pre[XPER];
+  if (tid == 0)
+    for (int s = 0; s < kTBPF; ++s) issue(T0 + s);
+
+  double b_prev = 0.0;                     // PRE: b of the pass-2 plane
+  double xq0 = 0.0, xq1 = 0.0, xq2 = 0.0;  // x~ at this column: planes t-2, t-1, t (POST)
+  double dq0 = 0.0, dq1 = 0.0, dq2 = 0.0;  // d0: pass-2 plane - 1, pass-2 plane, pass-2 plane + 1
+  double rq1 = 0.0, rq2 = 0.0;             // r0: pass-2 plane, pass-1 plane (POST)
+  for (int t = T0; t <= T1; ++t) {
+    const int p1 = t - LAG1, p2 = p1 - 1;  // pass-1 and pass-2 planes
+    mbar_wait(&S.bar[slot(t)], parity(t));
+    __syncthreads();  // slot of group t-1 is free; d / xt buffers of step t-2 are free
+    if (tid == 0) {
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      issue(t + kTBPF);
+    }
+    const double bown = reinterpret_cast<const double*>(S.b[slot(t)])[ty * kTBSX + tx + 1];
     if (!PRE) {
-#pragma unroll
-      for (int t = 0; t < XPER; ++t) {
-        const int e = tid + t * NT;
-        pre[t] = 0.0;
-        if (e < RX * RY && k + 3 < k1 + 2) pre[t] = x_fetch(ox + e % RX - 2, oy + e / RX - 2, k + 3);
+      // x~(t): own column into the register queue, the whole ring into S.xt[t & 1]
+      double(*xt)[kTBSX] = S.xt[t & 1];
+      xq2 = xtilde(t, tx + 1, ty + 1);
+      xt[ty + 1][tx + 1] = xq2;
+      if (tid < 2 * kTBSY + 2 * (kTBSX - 2)) {  // the 100 positions outside the thread ring
+        int lx, ly;
+        if (tid < 2 * kTBSY) {
+          lx = (tid & 1) ? kTBSX - 1 : 0;
+          ly = tid >> 1;
+        } else {
+          const int e = tid - 2 * kTBSY;
+          lx = 1 + (e >> 1);
+          ly = (e & 1) ? kTBSY - 1 : 0;
+        }
+        xt[ly][lx] = xtilde(t, lx, ly);
       }
     }
-    // (B) pass 1 one plane ahead
-    pass1(k + 1);
-    __syncthreads();
-    // (C) pass 2 on the tile, plane k
-    const int tx = threadIdx.x, ty = threadIdx.y;
-    const int i = ox + tx, j = oy + ty;
-    if (i < g.ex && j < g.ey) {
-      const long long v = vidx(g, i, j, k);
-      const Pt p = make_pt(g, i, j, k);
-      const Coef c = coef_fc<VAR>(g, op, p, v);
-      const double d0 = dv(k, tx, ty);
-      const double x1 = PRE ? d0 : xv(k, tx, ty) + d0;
-      const double ad = row_apply(p, c, dv(k - 1, tx, ty), dv(k, tx, ty - 1), dv(k, tx - 1, ty), d0, dv(k, tx + 1, ty),
-                                  dv(k, tx, ty + 1), dv(k + 1, tx, ty));
-      const double r0 = PRE ? b[v] : rs[(k + 2) & 1][ty][tx];
+    // pass 1 on plane p1 (this column)
+    if (p1 >= k0 - 1 && p1 <= k1) {
+      double d0 = 0.0, rr = 0.0;
+      if (in_xy && in_z(p1)) {
+        const long long v = vij + g.pxy * (long long)p1;
+        const Coef c = coef_fc<VAR>(g, op, v);
+        if (PRE) {
+          d0 = (bown * c.invd) * s_theta;
+        } else {
+          const double(*X)[kTBSX] = S.xt[p1 & 1];
+          const double xw = X[ty + 1][tx], xe = X[ty + 1][tx + 2], xs_ = X[ty][tx + 1], xn = X[ty + 2][tx + 1];
+          double ax;
+          if (fast_xy && fast_z(p1))
+            ax = row_full(c, xq0, xs_, xw, xq1, xe, xn, xq2);
+          else
+            ax = row_apply(make_pt(g, i, j, p1), c, xq0, xs_, xw, xq1, xe, xn, xq2);
+          rr = bown - ax;
+          d0 = (rr * c.invd) * s_theta;
+        }
+      }
+      dq2 = d0;
+      rq2 = rr;
+      S.d[p1 & 1][ty][tx] = d0;
+    }
+    // pass 2 on plane p2 (interior columns); d0 of p2's in-plane neighbours came from step t-1
+    if (out_xy && p2 >= k0 && p2 < k1) {
+      const long long v = vij + g.pxy * (long long)p2;
+      const Coef c = coef_fc<VAR>(g, op, v);
+      const double(*D)[kTBX] = S.d[p2 & 1];
+      const double d0 = dq1;
+      const double x1 = PRE ? d0 : xq0 + d0;
+      const double dw = D[ty][tx - 1], de = D[ty][tx + 1], ds = D[ty - 1][tx], dn_ = D[ty + 1][tx];
+      double ad;
+      if (fast_xy && fast_z(p2))
+        ad = row_full(c, dq0, ds, dw, d0, de, dn_, dq2);
+      else
+        ad = row_apply(make_pt(g, i, j, p2), c, dq0, ds, dw, d0, de, dn_, dq2);
+      const double r0 = PRE ? b_prev : rq1;
       const double r1 = r0 - ad;
       const double z = r1 * c.invd;
       const double dn = c1 * d0 + c2 * z;
       xout[v] = x1 + dn;
     }
-    // (D) x plane k+3 into the ring slot of plane k-1
-    if (!PRE) {
-#pragma unroll
-      for (int t = 0; t < XPER; ++t) {
-        const int e = tid + t * NT;
-        if (e < RX * RY) xs[(k + 3 + 4) & 3][e / RX][e % RX] = pre[t];
-      }
-    }
-    __syncthreads();
+    // rotate the queues
+    b_prev = bown;
+    dq0 = dq1;
+    dq1 = dq2;
+    rq1 = rq2;
+    xq0 = xq1;
+    xq1 = xq2;
   }
 }
 
@@ -1144,21 +1288,103 @@ int launch_apply(const BoxGeo& g, const OpParams& op, const double* x, double* y
   return 1;
 }
 
+// TMA descriptor of a padded box array (dims px x (ey+2) x (ez+2), fp64, zero fill outside),
+// cached per (array, box shape).
+static CUtensorMap tensor_map(const BoxGeo& g, const double* base_ptr, int bx, int by) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+  if (!enc) {
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&enc), cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        !enc)
+      throw std::runtime_error("cuTensorMapEncodeTiled unavailable");
+  }
+  struct Key {
+    const double* p;
+    long long px, ey, ez;
+    int bx, by;
+    bool operator<(const Key& o) const {
+      return std::tie(p, px, ey, ez, bx, by) < std::tie(o.p, o.px, o.ey, o.ez, o.bx, o.by);
+    }
+  };
+  static std::map<Key, CUtensorMap> cache;
+  const Key key{base_ptr, g.px, g.ey, g.ez, bx, by};
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  CUtensorMap m;
+  const cuuint64_t dims[3] = {(cuuint64_t)g.px, (cuuint64_t)(g.ey + 2), (cuuint64_t)(g.ez + 2)};
+  const cuuint64_t strides[2] = {(cuuint64_t)g.px * 8, (cuuint64_t)g.pxy * 8};
+  const cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, 1};
+  const cuuint32_t es[3] = {1, 1, 1};
+  const CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base_ptr), dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  cache.emplace(key, m);
+  return m;
+}
+
+// TMA boxes may not exceed the tensor (the TMA unit traps): the blocked smoother needs a level
+// at least 30 x 16 vertices across (and a coarse level at least 16 x 8 when fused).
+bool cheb2_tb_supported(const BoxGeo& g, const BoxGeo* coarse) {
+  if (g.px < kTBSX || g.ey + 2 < kTBSY) return false;
+  if (coarse && (coarse->px < kTBCW || coarse->ey + 2 < kTBCH)) return false;
+  return true;
+}
+
 int launch_cheb2_tb(const BoxGeo& g, const OpParams& op, const double* b, const double* xin, double* xout,
                     double s_theta, ChebStep c, bool pre, const double* xc, const BoxGeo* coarse, cudaStream_t s) {
   const BoxGeo cg = coarse ? *coarse : g;
-  const dim3 gr((g.ex + kTBX - 1) / kTBX, (g.ey + kTBY - 1) / kTBY, (g.ez + g.zc - 1) / g.zc);
+  TBMaps maps;
+  std::memset(&maps, 0, sizeof(maps));
+  maps.b = tensor_map(g, b, kTBSX, kTBY);
+  if (!pre) maps.x = tensor_map(g, xin, kTBSX, kTBSY);
+  if (!pre && xc) maps.c = tensor_map(cg, xc, kTBCW, kTBCH);
+  const int fuse = (!pre && xc) ? 1 : 0;
   const dim3 bl(kTBX, kTBY);
+  auto go = [&](auto kern, size_t smem, int& slots) {  // slots: resident blocks on the device
+    if (!slots) {
+      int dev = 0, sms = 0, per = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kTBNT, smem);
+      slots = std::max(1, sms * std::max(per, 1));
+    }
+    // z planes per block: minimise waves x (planes + 2-plane pipeline fill) over the split count
+    BoxGeo gt = g;
+    const long long cols = (long long)((g.ex + kTBOX - 1) / kTBOX) * ((g.ey + kTBOY - 1) / kTBOY);
+    static const int zc_env = [] {
+      const char* e = std::getenv("TMGX_TB_ZC");
+      return e ? std::max(1, std::atoi(e)) : 0;
+    }();
+    int best = g.ez;
+    if (zc_env) {
+      best = std::min(zc_env, g.ez);
+    } else {
+      long long best_cost = -1;
+      for (int nzb = 1; nzb <= g.ez; ++nzb) {
+        const int zc = (g.ez + nzb - 1) / nzb;
+        const long long waves = (cols * nzb + slots - 1) / slots;
+        const long long cost = waves * (zc + 3);
+        if (best_cost < 0 || cost < best_cost) best_cost = cost, best = zc;
+      }
+    }
+    gt.zc = best;
+    const dim3 gr((g.ex + kTBOX - 1) / kTBOX, (g.ey + kTBOY - 1) / kTBOY, (g.ez + gt.zc - 1) / gt.zc);
+    kern<<<gr, bl, smem, s>>>(maps, gt, op, xout, s_theta, c.c1, c.c2, fuse, cg);
+  };
+  static int slots[4] = {0, 0, 0, 0};
   if (op.fc) {
     if (pre)
-      k_cheb2_tb<true, true><<<gr, bl, 0, s>>>(g, op, b, xin, xout, s_theta, c.c1, c.c2, xc, cg);
+      go(k_cheb2_tb<true, true>, sizeof(TBSmem<true>), slots[0]);
     else
-      k_cheb2_tb<true, false><<<gr, bl, 0, s>>>(g, op, b, xin, xout, s_theta, c.c1, c.c2, xc, cg);
+      go(k_cheb2_tb<true, false>, sizeof(TBSmem<false>), slots[1]);
   } else {
     if (pre)
-      k_cheb2_tb<false, true><<<gr, bl, 0, s>>>(g, op, b, xin, xout, s_theta, c.c1, c.c2, xc, cg);
+      go(k_cheb2_tb<false, true>, sizeof(TBSmem<true>), slots[2]);
     else
-      k_cheb2_tb<false, false><<<gr, bl, 0, s>>>(g, op, b, xin, xout, s_theta, c.c1, c.c2, xc, cg);
+      go(k_cheb2_tb<false, false>, sizeof(TBSmem<false>), slots[3]);
   }
   return 1;
 }

@@ -94,6 +94,7 @@ int launch_cheb_step(const BoxGeo& g, const OpParams& op, const double* d, const
 // xout = S(b); post: xout = S(b, xin + P xc) with xin != xout (xc may be null: no prolongation).
 int launch_cheb2_tb(const BoxGeo& g, const OpParams& op, const double* b, const double* xin, double* xout,
                     double s_theta, ChebStep c, bool pre, const double* xc, const BoxGeo* coarse, cudaStream_t s);
+bool cheb2_tb_supported(const BoxGeo& g, const BoxGeo* coarse);
 // xo = xf + P xc (out of place)
 int launch_prolong_to(const BoxGeo& fine, const BoxGeo& coarse, const double* xc, const double* xf, double* xo,
                       cudaStream_t s);
