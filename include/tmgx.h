@@ -204,7 +204,8 @@ int tmgx_plan_summary(int n_ranks, int nproc, int proc, const tmgx_problem *prob
  * which: 0 cheb_step (full: read d,r,x write d',r,x) 1 cheb_step (last: read d,r,x write x)
  *        2 operator apply 3 residual 4 restriction 5 prolongation 6 cg_update 7 spmv+dot
  *        8 temporally blocked V(2,2) pre-smooth side (b in, x out)
- *        9 temporally blocked post-smooth side with the prolongation fused (x, b, x_c in, x out) */
+ *        9 temporally blocked post-smooth side (x, b in, x out)
+ *       10 out-of-place prolongation x~ = x + P x_c (x, x_c in, x~ out) */
 int tmgx_bench_kernel(tmgx_solver s, int which, int level, int iters, double *ms_per_launch,
                       double *bytes_per_launch);
 

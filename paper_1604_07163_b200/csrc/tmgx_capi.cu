@@ -495,8 +495,9 @@ extern "C" int tmgx_bench_kernel(tmgx_solver s, int which, int level, int iters,
           case 5: tmgx::launch_prolong_add(g, S.nodes[i + 1].dist->geo[q], S.nodes[i + 1].x.p[q], nd.x.p[q], S.W.stream); break;
           case 6: tmgx::launch_cg_update(g, nd.d.p[q], nd.d2.p[q], nd.x.p[q], nd.r.p[q], S.scal, tmgx::S_TMP1, tmgx::S_FLAG_PW, S.W.stream); break;
           case 7: tmgx::launch_spmv_dot(g, nd.op[q], nd.x.p[q], nd.b.p[q], S.part + S.part_off[q], S.W.stream); break;
-          case 8: tmgx::launch_cheb2_tb(g, nd.op[q], nd.b.p[q], nullptr, nd.d.p[q], 1.0, cs, true, nullptr, nullptr, S.W.stream); break;
-          case 9: tmgx::launch_cheb2_tb(g, nd.op[q], nd.b.p[q], nd.d.p[q], nd.x.p[q], 1.0, cs, false, S.nodes[i + 1].x.p[q], &S.nodes[i + 1].dist->geo[q], S.W.stream); break;
+          case 8: tmgx::launch_cheb2_tb(g, nd.op[q], nd.b.p[q], nullptr, nd.d.p[q], 1.0, cs, true, S.W.stream); break;
+          case 9: tmgx::launch_cheb2_tb(g, nd.op[q], nd.b.p[q], nd.d.p[q], nd.x.p[q], 1.0, cs, false, S.W.stream); break;
+          case 10: tmgx::launch_prolong_to(g, S.nodes[i + 1].dist->geo[q], S.nodes[i + 1].x.p[q], nd.d.p[q], nd.r.p[q], S.W.stream); break;
           default: throw tmg::Error("unknown kernel id");
         }
       }
@@ -511,7 +512,8 @@ extern "C" int tmgx_bench_kernel(tmgx_solver s, int which, int level, int iters,
       case 6: per_pt = 48; break;
       case 7: per_pt = 16 + kb; break;
       case 8: per_pt = 16 + kb; break;             // temporally blocked pre-smooth: b in, x out
-      case 9: per_pt = 24 + 8.0 / 8.0 + kb; break; // blocked post-smooth: x, b, x_c in, x out
+      case 9: per_pt = 24 + kb; break;             // blocked post-smooth: x, b in, x out
+      case 10: per_pt = 16 + 8.0 / 8.0; break;     // out-of-place prolongation: x, x_c in, x~ out
       default: throw tmg::Error("unknown kernel id");
     }
     tmgx::cuda_check(cudaMemsetAsync(S.scal, 0, sizeof(double) * tmgx::S_NSLOTS, S.W.stream), "memset");

@@ -728,7 +728,7 @@ void Solver::smooth(int i, bool zero_x) {
       for (size_t q = 0; q < nb; ++q) W.cnt.launches += launch_copy_interior(D.geo[q], nd.x.p[q], nd.d.p[q], W.stream);
     for (size_t q = 0; q < nb; ++q)
       W.cnt.launches += launch_cheb2_tb(D.geo[q], nd.op[q], nd.b.p[q], nd.d.p[q], nd.x.p[q], s_theta, cs, zero_x,
-                                        nullptr, nullptr, W.stream);
+                                        W.stream);
     return;
   }
   if (zero_x) {
@@ -778,12 +778,11 @@ void Solver::vcycle(int i) {
   Node& cn = nodes[i + 1];
   if (use_tb(i)) {
     // blocked pre-smooth b -> d (x after pre-smoothing), residual, restriction, coarse
-    // correction, then the blocked post-smooth reads d + P x_c (prolongation fused) -> x
+    // correction x~ = d + P x_c into r (free after the restriction), blocked post-smooth r -> x
     const ChebStep cs = cheb_first_step(nd);
     const double s_theta = 1.0 / (0.5 * (nd.hi + nd.lo));
     for (size_t q = 0; q < D.local.size(); ++q)
-      W.cnt.launches += launch_cheb2_tb(D.geo[q], nd.op[q], nd.b.p[q], nullptr, nd.d.p[q], s_theta, cs, true, nullptr,
-                                        nullptr, W.stream);
+      W.cnt.launches += launch_cheb2_tb(D.geo[q], nd.op[q], nd.b.p[q], nullptr, nd.d.p[q], s_theta, cs, true, W.stream);
     for (size_t q = 0; q < D.local.size(); ++q)
       W.cnt.launches += launch_residual(D.geo[q], nd.op[q], nd.b.p[q], nd.d.p[q], nd.r.p[q], W.stream);
     for (size_t q = 0; q < D.local.size(); ++q)
@@ -791,8 +790,9 @@ void Solver::vcycle(int i) {
     vcycle(i + 1);
     halo(i + 1, cn.x);
     for (size_t q = 0; q < D.local.size(); ++q)
-      W.cnt.launches += launch_cheb2_tb(D.geo[q], nd.op[q], nd.b.p[q], nd.d.p[q], nd.x.p[q], s_theta, cs, false,
-                                        cn.x.p[q], &cn.dist->geo[q], W.stream);
+      W.cnt.launches += launch_prolong_to(D.geo[q], cn.dist->geo[q], cn.x.p[q], nd.d.p[q], nd.r.p[q], W.stream);
+    for (size_t q = 0; q < D.local.size(); ++q)
+      W.cnt.launches += launch_cheb2_tb(D.geo[q], nd.op[q], nd.b.p[q], nd.r.p[q], nd.x.p[q], s_theta, cs, false, W.stream);
     return;
   }
   smooth(i, true);
@@ -823,11 +823,8 @@ ChebStep Solver::cheb_first_step(const Node& nd) const {
 // (TMGX_TB=0 disables it).
 bool Solver::use_tb(int i) const {
   const Node& nd = nodes[i];
-  if (!(tb_enabled && mgd.m == 2 && nd.kind == SMOOTH && nd.dist->h.n_ranks() == 1 && !nd.dist->local.empty() &&
-        nd.op[0].S == nullptr))
-    return false;
-  const bool coarse_ok = i + 1 < (int)nodes.size() && nodes[i + 1].kind != TELESCOPE && !nodes[i + 1].dist->geo.empty();
-  return cheb2_tb_supported(nd.dist->geo[0], coarse_ok ? &nodes[i + 1].dist->geo[0] : nullptr) && coarse_ok;
+  return tb_enabled && mgd.m == 2 && nd.kind == SMOOTH && nd.dist->h.n_ranks() == 1 && !nd.dist->local.empty() &&
+         nd.op[0].S == nullptr && cheb2_tb_supported(nd.dist->geo[0]);
 }
 
 void Solver::device_allreduce_ranksums(int nslots) {

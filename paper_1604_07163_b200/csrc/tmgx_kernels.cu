@@ -445,52 +445,53 @@ __global__ void __launch_bounds__(128) k_galerkin(BoxGeo F, OpParams fop, BoxGeo
 
 // ------------------------------------------------------------------------------------------
 // Temporally blocked Chebyshev, m = 2 (one kernel per smoothing side, solver.cpp:88-110):
-//   pass 1:  d0 = D^-1 (b - A x~) / theta          (PRE, x = 0: d0 = D^-1 b / theta)
-//   pass 2:  x' = (x~ + d0) + (c1 d0 + c2 D^-1 (r0 - A d0))   (PRE: x~ = 0, r0 = b)
-// with x~ = x + P x_c when the V-cycle hands over the coarse correction (the prolongation
-// x += P x_c of grid.cpp:373-428 fused in) and x~ = x otherwise.
+//   pass 1:  d0 = D^-1 (b - A x) / theta          (PRE, x = 0: d0 = D^-1 b / theta)
+//   pass 2:  x' = (x + d0) + (c1 d0 + c2 D^-1 (r0 - A d0))   (PRE: x = 0, r0 = b)
+// (the V-cycle's post-smooth runs on x~ = x + P x_c from k_prolong_pair).
 //
-// Mapping: a 32 x 16 thread block is the pass-1 ring; each thread owns one (i, j) column of
-// it and marches z, so the z-neighbours of x~, d0 and r0 live in per-thread register queues
-// and only in-plane neighbours go through shared memory (one plane of x~ and one of d0, double
-// buffered: one __syncthreads per plane). The interior 30 x 14 threads also run pass 2 and
-// write x'. Pass 1 runs one plane behind the x~ staging, pass 2 one plane behind pass 1.
-// Loads are TMA box copies (cp.async.bulk.tensor.3d, one elected thread, mbarrier completion)
-// of the b plane over the ring, the raw x plane over the ring grown by one and the coarse x_c
-// plane under it, kTBPF planes ahead of use; out-of-array boxes are zero-filled by the TMA unit.
-// Arithmetic is exactly that of k_cheb_start_res/_zero + (k_prolong_add) + k_cheb_step(last),
-// so results are bitwise identical to the unfused path. Algorithmic DRAM traffic: x, b in,
-// x' out (24 B/pt, + 1 B/pt of x_c); PRE: b in, x' out (16 B/pt) -- instead of 64 + 17
-// (PRE 40) for the unfused passes. Valid on single-box levels: the ring's out-of-box vertices
-// are out of the grid and never enter the arithmetic (row_apply reads coupled neighbours only).
+// Mapping: the 32 x 8 thread block covers a 32 x (8 NR) pass-1 ring; a thread owns one x
+// column and NR consecutive rows of it and marches z, so the z-neighbours of x, d0 and r0 live
+// in per-thread register queues, the y-neighbours inside a thread's rows are registers too,
+// and only x-neighbours and the rows at a thread's edge go through shared memory: x straight
+// from the TMA slot, d0 through one double-buffered plane (one __syncthreads per plane).
+// Interior ring points also run pass 2 and write x' (output tile 30 x (8 NR - 2)). Pass 1 runs
+// one plane behind the x staging, pass 2 one plane behind pass 1.
+// Loads are TMA box copies (cp.async.bulk.tensor.3d issued by one thread, mbarrier completion)
+// of the b plane over the ring and the x plane over the ring grown by one, kTBPF planes ahead of
+// use; boxes outside the array are zero-filled by the TMA unit. Arithmetic is exactly that of
+// k_cheb_start_res/_zero + k_cheb_step(last), so results are bitwise identical to the unfused
+// path. Algorithmic DRAM traffic: x, b in, x' out (24 B/pt); PRE: b in, x' out (16 B/pt) --
+// instead of 64 (PRE 40) for the unfused passes. Valid on single-box levels: the ring's
+// out-of-box vertices are out of the grid and never enter the arithmetic.
 // ------------------------------------------------------------------------------------------
-constexpr int kTBX = 32, kTBY = 16, kTBNT = kTBX * kTBY;  // threads = pass-1 ring
-constexpr int kTBOX = kTBX - 2, kTBOY = kTBY - 2;          // output tile 30 x 14
-constexpr int kTBSX = kTBX + 2, kTBSY = kTBY + 2;          // staged x~ ring 34 x 18
+constexpr int kTBX = 32, kTBY = 8, kTBNT = kTBX * kTBY;
+constexpr int kTBSX = kTBX + 2;  // staged width (ring + 1 each side; TMA x-start must be even)
 #ifndef TMGX_TB_PF
 #define TMGX_TB_PF 3
 #endif
 constexpr int kTBPF = TMGX_TB_PF;  // plane groups in flight
-constexpr int kTBNS = kTBPF + 1;   // plane slots
-constexpr int kTBCW = 20, kTBCH = 10, kTBNC = 4;  // coarse box: columns, rows; plane slots
-static_assert(kTBPF >= 1 && kTBPF <= 4, "the 4-slot coarse ring covers at most 4 planes in flight");
-// TMA box starts must be 16-byte aligned in x (even fp64 column): b is staged 34 wide from the
-// ring's column -1 (rows of the ring only), x from -1 with one extra row above/below.
-constexpr int kTBRawB = kTBSX * kTBSY * 8, kTBBB = kTBSX * kTBY * 8, kTBCB = kTBCW * kTBCH * 8;  // box bytes
-constexpr int tb_al128(int b) { return (b + 127) / 128 * 128; }
+__host__ __device__ constexpr int tb_al128(int b) { return (b + 127) / 128 * 128; }
 
-template <bool PRE>
-struct alignas(128) TBSmem {
-  alignas(128) unsigned char b[kTBNS][tb_al128(kTBBB)];
-  alignas(128) unsigned char raw[PRE ? 1 : kTBNS][tb_al128(kTBRawB)];
-  alignas(128) unsigned char c[PRE ? 1 : kTBNC][tb_al128(kTBCB)];
-  double xt[PRE ? 1 : 2][kTBSY][kTBSX];
-  double d[2][kTBY][kTBX];
-  unsigned long long bar[kTBNS];
+template <int NR>
+struct TBG {
+  static constexpr int RY = kTBY * NR;              // ring rows
+  static constexpr int OX = kTBX - 2, OY = RY - 2;  // output tile
+  static constexpr int SY = RY + 2;                 // staged x rows
+  static constexpr int BB = kTBSX * RY * 8, XB = kTBSX * SY * 8;  // box bytes
 };
 
-struct TBMaps {  // TMA descriptors (host-encoded, passed as __grid_constant__ parameters)
-  CUtensorMap b, x, c;
+template <int NR, bool PRE>
+struct alignas(128) TBSmem {
+  using G = TBG<NR>;
+  static constexpr int NS = PRE ? kTBPF + 1 : kTBPF + 2;  // POST keeps x of the pass-1 plane
+  alignas(128) unsigned char b[NS][tb_al128(G::BB)];
+  alignas(128) unsigned char x[PRE ? 1 : NS][tb_al128(G::XB)];
+  double d[2][G::RY][kTBX];
+  unsigned long long bar[NS];
+};
+
+struct TBMaps {  // TMA descriptors (host-encoded, passed as a __grid_constant__ parameter)
+  CUtensorMap b, x;
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -501,7 +502,7 @@ __device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
-__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+__device__ __forceinline__ void mbar_wait(unsigned bar_addr, unsigned parity) {
   asm volatile(
       "{\n"
       ".reg .pred P1;\n"
@@ -510,16 +511,15 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
       "@P1 bra TB_DONE;\n"
       "bra TB_WAIT;\n"
       "TB_DONE:\n"
-      "}\n" ::"r"(smem_u32(bar)),
+      "}\n" ::"r"(bar_addr),
       "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ void tma_load3(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
-                                          unsigned long long* bar) {
+__device__ __forceinline__ void tma_load3(unsigned dst, const CUtensorMap* map, int c0, int c1, int c2, unsigned bar) {
   asm volatile(
       "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::
-          "r"(smem_u32(dst)),
-      "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+          "r"(dst),
+      "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
       : "memory");
 }
 
@@ -560,199 +560,208 @@ __device__ __forceinline__ double row_full(const Coef& c, double uzm, double uym
   return acc;
 }
 
-template <bool VAR, bool PRE>
-__global__ void __launch_bounds__(kTBNT, 2)
+template <bool VAR, bool PRE, int NR>
+__global__ void __launch_bounds__(kTBNT, NR >= 4 ? 2 : (NR == 2 ? 3 : 4))
     k_cheb2_tb(const __grid_constant__ TBMaps maps, BoxGeo g, OpParams op, double* __restrict__ xout, double s_theta,
-               double c1, double c2, int fuse_p, BoxGeo Cg) {
+               double c1, double c2) {
+  using G = TBG<NR>;
+  using SM = TBSmem<NR, PRE>;
+  constexpr int NS = SM::NS;
   extern __shared__ __align__(1024) unsigned char tb_smem_raw[];
-  TBSmem<PRE>& S = *reinterpret_cast<TBSmem<PRE>*>(tb_smem_raw);
+  SM& S = *reinterpret_cast<SM*>(tb_smem_raw);
   const int tx = threadIdx.x, ty = threadIdx.y, tid = tx + kTBX * ty;
-  const int ox = blockIdx.x * kTBOX, oy = blockIdx.y * kTBOY;
+  const int ox = blockIdx.x * G::OX, oy = blockIdx.y * G::OY;
   const int k0 = blockIdx.z * g.zc, k1 = min(k0 + g.zc, g.ez);
-  const int i = ox - 1 + tx, j = oy - 1 + ty;  // this thread's ring column
-  const int gi = g.gx + i, gj = g.gy + j;
-  const bool in_xy = gi >= 0 && gj >= 0 && gi < g.Nx && gj < g.Ny;
-  const bool fast_xy = gi >= 2 && gj >= 2 && gi <= g.Nx - 3 && gj <= g.Ny - 3;
-  const bool out_xy = tx >= 1 && ty >= 1 && tx <= kTBOX && ty <= kTBOY && i < g.ex && j < g.ey;
-  const long long vij = g.base + i + g.px * (long long)j;
-  auto in_z = [&](int k) { return g.gz + k >= 0 && g.gz + k < g.Nz; };
-  auto fast_z = [&](int k) { return g.gz + k >= 2 && g.gz + k <= g.Nz - 3; };
+  const int jr0 = ty * NR;  // first ring row of this thread
+  const int i = ox - 1 + tx, j0 = oy - 1 + jr0;
+  const int gi = g.gx + i;
+  const bool in_x = gi >= 0 && gi < g.Nx, fast_x = gi >= 2 && gi <= g.Nx - 3;
+  const bool out_x = tx >= 1 && tx <= kTBX - 2 && i < g.ex;
+  unsigned in_y = 0, fast_y = 0, out_y = 0;
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    const int gj = g.gy + j0 + r, jr = jr0 + r;
+    in_y |= (gj >= 0 && gj < g.Ny) ? 1u << r : 0u;
+    fast_y |= (gj >= 2 && gj <= g.Ny - 3) ? 1u << r : 0u;
+    out_y |= (jr >= 1 && jr <= G::RY - 2 && j0 + r < g.ey) ? 1u << r : 0u;
+  }
+  if (!in_x) in_y = 0;
+  if (!fast_x) fast_y = 0;
+  if (!out_x) out_y = 0;
 
-  // plane schedule: step t stages x~(t) (POST), runs pass 1 on plane t - LAG1 and pass 2 on
-  // t - LAG1 - 1. Group t = {b(t - LAG1), raw x(t), coarse planes first needed by x~(t)}.
+  // plane schedule: step t brings group t = {b(t - LAG1), x(t)}, runs pass 1 on plane
+  // p1 = t - LAG1 and pass 2 on p2 = p1 - 1.
   constexpr int LAG1 = PRE ? 0 : 1;
   const int T0 = k0 - 1 - LAG1, T1 = k1 + LAG1;
-  const int cxs = (((g.gx + ox - 2) >> 1) - Cg.gx) & ~1;  // first staged coarse column (even) / row
-  const int cys = ((g.gy + oy - 2) >> 1) - Cg.gy;
-  auto slot = [&](int t) { return (t - T0) % kTBNS; };
-  auto parity = [&](int t) { return (unsigned)(((t - T0) / kTBNS) & 1); };
-  auto issue = [&](int t) {  // elected thread only
+  const unsigned sb = smem_u32(&S.b[0][0]), sx = smem_u32(&S.x[0][0]), sbar = smem_u32(&S.bar[0]);
+  auto issue = [&](int t, int sl) {  // elected thread only
     if (t > T1) return;
-    unsigned long long* bar = &S.bar[slot(t)];
-    const int pb = t - LAG1;
-    unsigned bytes = kTBBB;
-    int q0 = 0, nq = 0;
-    if (!PRE) {
-      bytes += kTBRawB;
-      if (fuse_p) {
-        const int fz = g.gz + t;
-        if (t == T0) q0 = (fz >> 1) - Cg.gz, nq = (fz & 1) ? 2 : 1;
-        else if (fz & 1) q0 = (fz >> 1) + 1 - Cg.gz, nq = 1;
-        bytes += nq * kTBCB;
-      }
-    }
-    mbar_expect_tx(bar, bytes);
-    tma_load3(S.b[slot(t)], &maps.b, kXO + ox - 2, oy, pb + 1, bar);
-    if (!PRE) {
-      tma_load3(S.raw[slot(t)], &maps.x, kXO + ox - 2, oy - 1, t + 1, bar);
-      for (int q = q0; q < q0 + nq; ++q) tma_load3(S.c[q & (kTBNC - 1)], &maps.c, kXO + cxs, cys + 1, q + 1, bar);
-    }
+    const unsigned bar = sbar + 8 * sl;
+    mbar_expect_tx(&S.bar[sl], PRE ? G::BB : G::BB + G::XB);
+    tma_load3(sb + sl * tb_al128(G::BB), &maps.b, kXO + ox - 2, oy, t - LAG1 + 1, bar);
+    if (!PRE) tma_load3(sx + sl * tb_al128(G::XB), &maps.x, kXO + ox - 2, oy - 1, t + 1, bar);
   };
-  // x~ at staged ring position (lx, ly) of plane p: raw + P x_c in grid (k_prolong_add order), else 0
-  auto xtilde = [&](int p, int lx, int ly) -> double {
-    const int fx = g.gx + ox - 2 + lx, fy = g.gy + oy - 2 + ly, fz = g.gz + p;
-    if (fx < 0 || fy < 0 || fz < 0 || fx >= g.Nx || fy >= g.Ny || fz >= g.Nz) return 0.0;
-    const double* raw = reinterpret_cast<const double*>(S.raw[slot(p)]);
-    const double xo = raw[ly * kTBSX + lx];
-    if (!fuse_p) return xo;
-    const int nx = 1 + (fx & 1), ny = 1 + (fy & 1), nz = 1 + (fz & 1);
-    const int cx0 = (fx >> 1) - Cg.gx - cxs, cy0 = (fy >> 1) - Cg.gy - cys, cz0 = (fz >> 1) - Cg.gz;
-    const double wx = nx == 2 ? 0.5 : 1.0, wy = ny == 2 ? 0.5 : 1.0, wz = nz == 2 ? 0.5 : 1.0;
-    double acc = 0.0;
-#pragma unroll
-    for (int tz = 0; tz < 2; ++tz) {
-      if (tz < nz) {
-        const double* cp = reinterpret_cast<const double*>(S.c[(cz0 + tz) & (kTBNC - 1)]);
-#pragma unroll
-        for (int uy = 0; uy < 2; ++uy) {
-          if (uy < ny) {
-#pragma unroll
-            for (int ux = 0; ux < 2; ++ux) {
-              if (ux < nx) {
-                const double ww = wx * wy * wz;
-                acc += ww * cp[(cy0 + uy) * kTBCW + cx0 + ux];
-              }
-            }
-          }
-        }
-      }
-    }
-    return xo + acc;
-  };
-
   if (tid == 0) {
-    for (int s = 0; s < kTBNS; ++s) mbar_init(&S.bar[s], 1);
+    for (int s = 0; s < NS; ++s) mbar_init(&S.bar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    for (int s = 0; s < kTBPF; ++s) issue(T0 + s, s);
   }
   __syncthreads();
-  if (tid == 0)
-    for (int s = 0; s < kTBPF; ++s) issue(T0 + s);
 
-  double b_prev = 0.0;                     // PRE: b of the pass-2 plane
-  double xq0 = 0.0, xq1 = 0.0, xq2 = 0.0;  // x~ at this column: planes t-2, t-1, t (POST)
-  double dq0 = 0.0, dq1 = 0.0, dq2 = 0.0;  // d0: pass-2 plane - 1, pass-2 plane, pass-2 plane + 1
-  double rq1 = 0.0, rq2 = 0.0;             // r0: pass-2 plane, pass-1 plane (POST)
-  for (int t = T0; t <= T1; ++t) {
+  double xq0[NR], xq1[NR], xq2[NR];  // x of this thread's rows: planes t-2, t-1, t (POST)
+  double dq0[NR], dq1[NR], dq2[NR];  // d0: pass-2 plane - 1, pass-2 plane, pass-2 plane + 1
+  double rq1[NR], rq2[NR];           // r0 (POST) / b (PRE): pass-2 plane, pass-1 plane
+#pragma unroll
+  for (int r = 0; r < NR; ++r) xq0[r] = xq1[r] = xq2[r] = dq0[r] = dq1[r] = dq2[r] = rq1[r] = rq2[r] = 0.0;
+  int sl = 0, isl = kTBPF, psl = NS - 1;  // slots of groups t, t + kTBPF, t - 1
+  unsigned ph = 0;                         // mbarrier parity of group t
+  double* outp = xout + g.base + i + g.px * (long long)j0 + g.pxy * (long long)(T0 - LAG1 - 1);
+  for (int t = T0; t <= T1; ++t, outp += g.pxy) {
     const int p1 = t - LAG1, p2 = p1 - 1;  // pass-1 and pass-2 planes
-    mbar_wait(&S.bar[slot(t)], parity(t));
-    __syncthreads();  // slot of group t-1 is free; d / xt buffers of step t-2 are free
+    mbar_wait(sbar + 8 * sl, ph);
+    __syncthreads();  // slot of group t+kTBPF-NS and the d buffer of step t-2 are free
     if (tid == 0) {
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      issue(t + kTBPF);
+      issue(t + kTBPF, isl);
     }
-    const double bown = reinterpret_cast<const double*>(S.b[slot(t)])[ty * kTBSX + tx + 1];
+    const double* bsm = reinterpret_cast<const double*>(S.b[sl]);
     if (!PRE) {
-      // x~(t): own column into the register queue, the whole ring into S.xt[t & 1]
-      double(*xt)[kTBSX] = S.xt[t & 1];
-      xq2 = xtilde(t, tx + 1, ty + 1);
-      xt[ty + 1][tx + 1] = xq2;
-      if (tid < 2 * kTBSY + 2 * (kTBSX - 2)) {  // the 100 positions outside the thread ring
-        int lx, ly;
-        if (tid < 2 * kTBSY) {
-          lx = (tid & 1) ? kTBSX - 1 : 0;
-          ly = tid >> 1;
-        } else {
-          const int e = tid - 2 * kTBSY;
-          lx = 1 + (e >> 1);
-          ly = (e & 1) ? kTBSY - 1 : 0;
-        }
-        xt[ly][lx] = xtilde(t, lx, ly);
-      }
+      const double* xs = reinterpret_cast<const double*>(S.x[sl]);
+#pragma unroll
+      for (int r = 0; r < NR; ++r) xq2[r] = xs[(jr0 + r + 1) * kTBSX + tx + 1];
     }
-    // pass 1 on plane p1 (this column)
+    // pass 1 on plane p1
     if (p1 >= k0 - 1 && p1 <= k1) {
-      double d0 = 0.0, rr = 0.0;
-      if (in_xy && in_z(p1)) {
-        const long long v = vij + g.pxy * (long long)p1;
-        const Coef c = coef_fc<VAR>(g, op, v);
-        if (PRE) {
-          d0 = (bown * c.invd) * s_theta;
-        } else {
-          const double(*X)[kTBSX] = S.xt[p1 & 1];
-          const double xw = X[ty + 1][tx], xe = X[ty + 1][tx + 2], xs_ = X[ty][tx + 1], xn = X[ty + 2][tx + 1];
-          double ax;
-          if (fast_xy && fast_z(p1))
-            ax = row_full(c, xq0, xs_, xw, xq1, xe, xn, xq2);
-          else
-            ax = row_apply(make_pt(g, i, j, p1), c, xq0, xs_, xw, xq1, xe, xn, xq2);
-          rr = bown - ax;
-          d0 = (rr * c.invd) * s_theta;
+      const bool in_z1 = g.gz + p1 >= 0 && g.gz + p1 < g.Nz;
+      const bool fz1 = g.gz + p1 >= 2 && g.gz + p1 <= g.Nz - 3;
+      const double* X = reinterpret_cast<const double*>(S.x[psl]);  // x plane p1 (staged rows +1)
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        const double bb = bsm[(jr0 + r) * kTBSX + tx + 1];
+        double d0 = 0.0, rr = 0.0;
+        if (((in_y >> r) & 1) && in_z1) {
+          const Coef c = coef_fc<VAR>(g, op, g.base + i + g.px * (long long)(j0 + r) + g.pxy * (long long)p1);
+          if (PRE) {
+            d0 = (bb * c.invd) * s_theta;
+            rr = bb;
+          } else {
+            const int ly = jr0 + r + 1;
+            const double xw = X[ly * kTBSX + tx], xe = X[ly * kTBSX + tx + 2];
+            const double xs_ = r == 0 ? X[(ly - 1) * kTBSX + tx + 1] : xq1[r > 0 ? r - 1 : 0];
+            const double xn = r == NR - 1 ? X[(ly + 1) * kTBSX + tx + 1] : xq1[r < NR - 1 ? r + 1 : 0];
+            double ax;
+            if (((fast_y >> r) & 1) && fz1)
+              ax = row_full(c, xq0[r], xs_, xw, xq1[r], xe, xn, xq2[r]);
+            else
+              ax = row_apply(make_pt(g, i, j0 + r, p1), c, xq0[r], xs_, xw, xq1[r], xe, xn, xq2[r]);
+            rr = bb - ax;
+            d0 = (rr * c.invd) * s_theta;
+          }
         }
+        dq2[r] = d0;
+        rq2[r] = rr;
+        S.d[p1 & 1][jr0 + r][tx] = d0;
       }
-      dq2 = d0;
-      rq2 = rr;
-      S.d[p1 & 1][ty][tx] = d0;
     }
-    // pass 2 on plane p2 (interior columns); d0 of p2's in-plane neighbours came from step t-1
-    if (out_xy && p2 >= k0 && p2 < k1) {
-      const long long v = vij + g.pxy * (long long)p2;
-      const Coef c = coef_fc<VAR>(g, op, v);
+    // pass 2 on plane p2 (interior ring points); in-plane d0 of p2 came from step t-1
+    if (out_y && p2 >= k0 && p2 < k1) {
+      const bool fz2 = g.gz + p2 >= 2 && g.gz + p2 <= g.Nz - 3;
       const double(*D)[kTBX] = S.d[p2 & 1];
-      const double d0 = dq1;
-      const double x1 = PRE ? d0 : xq0 + d0;
-      const double dw = D[ty][tx - 1], de = D[ty][tx + 1], ds = D[ty - 1][tx], dn_ = D[ty + 1][tx];
-      double ad;
-      if (fast_xy && fast_z(p2))
-        ad = row_full(c, dq0, ds, dw, d0, de, dn_, dq2);
-      else
-        ad = row_apply(make_pt(g, i, j, p2), c, dq0, ds, dw, d0, de, dn_, dq2);
-      const double r0 = PRE ? b_prev : rq1;
-      const double r1 = r0 - ad;
-      const double z = r1 * c.invd;
-      const double dn = c1 * d0 + c2 * z;
-      xout[v] = x1 + dn;
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        if (!((out_y >> r) & 1)) continue;
+        const Coef c = coef_fc<VAR>(g, op, (outp - xout) + g.px * r);
+        const double d0 = dq1[r];
+        const double x1 = PRE ? d0 : xq0[r] + d0;
+        const int jr = jr0 + r;
+        const double dw = D[jr][tx - 1], de = D[jr][tx + 1];
+        const double ds = r == 0 ? D[jr - 1][tx] : dq1[r > 0 ? r - 1 : 0];
+        const double dn_ = r == NR - 1 ? D[jr + 1][tx] : dq1[r < NR - 1 ? r + 1 : 0];
+        double ad;
+        if (((fast_y >> r) & 1) && fz2)
+          ad = row_full(c, dq0[r], ds, dw, d0, de, dn_, dq2[r]);
+        else
+          ad = row_apply(make_pt(g, i, j0 + r, p2), c, dq0[r], ds, dw, d0, de, dn_, dq2[r]);
+        const double r1 = rq1[r] - ad;
+        const double z = r1 * c.invd;
+        const double dn = c1 * d0 + c2 * z;
+        outp[g.px * r] = x1 + dn;
+      }
     }
-    // rotate the queues
-    b_prev = bown;
-    dq0 = dq1;
-    dq1 = dq2;
-    rq1 = rq2;
-    xq0 = xq1;
-    xq1 = xq2;
+    // rotate the queues and the slot ring
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      dq0[r] = dq1[r];
+      dq1[r] = dq2[r];
+      rq1[r] = rq2[r];
+      xq0[r] = xq1[r];
+      xq1[r] = xq2[r];
+    }
+    psl = sl;
+    if (++sl == NS) sl = 0, ph ^= 1u;
+    if (++isl == NS) isl = 0;
   }
 }
 
-// out-of-place prolongation: xo = xf + P xc
-__global__ void k_prolong_to(BoxGeo F, BoxGeo Cg, const double* __restrict__ xc, const double* __restrict__ xf,
-                             double* __restrict__ xo) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y * blockDim.y + threadIdx.y;
-  const int k = blockIdx.z;
-  if (i >= F.ex || j >= F.ey) return;
-  const int fx = F.gx + i, fy = F.gy + j, fz = F.gz + k;
-  const int nx = 1 + (fx & 1), ny = 1 + (fy & 1), nz = 1 + (fz & 1);
-  const int cx0 = (fx >> 1) - Cg.gx, cy0 = (fy >> 1) - Cg.gy, cz0 = (fz >> 1) - Cg.gz;
-  const double wx = nx == 2 ? 0.5 : 1.0, wy = ny == 2 ? 0.5 : 1.0, wz = nz == 2 ? 0.5 : 1.0;
-  double acc = 0.0;
-  for (int tz = 0; tz < nz; ++tz)
-    for (int ty = 0; ty < ny; ++ty) {
-      const double* row = xc + vidx(Cg, cx0, cy0 + ty, cz0 + tz);
-      for (int tx = 0; tx < nx; ++tx) {
-        const double ww = wx * wy * wz;
-        acc += ww * __ldg(row + tx);
+// Prolongation over vertex pairs with a z-march: xo = xf + P xc (xo may alias xf: in-place
+// x += P x_c). Every coarse neighbour of the pair is loaded unconditionally (the padded coarse
+// array holds finite values on its ghost ring) and absent terms carry weight 0; the trilinear
+// weights are exact powers of two, so the sum equals k_prolong_add's (grid.cpp:421) bit for bit.
+__global__ void __launch_bounds__(kBX* kBY)
+    k_prolong_pair(BoxGeo F, BoxGeo Cg, const double* __restrict__ xc, const double* xf, double* xo) {
+  const int i0 = 2 * (blockIdx.x * kBX + threadIdx.x), j = blockIdx.y * kBY + threadIdx.y;
+  if (i0 >= F.ex || j >= F.ey) return;
+  const bool two = i0 + 1 < F.ex;
+  const int k0 = blockIdx.z * F.zc, k1 = min(k0 + F.zc, F.ez);
+  const int fx0 = F.gx + i0, fy = F.gy + j;
+  const int cx = (fx0 >> 1) - Cg.gx, cy = (fy >> 1) - Cg.gy;
+  // point q (fx = fx0 + q) reads coarse columns cx + sq, cx + sq + 1 with sq = (fx >> 1) - (fx0 >> 1)
+  // in {0, 1}; weights (w, w) for an odd fx (midpoint), (1, 0) for an even one (coincident)
+  const bool s1 = ((fx0 + 1) >> 1) != (fx0 >> 1);  // point 1 starts one coarse column later
+  const double w0a = (fx0 & 1) ? 0.5 : 1.0, w0b = (fx0 & 1) ? 0.5 : 0.0;
+  const double w1a = ((fx0 + 1) & 1) ? 0.5 : 1.0, w1b = ((fx0 + 1) & 1) ? 0.5 : 0.0;
+  const double wy0 = (fy & 1) ? 0.5 : 1.0, wy1 = (fy & 1) ? 0.5 : 0.0;
+  for (int k = k0; k < k1; ++k) {
+    const int fz = F.gz + k, cz = (fz >> 1) - Cg.gz;
+    const double wz0 = (fz & 1) ? 0.5 : 1.0, wz1 = (fz & 1) ? 0.5 : 0.0;
+    double cv[2][2][3];
+#pragma unroll
+    for (int tz = 0; tz < 2; ++tz)
+#pragma unroll
+      for (int uy = 0; uy < 2; ++uy) {
+        const double* row = xc + vidx(Cg, cx, cy + uy, cz + tz);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) cv[tz][uy][c] = __ldg(row + c);
       }
+    const long long v = vidx(F, i0, j, k);
+    double out[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const double wa = q ? w1a : w0a, wb = q ? w1b : w0b;
+      const bool sh = q ? s1 : false;
+      double acc = 0.0;
+#pragma unroll
+      for (int tz = 0; tz < 2; ++tz)
+#pragma unroll
+        for (int uy = 0; uy < 2; ++uy) {
+          const double wyz = (uy ? wy1 : wy0) * (tz ? wz1 : wz0);
+          const double va = sh ? cv[tz][uy][1] : cv[tz][uy][0];
+          const double vb = sh ? cv[tz][uy][2] : cv[tz][uy][1];
+          acc += (wa * wyz) * va;
+          acc += (wb * wyz) * vb;
+        }
+      out[q] = acc;
     }
-  const long long v = vidx(F, i, j, k);
-  xo[v] = xf[v] + acc;
+    if (two) {
+      const double2 xv = *reinterpret_cast<const double2*>(xf + v);
+      double2 o;
+      o.x = xv.x + out[0];
+      o.y = xv.y + out[1];
+      *reinterpret_cast<double2*>(xo + v) = o;
+    } else {
+      xo[v] = xf[v] + out[0];
+    }
+  }
 }
 
 struct NoIn {};
@@ -1288,6 +1297,21 @@ int launch_apply(const BoxGeo& g, const OpParams& op, const double* x, double* y
   return 1;
 }
 
+// TMA boxes may not exceed the tensor (the TMA unit traps): the blocked smoother with NR rows
+// per thread needs px >= 34 and ey + 2 >= 8 NR + 2.
+template <int NR>
+static bool tb_fits(const BoxGeo& g) {
+  return g.px >= kTBSX && g.ey + 2 >= TBG<NR>::SY;
+}
+static int tb_rows() {
+  static const int nr = [] {
+    const char* e = std::getenv("TMGX_TB_NR");
+    return e ? std::max(1, std::min(4, std::atoi(e))) : 2;
+  }();
+  return nr;
+}
+bool cheb2_tb_supported(const BoxGeo& g) { return tb_fits<1>(g); }
+
 // TMA descriptor of a padded box array (dims px x (ey+2) x (ez+2), fp64, zero fill outside),
 // cached per (array, box shape).
 static CUtensorMap tensor_map(const BoxGeo& g, const double* base_ptr, int bx, int by) {
@@ -1324,23 +1348,14 @@ static CUtensorMap tensor_map(const BoxGeo& g, const double* base_ptr, int bx, i
   return m;
 }
 
-// TMA boxes may not exceed the tensor (the TMA unit traps): the blocked smoother needs a level
-// at least 30 x 16 vertices across (and a coarse level at least 16 x 8 when fused).
-bool cheb2_tb_supported(const BoxGeo& g, const BoxGeo* coarse) {
-  if (g.px < kTBSX || g.ey + 2 < kTBSY) return false;
-  if (coarse && (coarse->px < kTBCW || coarse->ey + 2 < kTBCH)) return false;
-  return true;
-}
-
-int launch_cheb2_tb(const BoxGeo& g, const OpParams& op, const double* b, const double* xin, double* xout,
-                    double s_theta, ChebStep c, bool pre, const double* xc, const BoxGeo* coarse, cudaStream_t s) {
-  const BoxGeo cg = coarse ? *coarse : g;
+template <int NR>
+static void launch_tb_rows(const BoxGeo& g, const OpParams& op, const double* b, const double* xin, double* xout,
+                           double s_theta, ChebStep c, bool pre, cudaStream_t s) {
+  using G = TBG<NR>;
   TBMaps maps;
   std::memset(&maps, 0, sizeof(maps));
-  maps.b = tensor_map(g, b, kTBSX, kTBY);
-  if (!pre) maps.x = tensor_map(g, xin, kTBSX, kTBSY);
-  if (!pre && xc) maps.c = tensor_map(cg, xc, kTBCW, kTBCH);
-  const int fuse = (!pre && xc) ? 1 : 0;
+  maps.b = tensor_map(g, b, kTBSX, G::RY);
+  if (!pre) maps.x = tensor_map(g, xin, kTBSX, G::SY);
   const dim3 bl(kTBX, kTBY);
   auto go = [&](auto kern, size_t smem, int& slots) {  // slots: resident blocks on the device
     if (!slots) {
@@ -1351,9 +1366,9 @@ int launch_cheb2_tb(const BoxGeo& g, const OpParams& op, const double* b, const 
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kTBNT, smem);
       slots = std::max(1, sms * std::max(per, 1));
     }
-    // z planes per block: minimise waves x (planes + 2-plane pipeline fill) over the split count
+    // z planes per block: minimise waves x (planes + pipeline fill) over the split count
     BoxGeo gt = g;
-    const long long cols = (long long)((g.ex + kTBOX - 1) / kTBOX) * ((g.ey + kTBOY - 1) / kTBOY);
+    const long long cols = (long long)((g.ex + G::OX - 1) / G::OX) * ((g.ey + G::OY - 1) / G::OY);
     static const int zc_env = [] {
       const char* e = std::getenv("TMGX_TB_ZC");
       return e ? std::max(1, std::atoi(e)) : 0;
@@ -1371,27 +1386,40 @@ int launch_cheb2_tb(const BoxGeo& g, const OpParams& op, const double* b, const 
       }
     }
     gt.zc = best;
-    const dim3 gr((g.ex + kTBOX - 1) / kTBOX, (g.ey + kTBOY - 1) / kTBOY, (g.ez + gt.zc - 1) / gt.zc);
-    kern<<<gr, bl, smem, s>>>(maps, gt, op, xout, s_theta, c.c1, c.c2, fuse, cg);
+    const dim3 gr((g.ex + G::OX - 1) / G::OX, (g.ey + G::OY - 1) / G::OY, (g.ez + gt.zc - 1) / gt.zc);
+    kern<<<gr, bl, smem, s>>>(maps, gt, op, xout, s_theta, c.c1, c.c2);
   };
   static int slots[4] = {0, 0, 0, 0};
   if (op.fc) {
     if (pre)
-      go(k_cheb2_tb<true, true>, sizeof(TBSmem<true>), slots[0]);
+      go(k_cheb2_tb<true, true, NR>, sizeof(TBSmem<NR, true>), slots[0]);
     else
-      go(k_cheb2_tb<true, false>, sizeof(TBSmem<false>), slots[1]);
+      go(k_cheb2_tb<true, false, NR>, sizeof(TBSmem<NR, false>), slots[1]);
   } else {
     if (pre)
-      go(k_cheb2_tb<false, true>, sizeof(TBSmem<true>), slots[2]);
+      go(k_cheb2_tb<false, true, NR>, sizeof(TBSmem<NR, true>), slots[2]);
     else
-      go(k_cheb2_tb<false, false>, sizeof(TBSmem<false>), slots[3]);
+      go(k_cheb2_tb<false, false, NR>, sizeof(TBSmem<NR, false>), slots[3]);
   }
+}
+
+int launch_cheb2_tb(const BoxGeo& g, const OpParams& op, const double* b, const double* xin, double* xout,
+                    double s_theta, ChebStep c, bool pre, cudaStream_t s) {
+  const int nr = tb_rows();
+  if (nr >= 4 && tb_fits<4>(g))
+    launch_tb_rows<4>(g, op, b, xin, xout, s_theta, c, pre, s);
+  else if (nr >= 2 && tb_fits<2>(g))
+    launch_tb_rows<2>(g, op, b, xin, xout, s_theta, c, pre, s);
+  else if (tb_fits<1>(g))
+    launch_tb_rows<1>(g, op, b, xin, xout, s_theta, c, pre, s);
+  else
+    throw std::runtime_error("blocked smoother: level too small for the TMA boxes");
   return 1;
 }
 
 int launch_prolong_to(const BoxGeo& fine, const BoxGeo& coarse, const double* xc, const double* xf, double* xo,
                       cudaStream_t s) {
-  k_prolong_to<<<plane_grid(fine, 0), dim3(32, 4), 0, s>>>(fine, coarse, xc, xf, xo);
+  k_prolong_pair<<<tile_grid(fine), kBlock, 0, s>>>(fine, coarse, xc, xf, xo);
   return 1;
 }
 
@@ -1401,7 +1429,7 @@ int launch_restrict(const BoxGeo& fine, const BoxGeo& coarse, const double* rf, 
 }
 
 int launch_prolong_add(const BoxGeo& fine, const BoxGeo& coarse, const double* xc, double* xf, cudaStream_t s) {
-  k_prolong_add<<<plane_grid(fine, 0), dim3(32, 4), 0, s>>>(fine, coarse, xc, xf);
+  k_prolong_pair<<<tile_grid(fine), kBlock, 0, s>>>(fine, coarse, xc, xf, xf);
   return 1;
 }
 

@@ -90,11 +90,11 @@ int launch_cheb_start_res(const BoxGeo& g, const OpParams& op, const double* b, 
 // last: x_out = x1 + d_new only ; else x_out = x1, r_out = r1, d_new.
 int launch_cheb_step(const BoxGeo& g, const OpParams& op, const double* d, const double* r_in, const double* x_in,
                      double* d_new, double* r_out, double* x_out, ChebStep c, bool last, cudaStream_t s);
-// Temporally blocked m = 2 Chebyshev side (single-box levels, 7-point operator): pre (x = 0):
-// xout = S(b); post: xout = S(b, xin + P xc) with xin != xout (xc may be null: no prolongation).
+// Temporally blocked m = 2 Chebyshev side (single-box levels, 7-point operator, TMA-staged):
+// pre (x = 0): xout = S(b); post: xout = S(b, xin) with xin != xout.
 int launch_cheb2_tb(const BoxGeo& g, const OpParams& op, const double* b, const double* xin, double* xout,
-                    double s_theta, ChebStep c, bool pre, const double* xc, const BoxGeo* coarse, cudaStream_t s);
-bool cheb2_tb_supported(const BoxGeo& g, const BoxGeo* coarse);
+                    double s_theta, ChebStep c, bool pre, cudaStream_t s);
+bool cheb2_tb_supported(const BoxGeo& g);
 // xo = xf + P xc (out of place)
 int launch_prolong_to(const BoxGeo& fine, const BoxGeo& coarse, const double* xc, const double* xf, double* xo,
                       cudaStream_t s);
