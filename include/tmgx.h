@@ -205,7 +205,8 @@ int tmgx_plan_summary(int n_ranks, int nproc, int proc, const tmgx_problem *prob
  *        2 operator apply 3 residual 4 restriction 5 prolongation 6 cg_update 7 spmv+dot
  *        8 temporally blocked V(2,2) pre-smooth side (b in, x out)
  *        9 temporally blocked post-smooth side (x, b in, x out)
- *       10 out-of-place prolongation x~ = x + P x_c (x, x_c in, x~ out) */
+ *       10 out-of-place prolongation x~ = x + P x_c (x, x_c in, x~ out)
+ *       11 fused residual + restriction b_c = R (b - A x) (b, x in, b_c out) */
 int tmgx_bench_kernel(tmgx_solver s, int which, int level, int iters, double *ms_per_launch,
                       double *bytes_per_launch);
 

@@ -55,6 +55,7 @@ def build(parity=False, verbose=False, force=False):
                     "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc, "-Xptxas", "-v"]
     if parity:
         flags += ["-fmad=false", "-DTMGX_PARITY"]
+    flags += os.environ.get("TMGX_NVCC_EXTRA", "").split()  # tuning experiments (e.g. -DTMGX_TB_PF=6)
     cmds, objs = [], []
     for src in SOURCES:
         s = os.path.join(CSRC, src)

@@ -358,13 +358,7 @@ int tmgx_level_residual_restrict(tmgx_solver s, int fine_level, const double* b,
     auto& cn = S.nodes[i + 1];
     S.upload(i, nd.b, b, false);
     S.upload(i, nd.x, x, false);
-    S.halo(i, nd.x);
-    const auto& D = *nd.dist;
-    for (size_t q = 0; q < D.local.size(); ++q)
-      S.W.cnt.launches += tmgx::launch_residual(D.geo[q], nd.op[q], nd.b.p[q], nd.x.p[q], nd.r.p[q], S.W.stream);
-    S.halo(i, nd.r);
-    for (size_t q = 0; q < D.local.size(); ++q)
-      S.W.cnt.launches += tmgx::launch_restrict(D.geo[q], cn.dist->geo[q], nd.r.p[q], cn.b.p[q], S.W.stream);
+    S.residual_restrict(i, nd.x);  // the V-cycle's path (fused on single-box levels)
     S.download(i + 1, cn.b, bc, false);
     return 0;
   });
@@ -497,6 +491,7 @@ extern "C" int tmgx_bench_kernel(tmgx_solver s, int which, int level, int iters,
           case 7: tmgx::launch_spmv_dot(g, nd.op[q], nd.x.p[q], nd.b.p[q], S.part + S.part_off[q], S.W.stream); break;
           case 8: tmgx::launch_cheb2_tb(g, nd.op[q], nd.b.p[q], nullptr, nd.d.p[q], 1.0, cs, true, S.W.stream); break;
           case 9: tmgx::launch_cheb2_tb(g, nd.op[q], nd.b.p[q], nd.d.p[q], nd.x.p[q], 1.0, cs, false, S.W.stream); break;
+          case 11: tmgx::launch_resid_restrict(g, nd.op[q], S.nodes[i + 1].dist->geo[q], nd.b.p[q], nd.x.p[q], S.nodes[i + 1].b.p[q], S.W.stream); break;
           case 10: tmgx::launch_prolong_to(g, S.nodes[i + 1].dist->geo[q], S.nodes[i + 1].x.p[q], nd.d.p[q], nd.r.p[q], S.W.stream); break;
           default: throw tmg::Error("unknown kernel id");
         }
@@ -514,6 +509,7 @@ extern "C" int tmgx_bench_kernel(tmgx_solver s, int which, int level, int iters,
       case 8: per_pt = 16 + kb; break;             // temporally blocked pre-smooth: b in, x out
       case 9: per_pt = 24 + kb; break;             // blocked post-smooth: x, b in, x out
       case 10: per_pt = 16 + 8.0 / 8.0; break;     // out-of-place prolongation: x, x_c in, x~ out
+      case 11: per_pt = 16 + 8.0 / 8.0 + kb; break; // fused residual + restriction: b, x in, b_c out
       default: throw tmg::Error("unknown kernel id");
     }
     tmgx::cuda_check(cudaMemsetAsync(S.scal, 0, sizeof(double) * tmgx::S_NSLOTS, S.W.stream), "memset");

@@ -361,6 +361,7 @@ Solver::Solver(World& W_, const ProblemDesc& P, const MGDesc& M) : W(W_), prob(P
   CK(cudaSetDevice(W.device));
   if (const char* e = std::getenv("TMGX_GRAPHS")) use_graphs = std::string(e) != "0";
   if (const char* e = std::getenv("TMGX_TB")) tb_enabled = std::string(e) != "0";
+  if (const char* e = std::getenv("TMGX_FUSE_RR")) fuse_rr = std::string(e) != "0";
   if (mgd.nlevels < 1) throw tmg::ConfigError("mg: number of levels must be >= 1");
   if (mgd.m < 1) throw tmg::ConfigError("mg: smoother iterations must be >= 1");
   if (prob.kind == 1) {
@@ -783,10 +784,7 @@ void Solver::vcycle(int i) {
     const double s_theta = 1.0 / (0.5 * (nd.hi + nd.lo));
     for (size_t q = 0; q < D.local.size(); ++q)
       W.cnt.launches += launch_cheb2_tb(D.geo[q], nd.op[q], nd.b.p[q], nullptr, nd.d.p[q], s_theta, cs, true, W.stream);
-    for (size_t q = 0; q < D.local.size(); ++q)
-      W.cnt.launches += launch_residual(D.geo[q], nd.op[q], nd.b.p[q], nd.d.p[q], nd.r.p[q], W.stream);
-    for (size_t q = 0; q < D.local.size(); ++q)
-      W.cnt.launches += launch_restrict(D.geo[q], cn.dist->geo[q], nd.r.p[q], cn.b.p[q], W.stream);
+    residual_restrict(i, nd.d);
     vcycle(i + 1);
     halo(i + 1, cn.x);
     for (size_t q = 0; q < D.local.size(); ++q)
@@ -796,17 +794,30 @@ void Solver::vcycle(int i) {
     return;
   }
   smooth(i, true);
-  halo(i, nd.x);
-  for (size_t q = 0; q < D.local.size(); ++q)
-    W.cnt.launches += launch_residual(D.geo[q], nd.op[q], nd.b.p[q], nd.x.p[q], nd.r.p[q], W.stream);
-  halo(i, nd.r);
-  for (size_t q = 0; q < D.local.size(); ++q)
-    W.cnt.launches += launch_restrict(D.geo[q], cn.dist->geo[q], nd.r.p[q], cn.b.p[q], W.stream);
+  residual_restrict(i, nd.x);
   vcycle(i + 1);
   halo(i + 1, cn.x);
   for (size_t q = 0; q < D.local.size(); ++q)
     W.cnt.launches += launch_prolong_add(D.geo[q], cn.dist->geo[q], cn.x.p[q], nd.x.p[q], W.stream);
   smooth(i, false);
+}
+
+// b_c = R (b - A x) of level i into the next node's b: fused on single-box 7-point levels
+// (the residual stays on chip), else residual into r, box halo of r, restriction.
+void Solver::residual_restrict(int i, const Field& x) {
+  Node& nd = nodes[i];
+  Node& cn = nodes[i + 1];
+  const Dist& D = *nd.dist;
+  if (D.h.n_ranks() == 1 && D.local.size() == 1 && resid_restrict_supported(nd.op[0]) && fuse_rr) {
+    W.cnt.launches += launch_resid_restrict(D.geo[0], nd.op[0], cn.dist->geo[0], nd.b.p[0], x.p[0], cn.b.p[0], W.stream);
+    return;
+  }
+  halo(i, x);
+  for (size_t q = 0; q < D.local.size(); ++q)
+    W.cnt.launches += launch_residual(D.geo[q], nd.op[q], nd.b.p[q], x.p[q], nd.r.p[q], W.stream);
+  halo(i, nd.r);
+  for (size_t q = 0; q < D.local.size(); ++q)
+    W.cnt.launches += launch_restrict(D.geo[q], cn.dist->geo[q], nd.r.p[q], cn.b.p[q], W.stream);
 }
 
 // First Chebyshev step coefficients (solver.cpp:90-93, 106-108) for the m = 2 blocked kernel.

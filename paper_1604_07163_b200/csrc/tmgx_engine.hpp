@@ -213,6 +213,7 @@ class Solver {
   // primitives
   void vcycle(int i);  // nodes[i].b -> nodes[i].x
   void smooth(int i, bool zero_x);
+  void residual_restrict(int i, const Field& x);  // nodes[i+1].b = R (nodes[i].b - A x)
   void halo(int i, const Field& f);
   void apply(int i, const Field& x, const Field& y);
   void coarse_solve(int i);
@@ -234,6 +235,8 @@ class Solver {
   // CG iteration as one CUDA graph (TMGX_GRAPHS=0 disables capture)
   bool use_graphs = true;
   bool tb_enabled = true;  // temporally blocked V(2,2) smoother (TMGX_TB=0 disables)
+  bool fuse_rr = false;    // fused residual + restriction on single-box levels (TMGX_FUSE_RR=1; measured
+                           // slower than residual + restriction on B200)
   bool use_tb(int i) const;
   ChebStep cheb_first_step(const Node& nd) const;
   cudaGraphExec_t iter_exec = nullptr;

@@ -703,6 +703,121 @@ __global__ void __launch_bounds__(kTBNT, NR >= 4 ? 2 : (NR == 2 ? 3 : 4))
   }
 }
 
+// Residual fused with the restriction (single-box levels, 7-point rows):
+//   r = b - A x  (k_march FApply<1> arithmetic)   b_c = 2^-3 P^T r  (k_restrict order)
+// A block owns a 15 x 7 coarse tile and marches coarse planes; its 32 x 8 threads compute the
+// residual on the 32 x 16 fine region under the tile (two rows per thread, z register queue
+// for x, +-x / +-y from L1) into a 3-plane shared ring, then 105 threads gather the 27-point
+// restriction from shared memory. DRAM traffic: x, b in, b_c out (17 B per fine point) instead
+// of 24 + 9 with r round-tripping through HBM. Out-of-grid fine vertices hold r = 0, which
+// adds exact zeros where k_restrict skips the term.
+constexpr int kRRCX = 15, kRRCY = 7;  // coarse tile
+template <bool VAR>
+__global__ void __launch_bounds__(kBX * 8)
+    k_resid_restrict(BoxGeo F, OpParams op, BoxGeo Cg, const double* __restrict__ b, const double* __restrict__ x,
+                     double* __restrict__ bc) {
+  __shared__ double rs[3][16][32];
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = tx + 32 * ty;
+  const int I0 = blockIdx.x * kRRCX, J0 = blockIdx.y * kRRCY;
+  const int K0 = blockIdx.z * Cg.zc, K1 = min(K0 + Cg.zc, Cg.ez);
+  // fine region origin (local fine coordinates) = 2 * (global coarse origin) - 1
+  const int fi = 2 * (Cg.gx + I0) - 1 - F.gx + tx;
+  const int fj0 = 2 * (Cg.gy + J0) - 1 - F.gy + ty;
+  const int gi = F.gx + fi;
+  const long long px = F.px, pxy = F.pxy;
+  bool in_p[2], fast_p[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int gj = F.gy + fj0 + 8 * h;
+    in_p[h] = gi >= 0 && gi < F.Nx && gj >= 0 && gj < F.Ny;
+    fast_p[h] = gi >= 2 && gi <= F.Nx - 3 && gj >= 2 && gj <= F.Ny - 3;
+  }
+  const int f0 = 2 * (Cg.gz + K0) - 1 - F.gz;  // first fine plane (local)
+  const int f1 = 2 * (Cg.gz + K1 - 1) + 1 - F.gz;
+  const int kin0 = -F.gz, kin1 = F.Nz - 1 - F.gz;    // in-grid plane range (local)
+  const int kf0 = 2 - F.gz, kf1 = F.Nz - 3 - F.gz;   // interior-row plane range
+  // per point: pointer to (fi, fj, f) advanced one plane per step
+  const long long o0 = F.base + fi + px * fj0 + pxy * (long long)f0;
+  const double* xp0 = x + o0;
+  const double* bp0 = b + o0;
+  const long long o8 = 8 * px;
+  auto ldx = [&](int h, int k, long long dz) -> double {  // x at point h, plane k (= f + dz)
+    return (in_p[h] && k >= kin0 && k <= kin1) ? __ldg(xp0 + (h ? o8 : 0) + dz * pxy) : 0.0;
+  };
+  double xm[2], xc[2], xn[2], xnn[2], bq[2], bqn[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    xm[h] = ldx(h, f0 - 1, -1);
+    xc[h] = ldx(h, f0, 0);
+    xn[h] = ldx(h, f0 + 1, 1);
+    bq[h] = (in_p[h] && f0 >= kin0 && f0 <= kin1) ? __ldg(bp0 + (h ? o8 : 0)) : 0.0;
+  }
+  // coarse gather role
+  const bool gth = tid < kRRCX * kRRCY;
+  const int cI = tid % kRRCX, cJ = tid / kRRCX;
+  const bool gout = gth && I0 + cI < Cg.ex && J0 + cJ < Cg.ey;
+  double* bcp = bc + vidx(Cg, I0 + cI, J0 + cJ, K0);
+  int slot = (F.gz + f0 + 3) % 3;  // ring slot of fine plane f (global plane index mod 3)
+  long long dz = 0;
+  for (int f = f0; f <= f1; ++f, dz += pxy) {
+    const bool in_z = f >= kin0 && f <= kin1, fast_z = f >= kf0 && f <= kf1;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const double* xq = xp0 + (h ? o8 : 0) + dz;
+      xnn[h] = (in_p[h] && f + 2 <= kin1 && f + 2 >= kin0) ? __ldg(xq + 2 * pxy) : 0.0;
+      bqn[h] = (in_p[h] && f + 1 <= kin1 && f + 1 >= kin0) ? __ldg(bp0 + (h ? o8 : 0) + dz + pxy) : 0.0;
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      double rr = 0.0;
+      if (in_p[h] && in_z) {
+        const double* xq = xp0 + (h ? o8 : 0) + dz;
+        const Coef c = coef_fc<VAR>(F, op, xq - x);
+        const double uw = __ldg(xq - 1), ue = __ldg(xq + 1), us = __ldg(xq - px), un = __ldg(xq + px);
+        double ax;
+        if (fast_p[h] && fast_z)
+          ax = row_full(c, xm[h], us, uw, xc[h], ue, un, xn[h]);
+        else
+          ax = row_apply(make_pt(F, fi, fj0 + 8 * h, f), c, xm[h], us, uw, xc[h], ue, un, xn[h]);
+        rr = bq[h] - ax;
+      }
+      rs[slot][ty + 8 * h][tx] = rr;
+      xm[h] = xc[h];
+      xc[h] = xn[h];
+      xn[h] = xnn[h];
+      bq[h] = bqn[h];
+    }
+    // after fine plane 2K+1 (global, odd) the coarse plane K is complete
+    const int gk = F.gz + f;
+    if ((gk & 1) && f > f0) {
+      __syncthreads();
+      if (gout) {
+        double acc = 0.0;
+#pragma unroll
+        for (int dk = -1; dk <= 1; ++dk) {
+          const double wz = dk == 0 ? 1.0 : 0.5;
+          const int sk = slot + dk - 1 < 0 ? slot + dk + 2 : (slot + dk - 1 > 2 ? slot + dk - 4 : slot + dk - 1);
+          const double(*R)[32] = rs[sk];
+#pragma unroll
+          for (int dj = -1; dj <= 1; ++dj) {
+            const double wy = dj == 0 ? 1.0 : 0.5;
+#pragma unroll
+            for (int di = -1; di <= 1; ++di) {
+              const double wx = di == 0 ? 1.0 : 0.5;
+              const double w = wx * wy * wz;
+              acc += w * R[2 * cJ + 1 + dj][2 * cI + 1 + di];
+            }
+          }
+        }
+        *bcp = 0.125 * acc;
+        bcp += Cg.pxy;
+      }
+      __syncthreads();
+    }
+    slot = slot == 2 ? 0 : slot + 1;
+  }
+}
+
 // Prolongation over vertex pairs with a z-march: xo = xf + P xc (xo may alias xf: in-place
 // x += P x_c). Every coarse neighbour of the pair is loaded unconditionally (the padded coarse
 // array holds finite values on its ghost ring) and absent terms carry weight 0; the trilinear
@@ -1414,6 +1529,18 @@ int launch_cheb2_tb(const BoxGeo& g, const OpParams& op, const double* b, const 
     launch_tb_rows<1>(g, op, b, xin, xout, s_theta, c, pre, s);
   else
     throw std::runtime_error("blocked smoother: level too small for the TMA boxes");
+  return 1;
+}
+
+bool resid_restrict_supported(const OpParams& op) { return op.S == nullptr && (op.fc != nullptr || op.k == nullptr); }
+
+int launch_resid_restrict(const BoxGeo& fine, const OpParams& op, const BoxGeo& coarse, const double* b,
+                          const double* x, double* bc, cudaStream_t s) {
+  const dim3 gr((coarse.ex + kRRCX - 1) / kRRCX, (coarse.ey + kRRCY - 1) / kRRCY, (coarse.ez + coarse.zc - 1) / coarse.zc);
+  if (op.fc)
+    k_resid_restrict<true><<<gr, dim3(32, 8), 0, s>>>(fine, op, coarse, b, x, bc);
+  else
+    k_resid_restrict<false><<<gr, dim3(32, 8), 0, s>>>(fine, op, coarse, b, x, bc);
   return 1;
 }
 

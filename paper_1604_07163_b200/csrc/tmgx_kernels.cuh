@@ -101,6 +101,10 @@ int launch_prolong_to(const BoxGeo& fine, const BoxGeo& coarse, const double* xc
 int launch_residual(const BoxGeo& g, const OpParams& op, const double* b, const double* x, double* r,
                     cudaStream_t s);
 int launch_apply(const BoxGeo& g, const OpParams& op, const double* x, double* y, cudaStream_t s);
+// Single-box levels, 7-point rows: bc = 2^-3 P^T (b - A x) with the residual kept on chip.
+bool resid_restrict_supported(const OpParams& op);
+int launch_resid_restrict(const BoxGeo& fine, const OpParams& op, const BoxGeo& coarse, const double* b,
+                          const double* x, double* bc, cudaStream_t s);
 // bc = 2^-3 P^T rf over the coarse box (rf needs a box halo incl. corners).
 int launch_restrict(const BoxGeo& fine, const BoxGeo& coarse, const double* rf, double* bc, cudaStream_t s);
 // xf += P xc (xc needs a box halo incl. corners).

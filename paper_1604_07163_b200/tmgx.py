@@ -91,6 +91,8 @@ _libs = {}
 
 
 def lib_path(parity=False):
+    if not parity and os.environ.get("TMGX_LIB"):  # tuning experiments: an alternative in-tree build
+        return os.path.join(HERE, os.environ["TMGX_LIB"])
     return os.path.join(HERE, "libtmgx_parity.so" if parity else "libtmgx.so")
 
 

@@ -19,7 +19,7 @@ s = T.SolverNode(w, T.Problem(np3, kind), T.MGConfig(nl, m, T.EST_LANCZOS))
 cfg = T.KrylovConfig("cg", rtol=rtol)
 out = {"tb": os.environ.get("TMGX_TB", "1"), "zc": os.environ.get("TMGX_TB_ZC", "32")}
 for lvl in range(nl - 1, 0, -1):
-    for which in (1, 3, 4, 5, 6, 7, 8, 9, 10):
+    for which in (1, 3, 4, 5, 6, 7, 8, 9, 10, 11):
         try:
             ms, by = s.bench_kernel(which, lvl, iters=20)
             out[f"L{lvl}_k{which}"] = [round(ms * 1e3, 2), round(by / ms / 1e6, 1)]  # us, GB/s
