@@ -270,17 +270,32 @@ def main():
     e2e_t = max_over_ranks(e2e_t)
     e2e = n_dof * args.steps / e2e_t
 
-    # ---- roofline of the dominant smoother kernel (fine-level Chebyshev pass), live
+    # ---- roofline of the dominant kernel of the solve, live (CUDA events on the library stream)
+    # The finest level runs the temporally blocked post-smooth (TMA-staged, 24 B/pt) when the
+    # blocked smoother applies (m = 2, single-box level), else the fused Chebyshev pass.
     peak, peak_kind = read_peaks()
-    ms, by = s.bench_kernel(1, nlevels - 1, iters=20)
+    tb = m == 2 and world == 1 and os.environ.get("TMGX_TB", "1") != "0" and not galerkin
+    dom_id, dom_key, dom_name = ((9, "tb_post", "k_cheb2_tb<post> (blocked V(2,2) post-smooth, fine level)") if tb
+                                 else (1, "cheb_step_last", "k_cheb_step (last pass, fine level)"))
+    ms, by = s.bench_kernel(dom_id, nlevels - 1, iters=20)
     ms_all = max_over_ranks(ms)
     achieved = by / (ms_all * 1e-3) / 1e9
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            traffic = json.load(f).get(f"{args.config}:cheb_step_last")
+            traffic = json.load(f).get(f"{args.config}:{dom_key}")
     except Exception:
         pass
+    # every fine-level kernel of the path: live us/launch and algorithmic GB/s
+    kernels = {}
+    names = {1: "cheb_step_last", 3: "residual", 4: "restrict", 5: "prolong_add", 6: "cg_update", 7: "spmv_dot",
+             8: "tb_pre", 9: "tb_post", 10: "prolong_to", 11: "resid_restrict"}
+    for kid, kname in names.items():
+        try:
+            kms, kby = s.bench_kernel(kid, nlevels - 1, iters=10)
+            kernels[kname] = {"us": round(kms * 1e3, 2), "GB/s": round(kby / (kms * 1e-3) / 1e9, 1)}
+        except Exception:  # noqa: BLE001 (kernel not applicable to this level)
+            pass
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -307,8 +322,8 @@ def main():
             "gpu_launches": launches,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "k_cheb_step (last pass, fine level)", "peak_kind": peak_kind,
-                         "bytes_per_launch": by, "ms_per_launch": ms_all},
+                         "kernel": dom_name, "peak_kind": peak_kind,
+                         "bytes_per_launch": by, "ms_per_launch": ms_all, "fine_level_kernels": kernels},
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
         }

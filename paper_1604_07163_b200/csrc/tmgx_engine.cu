@@ -361,6 +361,8 @@ Solver::Solver(World& W_, const ProblemDesc& P, const MGDesc& M) : W(W_), prob(P
   CK(cudaSetDevice(W.device));
   if (const char* e = std::getenv("TMGX_GRAPHS")) use_graphs = std::string(e) != "0";
   if (const char* e = std::getenv("TMGX_TB")) tb_enabled = std::string(e) != "0";
+  if (const char* e = std::getenv("TMGX_FUSE_CG")) fuse_cg = std::string(e) != "0";
+  if (const char* e = std::getenv("TMGX_FUSE_DOTS")) fuse_dots = std::string(e) != "0";
   if (const char* e = std::getenv("TMGX_FUSE_RR")) fuse_rr = std::string(e) != "0";
   if (mgd.nlevels < 1) throw tmg::ConfigError("mg: number of levels must be >= 1");
   if (mgd.m < 1) throw tmg::ConfigError("mg: smoother iterations must be >= 1");
@@ -464,6 +466,7 @@ void Solver::build_nodes() {
     cr = make_field(arena, D0);
     cz = make_field(arena, D0);
     cp = make_field(arena, D0);
+    cp2 = make_field(arena, D0);
     cw = make_field(arena, D0);
   }
   // buffers, operators, plans
@@ -765,6 +768,7 @@ void Solver::smooth(int i, bool zero_x) {
 // TelescopePC::apply: gather, inner V-cycle on the members, scatter back.
 void Solver::vcycle(int i) {
   Node& nd = nodes[i];
+  if (i == 0) dots_nblk = 0;
   if (nd.kind == COARSE) {
     coarse_solve(i);
     return;
@@ -789,8 +793,13 @@ void Solver::vcycle(int i) {
     halo(i + 1, cn.x);
     for (size_t q = 0; q < D.local.size(); ++q)
       W.cnt.launches += launch_prolong_to(D.geo[q], cn.dist->geo[q], cn.x.p[q], nd.d.p[q], nd.r.p[q], W.stream);
-    for (size_t q = 0; q < D.local.size(); ++q)
-      W.cnt.launches += launch_cheb2_tb(D.geo[q], nd.op[q], nd.b.p[q], nd.r.p[q], nd.x.p[q], s_theta, cs, false, W.stream);
+    if (i == 0 && D.local.size() == 1 && !parity_build() && fuse_dots)  // + the CG's r.z, z.z partials
+      W.cnt.launches += launch_cheb2_tb(D.geo[0], nd.op[0], nd.b.p[0], nd.r.p[0], nd.x.p[0], s_theta, cs, false,
+                                        W.stream, part + part_off[0], nblk_max, nblk_max, &dots_nblk);
+    else
+      for (size_t q = 0; q < D.local.size(); ++q)
+        W.cnt.launches += launch_cheb2_tb(D.geo[q], nd.op[q], nd.b.p[q], nd.r.p[q], nd.x.p[q], s_theta, cs, false,
+                                          W.stream);
     return;
   }
   smooth(i, true);
@@ -850,14 +859,14 @@ void Solver::device_allreduce_ranksums(int nslots) {
 // in a fixed tree, then summed over the communicator's ranks in rank order (the reference's
 // ordered_fold_sum, comm.cpp:338-351, at box granularity). Identical on every process.
 // The parity build replaces the tree by the reference's serial left fold (a.b recomputed).
-void Solver::reduce_local(const Dist& D, int nslots, const Field* a, const Field* b, const Field* c) {
+void Solver::reduce_local(const Dist& D, int nslots, const Field* a, const Field* b, const Field* c, int nblk) {
   for (size_t q = 0; q < D.local.size(); ++q) {
     double* out = rank_sums + D.wr[D.local[q]];
     if (parity_build() && a && b)
       W.cnt.launches += launch_fold_dot(D.geo[q], a->p[q], b->p[q], c ? c->p[q] : nullptr, out, W.R, W.stream);
     else
-      W.cnt.launches += launch_reduce_partials(part + part_off[q], grid_blocks(D.geo[q]), nslots, nblk_max, out,
-                                               W.R, W.stream);
+      W.cnt.launches += launch_reduce_partials(part + part_off[q], nblk > 0 ? nblk : grid_blocks(D.geo[q]), nslots,
+                                               nblk_max, out, W.R, W.stream);
   }
 }
 
@@ -1012,57 +1021,76 @@ void Solver::download(int i, const Field& f, double* dst, bool on_device) {
 void Solver::cg_dots(int op) {
   const Dist& D = *nodes[0].dist;
   CK(cudaMemsetAsync(rank_sums, 0, sizeof(double) * 2 * W.R, W.stream));
-  if (!parity_build())
+  const int fused = parity_build() ? 0 : dots_nblk;  // r.z, z.z partials from the finest post-smooth
+  if (!parity_build() && !fused)
     for (size_t q = 0; q < D.local.size(); ++q)
       W.cnt.launches += launch_dot2(D.geo[q], cr.p[q], cz.p[q], cz.p[q], part + part_off[q],
                                     part + part_off[q] + nblk_max, W.stream);
-  reduce_local(D, 2, &cr, &cz, &cz);
+  reduce_local(D, 2, &cr, &cz, &cz, fused);
   device_allreduce_ranksums(2);
   W.cnt.launches += launch_cg_scalars(op, rank_sums, W.R, ranks_dev, D.h.n_ranks(), scal, W.stream);
 }
 
-void Solver::cg_iteration() {
+// Single-box fine level: p = z + beta p fused into w = A p (ping-pong between cp and cp2 by
+// iteration parity, one captured graph per parity).
+bool Solver::fused_cg() const {
+  const Node& top = nodes[0];
+  return fuse_cg && top.dist->h.n_ranks() == 1 && top.dist->local.size() == 1 && pspmv_supported(top.op[0]);
+}
+
+void Solver::cg_iteration(int par) {
   Node& top = nodes[0];
   const Dist& D = *top.dist;
   const size_t nb = D.local.size();
-  for (size_t q = 0; q < nb; ++q) W.cnt.launches += launch_p_update(D.geo[q], cz.p[q], cp.p[q], scal, S_BETA, W.stream);
-  halo(0, cp);
+  const bool fused = fused_cg();
+  Field& pn = (fused && par == 0) ? cp2 : cp;  // direction written this iteration
   CK(cudaMemsetAsync(rank_sums, 0, sizeof(double) * 2 * W.R, W.stream));
-  for (size_t q = 0; q < nb; ++q)
-    W.cnt.launches += launch_spmv_dot(D.geo[q], top.op[q], cp.p[q], cw.p[q], part + part_off[q], W.stream);
-  reduce_local(D, 1, &cp, &cw, nullptr);
+  if (fused) {
+    const Field& po = par == 0 ? cp : cp2;
+    W.cnt.launches += launch_pspmv_dot(D.geo[0], top.op[0], cz.p[0], po.p[0], pn.p[0], cw.p[0], part + part_off[0],
+                                       scal, S_BETA, W.stream);
+  } else {
+    for (size_t q = 0; q < nb; ++q)
+      W.cnt.launches += launch_p_update(D.geo[q], cz.p[q], cp.p[q], scal, S_BETA, W.stream);
+    halo(0, cp);
+    for (size_t q = 0; q < nb; ++q)
+      W.cnt.launches += launch_spmv_dot(D.geo[q], top.op[q], cp.p[q], cw.p[q], part + part_off[q], W.stream);
+  }
+  reduce_local(D, 1, &pn, &cw, nullptr);
   device_allreduce_ranksums(1);
   W.cnt.launches += launch_cg_scalars(CG_ALPHA, rank_sums, W.R, ranks_dev, D.h.n_ranks(), scal, W.stream);
   for (size_t q = 0; q < nb; ++q)
-    W.cnt.launches += launch_cg_update(D.geo[q], cp.p[q], cw.p[q], cx.p[q], cr.p[q], scal, S_ALPHA, S_FLAG_PW,
+    W.cnt.launches += launch_cg_update(D.geo[q], pn.p[q], cw.p[q], cx.p[q], cr.p[q], scal, S_ALPHA, S_FLAG_PW,
                                        W.stream);
   vcycle(0);
   cg_dots(CG_BETA);
   CK(cudaMemcpyAsync(host_scal, scal, sizeof(double) * S_NSLOTS, cudaMemcpyDeviceToHost, W.stream));
 }
 
-void Solver::run_iteration() {
+void Solver::run_iteration(int par) {
+  if (!fused_cg()) par = 0;
   if (!use_graphs) {
-    cg_iteration();
+    cg_iteration(par);
     return;
   }
-  if (!iter_exec) {
+  if (!iter_exec[par]) {
     const long long l0 = W.cnt.launches;
     cudaGraph_t g;
     CK(cudaStreamBeginCapture(W.stream, cudaStreamCaptureModeThreadLocal));
-    cg_iteration();
+    cg_iteration(par);
     CK(cudaStreamEndCapture(W.stream, &g));
-    CK(cudaGraphInstantiate(&iter_exec, g, 0));
+    CK(cudaGraphInstantiate(&iter_exec[par], g, 0));
     CK(cudaGraphDestroy(g));
     iter_launches = W.cnt.launches - l0;
     W.cnt.launches = l0;
   }
-  CK(cudaGraphLaunch(iter_exec, W.stream));
+  CK(cudaGraphLaunch(iter_exec[par], W.stream));
   W.cnt.launches += iter_launches;
 }
 
 Solver::~Solver() {
-  if (iter_exec) cudaGraphExecDestroy(iter_exec);
+  for (auto& e : iter_exec)
+    if (e) cudaGraphExecDestroy(e);
   if (host_scal) cudaFreeHost(host_scal);
 }
 
@@ -1113,9 +1141,12 @@ int Solver::solve(const double* b, double* x, bool on_device, int method, double
     if (nrm0 <= tol) {
       *reason = nrm0 <= atol ? 1 : 0;
     } else {
-      for (size_t q = 0; q < nb; ++q) CK(cudaMemsetAsync(cp.p[q], 0, sizeof(double) * D.geo[q].total, W.stream));
+      for (size_t q = 0; q < nb; ++q) {
+        CK(cudaMemsetAsync(cp.p[q], 0, sizeof(double) * D.geo[q].total, W.stream));
+        CK(cudaMemsetAsync(cp2.p[q], 0, sizeof(double) * D.geo[q].total, W.stream));
+      }
       for (int it = 1; it <= max_its; ++it) {
-        run_iteration();
+        run_iteration((it - 1) & 1);
         CK(cudaStreamSynchronize(W.stream));
         if (host_scal[S_FLAG_PW] != 0.0) {  // solver.cpp:237-241 (x, r not updated)
           *reason = 4;

@@ -196,7 +196,7 @@ class Solver {
   std::vector<Sphere> spheres;
 
   // CG workspace on the top node's distribution
-  Field cx, cr, cz, cp, cw;
+  Field cx, cr, cz, cp, cp2, cw;
   double* part = nullptr;       // per local box partials [box][2][nblk]
   std::vector<long long> part_off;
   int nblk_max = 0;
@@ -221,7 +221,7 @@ class Solver {
 
   // collectives: per-box partials -> deterministic rank-ordered sums over dist (host)
   std::array<double, 2> collect2(int i, int nslots, const Field* a, const Field* b);
-  void reduce_local(const Dist& D, int nslots, const Field* a, const Field* b, const Field* c);
+  void reduce_local(const Dist& D, int nslots, const Field* a, const Field* b, const Field* c, int nblk = 0);
   void device_allreduce_ranksums(int nslots);
 
   // compact (host or device) <-> field
@@ -235,15 +235,19 @@ class Solver {
   // CG iteration as one CUDA graph (TMGX_GRAPHS=0 disables capture)
   bool use_graphs = true;
   bool tb_enabled = true;  // temporally blocked V(2,2) smoother (TMGX_TB=0 disables)
+  bool fuse_dots = true;   // CG r.z, z.z from the finest blocked post-smooth (TMGX_FUSE_DOTS=0)
+  int dots_nblk = 0;       // partials written by the last finest post-smooth (0: none)
+  bool fuse_cg = true;     // p update fused into w = A p on single-box fine levels (TMGX_FUSE_CG=0)
   bool fuse_rr = false;    // fused residual + restriction on single-box levels (TMGX_FUSE_RR=1; measured
                            // slower than residual + restriction on B200)
   bool use_tb(int i) const;
   ChebStep cheb_first_step(const Node& nd) const;
-  cudaGraphExec_t iter_exec = nullptr;
+  cudaGraphExec_t iter_exec[2] = {nullptr, nullptr};  // one captured CG iteration per p parity
   long long iter_launches = 0;
   void cg_dots(int op);
-  void cg_iteration();
-  void run_iteration();
+  void cg_iteration(int par);
+  void run_iteration(int par);
+  bool fused_cg() const;
 
  private:
   void build_nodes();

@@ -31,6 +31,8 @@
 #include <stdexcept>
 #include <string>
 #include <tuple>
+#include <type_traits>
+#include <utility>
 
 namespace tmgx {
 
@@ -251,9 +253,29 @@ __global__ void k_fill_rhs(BoxGeo g, double* __restrict__ b, unsigned long long 
 // and optionally two dot-product partials (block-reduced at the end).
 // ------------------------------------------------------------------------------------------
 
-template <bool VAR, class F>
+// Stencil input loaders: one array, or u = z + beta p (the CG direction update fused into the
+// operator apply; same expression as k_p_update, evaluated identically at every neighbour; the
+// new p goes to a different buffer, so neighbours always read the old one).
+struct ULoad {
+  const double* __restrict__ u;
+  __device__ double2 two(long long o) const { return ld2(u + o); }
+  __device__ double one(long long o) const { return __ldg(u + o); }
+};
+struct UPDir {
+  const double* __restrict__ z;
+  const double* __restrict__ p;
+  double beta;
+  __device__ double2 two(long long o) const {
+    const double2 zv = ld2(z + o), pv = ld2(p + o);
+    return double2{zv.x + beta * pv.x, zv.y + beta * pv.y};
+  }
+  __device__ double one(long long o) const { return __ldg(z + o) + beta * __ldg(p + o); }
+};
+
+template <bool VAR, class F, class U = ULoad>
 __global__ void __launch_bounds__(kBX* kBY)
-    k_march(BoxGeo g, OpParams op, const double* __restrict__ u, F f) {
+    k_march(BoxGeo g, OpParams op, U u, F f, const double* __restrict__ scal, int beta_slot) {
+  if constexpr (!std::is_same<U, ULoad>::value) u.beta = scal[beta_slot];
   __shared__ double sh[32];
   const int i0 = 2 * (blockIdx.x * kBX + threadIdx.x), j = blockIdx.y * kBY + threadIdx.y;
   double acc0 = 0.0, acc1 = 0.0;
@@ -261,7 +283,7 @@ __global__ void __launch_bounds__(kBX* kBY)
     const bool two = i0 + 1 < g.ex;
     const int k0 = blockIdx.z * g.zc, k1 = min(k0 + g.zc, g.ez);
     long long v = vidx(g, i0, j, k0);
-    double2 um = ld2(u + v - g.pxy), uc = ld2(u + v), un = ld2(u + v + g.pxy);
+    double2 um = u.two(v - g.pxy), uc = u.two(v), un = u.two(v + g.pxy);
     // VAR: precomputed rows (fc planes D, FX, FY, FZ); the -z face comes from a z queue
     const double *fD = op.fc, *fX = op.fc + op.fc_stride, *fY = op.fc + 2 * op.fc_stride,
                  *fZ = op.fc + 3 * op.fc_stride;
@@ -272,11 +294,11 @@ __global__ void __launch_bounds__(kBX* kBY)
       double2 unn{0.0, 0.0};
       typename F::In inn{};
       if (k + 1 < k1) {  // prefetch the next plane
-        unn = ld2(u + v + 2 * g.pxy);
+        unn = u.two(v + 2 * g.pxy);
         inn = f.load(v + g.pxy);
       }
-      const double2 uym = ld2(u + v - g.px), uyp = ld2(u + v + g.px);
-      const double uxl = __ldg(u + v - 1), uxr = __ldg(u + v + 2);
+      const double2 uym = u.two(v - g.px), uyp = u.two(v + g.px);
+      const double uxl = u.one(v - 1), uxr = u.one(v + 2);
       double2 dd{0.0, 0.0}, fx{0.0, 0.0}, fy{0.0, 0.0}, fym{0.0, 0.0}, fz{0.0, 0.0};
       double fxl = 0.0;
       if (VAR) {
@@ -560,10 +582,12 @@ __device__ __forceinline__ double row_full(const Coef& c, double uzm, double uym
   return acc;
 }
 
-template <bool VAR, bool PRE, int NR>
+template <bool VAR, bool PRE, int NR, bool DOTS = false>
 __global__ void __launch_bounds__(kTBNT, NR >= 4 ? 2 : (NR == 2 ? 3 : 4))
     k_cheb2_tb(const __grid_constant__ TBMaps maps, BoxGeo g, OpParams op, double* __restrict__ xout, double s_theta,
-               double c1, double c2) {
+               double c1, double c2, double* __restrict__ dpart, long long dstride) {
+  // DOTS (finest post-smooth of the CG preconditioner): block partials of b.x' and x'.x', i.e.
+  // the CG's r.z and z.z (solver.cpp:245-250) from the values already on chip.
   using G = TBG<NR>;
   using SM = TBSmem<NR, PRE>;
   constexpr int NS = SM::NS;
@@ -616,6 +640,7 @@ __global__ void __launch_bounds__(kTBNT, NR >= 4 ? 2 : (NR == 2 ? 3 : 4))
   int sl = 0, isl = kTBPF, psl = NS - 1;  // slots of groups t, t + kTBPF, t - 1
   unsigned ph = 0;                         // mbarrier parity of group t
   double* outp = xout + g.base + i + g.px * (long long)j0 + g.pxy * (long long)(T0 - LAG1 - 1);
+  double dot_bz = 0.0, dot_zz = 0.0;
   for (int t = T0; t <= T1; ++t, outp += g.pxy) {
     const int p1 = t - LAG1, p2 = p1 - 1;  // pass-1 and pass-2 planes
     mbar_wait(sbar + 8 * sl, ph);
@@ -685,7 +710,13 @@ __global__ void __launch_bounds__(kTBNT, NR >= 4 ? 2 : (NR == 2 ? 3 : 4))
         const double r1 = rq1[r] - ad;
         const double z = r1 * c.invd;
         const double dn = c1 * d0 + c2 * z;
-        outp[g.px * r] = x1 + dn;
+        const double xo = x1 + dn;
+        outp[g.px * r] = xo;
+        if (DOTS) {
+          const double bo = reinterpret_cast<const double*>(S.b[psl])[(jr0 + r) * kTBSX + tx + 1];  // b(p2)
+          dot_bz += bo * xo;
+          dot_zz += xo * xo;
+        }
       }
     }
     // rotate the queues and the slot ring
@@ -700,6 +731,15 @@ __global__ void __launch_bounds__(kTBNT, NR >= 4 ? 2 : (NR == 2 ? 3 : 4))
     psl = sl;
     if (++sl == NS) sl = 0, ph ^= 1u;
     if (++isl == NS) isl = 0;
+  }
+  if (DOTS) {
+    __shared__ double sh[32];
+    const double s0 = block_sum(dot_bz, sh);
+    const double s1 = block_sum(dot_zz, sh);
+    if (tid == 0) {
+      dpart[blk_linear()] = s0;
+      dpart[dstride + blk_linear()] = s1;
+    }
   }
 }
 
@@ -989,6 +1029,30 @@ struct FSpmvDot {
     a0 += uc * au;
   }
   __device__ void store(long long v, const Out& o, bool two) const { st2(w + v, o.w, two); }
+  __device__ void partials(int blk, double s0, double) const { part[blk] = s0; }
+};
+
+// p' = z + beta p written to a second buffer, w = A p', block partial of p'.w
+// (solver.cpp:261-262 then 235-236)
+struct FSpmvDotP {
+  double* w;
+  double* p_out;
+  double* part;
+  static constexpr int kDots = 1;
+  struct In {};
+  struct Out {
+    double2 w, p;
+  };
+  __device__ In load(long long) const { return In{}; }
+  __device__ void point(int q, double au, double, double uc, const In&, Out& o, double& a0, double&) const {
+    set(o.w, q, au);
+    set(o.p, q, uc);
+    a0 += uc * au;
+  }
+  __device__ void store(long long v, const Out& o, bool two) const {
+    st2(w + v, o.w, two);
+    st2(p_out + v, o.p, two);
+  }
   __device__ void partials(int blk, double s0, double) const { part[blk] = s0; }
 };
 
@@ -1384,9 +1448,24 @@ static void march(const BoxGeo& g, const OpParams& op, const double* u, const F&
   if (op.S)
     k_march27<F><<<tile_grid(g), kBlock, 0, s>>>(g, op, u, f);
   else if (op.fc)
-    k_march<true, F><<<tile_grid(g), kBlock, 0, s>>>(g, op, u, f);
+    k_march<true, F><<<tile_grid(g), kBlock, 0, s>>>(g, op, ULoad{u}, f, nullptr, 0);
   else
-    k_march<false, F><<<tile_grid(g), kBlock, 0, s>>>(g, op, u, f);
+    k_march<false, F><<<tile_grid(g), kBlock, 0, s>>>(g, op, ULoad{u}, f, nullptr, 0);
+}
+
+bool pspmv_supported(const OpParams& op) { return op.S == nullptr && (op.fc != nullptr || op.k == nullptr); }
+
+// p_new = z + beta p_old, w = A p_new and the block partials of p_new.w in one pass (single-box
+// levels: the stencil reads z and p_old at the neighbours, so no halo of p_new is needed).
+int launch_pspmv_dot(const BoxGeo& g, const OpParams& op, const double* z, const double* p_old, double* p_new,
+                     double* w, double* part, const double* scal, int beta_slot, cudaStream_t s) {
+  const UPDir u{z, p_old, 0.0};
+  const FSpmvDotP f{w, p_new, part};
+  if (op.fc)
+    k_march<true, FSpmvDotP, UPDir><<<tile_grid(g), kBlock, 0, s>>>(g, op, u, f, scal, beta_slot);
+  else
+    k_march<false, FSpmvDotP, UPDir><<<tile_grid(g), kBlock, 0, s>>>(g, op, u, f, scal, beta_slot);
+  return 1;
 }
 
 int launch_cheb_start_res(const BoxGeo& g, const OpParams& op, const double* b, const double* x, double* r, double* d,
@@ -1464,8 +1543,10 @@ static CUtensorMap tensor_map(const BoxGeo& g, const double* base_ptr, int bx, i
 }
 
 template <int NR>
-static void launch_tb_rows(const BoxGeo& g, const OpParams& op, const double* b, const double* xin, double* xout,
-                           double s_theta, ChebStep c, bool pre, cudaStream_t s) {
+static int launch_tb_rows(const BoxGeo& g, const OpParams& op, const double* b, const double* xin, double* xout,
+                          double s_theta, ChebStep c, bool pre, double* dpart, long long dstride, int dmax,
+                          cudaStream_t s) {
+  int nblk = 0;
   using G = TBG<NR>;
   TBMaps maps;
   std::memset(&maps, 0, sizeof(maps));
@@ -1481,7 +1562,8 @@ static void launch_tb_rows(const BoxGeo& g, const OpParams& op, const double* b,
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kTBNT, smem);
       slots = std::max(1, sms * std::max(per, 1));
     }
-    // z planes per block: minimise waves x (planes + pipeline fill) over the split count
+    // z planes per block: minimise waves x (planes + pipeline fill) over the split count (a
+    // pure function of the geometry, so repeated launches agree on the block count)
     BoxGeo gt = g;
     const long long cols = (long long)((g.ex + G::OX - 1) / G::OX) * ((g.ey + G::OY - 1) / G::OY);
     static const int zc_env = [] {
@@ -1502,33 +1584,54 @@ static void launch_tb_rows(const BoxGeo& g, const OpParams& op, const double* b,
     }
     gt.zc = best;
     const dim3 gr((g.ex + G::OX - 1) / G::OX, (g.ey + G::OY - 1) / G::OY, (g.ez + gt.zc - 1) / gt.zc);
-    kern<<<gr, bl, smem, s>>>(maps, gt, op, xout, s_theta, c.c1, c.c2);
+    nblk = (int)(gr.x * gr.y * gr.z);
+    return std::make_pair(gr, gt);
   };
-  static int slots[4] = {0, 0, 0, 0};
+  auto run = [&](auto kern, size_t smem, int& slots, bool dots) {
+    auto [gr, gt] = go(kern, smem, slots);
+    if (dots && nblk > dmax) return false;  // partial buffer too small: caller falls back
+    kern<<<gr, bl, smem, s>>>(maps, gt, op, xout, s_theta, c.c1, c.c2, dpart, dstride);
+    return true;
+  };
+  static int slots[6] = {0, 0, 0, 0, 0, 0};
+  const bool dots = dpart != nullptr && !pre;
+  bool ok;
   if (op.fc) {
     if (pre)
-      go(k_cheb2_tb<true, true, NR>, sizeof(TBSmem<NR, true>), slots[0]);
+      ok = run(k_cheb2_tb<true, true, NR>, sizeof(TBSmem<NR, true>), slots[0], false);
+    else if (dots)
+      ok = run(k_cheb2_tb<true, false, NR, true>, sizeof(TBSmem<NR, false>), slots[4], true);
     else
-      go(k_cheb2_tb<true, false, NR>, sizeof(TBSmem<NR, false>), slots[1]);
+      ok = run(k_cheb2_tb<true, false, NR>, sizeof(TBSmem<NR, false>), slots[1], false);
   } else {
     if (pre)
-      go(k_cheb2_tb<false, true, NR>, sizeof(TBSmem<NR, true>), slots[2]);
+      ok = run(k_cheb2_tb<false, true, NR>, sizeof(TBSmem<NR, true>), slots[2], false);
+    else if (dots)
+      ok = run(k_cheb2_tb<false, false, NR, true>, sizeof(TBSmem<NR, false>), slots[5], true);
     else
-      go(k_cheb2_tb<false, false, NR>, sizeof(TBSmem<NR, false>), slots[3]);
+      ok = run(k_cheb2_tb<false, false, NR>, sizeof(TBSmem<NR, false>), slots[3], false);
   }
+  return ok ? (dots ? nblk : 0) : -1;
 }
 
 int launch_cheb2_tb(const BoxGeo& g, const OpParams& op, const double* b, const double* xin, double* xout,
-                    double s_theta, ChebStep c, bool pre, cudaStream_t s) {
+                    double s_theta, ChebStep c, bool pre, cudaStream_t s, double* dpart, long long dstride, int dmax,
+                    int* dblocks) {
   const int nr = tb_rows();
+  int nb;
   if (nr >= 4 && tb_fits<4>(g))
-    launch_tb_rows<4>(g, op, b, xin, xout, s_theta, c, pre, s);
+    nb = launch_tb_rows<4>(g, op, b, xin, xout, s_theta, c, pre, dpart, dstride, dmax, s);
   else if (nr >= 2 && tb_fits<2>(g))
-    launch_tb_rows<2>(g, op, b, xin, xout, s_theta, c, pre, s);
+    nb = launch_tb_rows<2>(g, op, b, xin, xout, s_theta, c, pre, dpart, dstride, dmax, s);
   else if (tb_fits<1>(g))
-    launch_tb_rows<1>(g, op, b, xin, xout, s_theta, c, pre, s);
+    nb = launch_tb_rows<1>(g, op, b, xin, xout, s_theta, c, pre, dpart, dstride, dmax, s);
   else
     throw std::runtime_error("blocked smoother: level too small for the TMA boxes");
+  if (nb < 0) {  // no room for the fused partials: plain launch
+    nb = 0;
+    launch_cheb2_tb(g, op, b, xin, xout, s_theta, c, pre, s);
+  }
+  if (dblocks) *dblocks = nb;
   return 1;
 }
 

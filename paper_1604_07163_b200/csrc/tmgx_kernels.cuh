@@ -92,8 +92,11 @@ int launch_cheb_step(const BoxGeo& g, const OpParams& op, const double* d, const
                      double* d_new, double* r_out, double* x_out, ChebStep c, bool last, cudaStream_t s);
 // Temporally blocked m = 2 Chebyshev side (single-box levels, 7-point operator, TMA-staged):
 // pre (x = 0): xout = S(b); post: xout = S(b, xin) with xin != xout.
+// dpart (post only): also write block partials of b.x' and x'.x' (slots dpart, dpart + dstride,
+// at most dmax blocks); *dblocks = number of partials written (0: not fused).
 int launch_cheb2_tb(const BoxGeo& g, const OpParams& op, const double* b, const double* xin, double* xout,
-                    double s_theta, ChebStep c, bool pre, cudaStream_t s);
+                    double s_theta, ChebStep c, bool pre, cudaStream_t s, double* dpart = nullptr,
+                    long long dstride = 0, int dmax = 0, int* dblocks = nullptr);
 bool cheb2_tb_supported(const BoxGeo& g);
 // xo = xf + P xc (out of place)
 int launch_prolong_to(const BoxGeo& fine, const BoxGeo& coarse, const double* xc, const double* xf, double* xo,
@@ -120,6 +123,10 @@ int launch_galerkin(const BoxGeo& fine, const OpParams& fop, const BoxGeo& coars
 int grid_blocks(const BoxGeo& g);
 int launch_spmv_dot(const BoxGeo& g, const OpParams& op, const double* p, double* w, double* part,
                     cudaStream_t s);
+bool pspmv_supported(const OpParams& op);
+// p_new = z + beta p_old ; w = A p_new ; part = block partials of p_new.w (beta = scal[beta_slot])
+int launch_pspmv_dot(const BoxGeo& g, const OpParams& op, const double* z, const double* p_old, double* p_new,
+                     double* w, double* part, const double* scal, int beta_slot, cudaStream_t s);
 int launch_dot2(const BoxGeo& g, const double* a, const double* b, const double* c, double* part_ab,
                 double* part_cc, cudaStream_t s);  // a.b and c.c
 int launch_jacobi_dot(const BoxGeo& g, const OpParams& op, const double* r, double* z, double* part,
