@@ -181,6 +181,37 @@ int tmgx_coarse_solve(tmgx_solver s, const double *b, double *x);            /* 
 int tmgx_telescope_gather(tmgx_solver s, int stage, const double *x_parent, double *x_sub);
 int tmgx_telescope_scatter(tmgx_solver s, int stage, const double *y_sub, double *y_parent);
 
+/* Options database + solver-tree builder (the reference's missing options.cpp /
+ * solver_build.cpp): PETSc-style prefixed keys drive the GPU hierarchy, e.g.
+ * the paper's boxes "-pc_type mg -pc_mg_levels N1 -pc_mg_galerkin
+ * -mg_coarse_pc_type telescope -mg_coarse_pc_telescope_reduction_factor r
+ * -mg_coarse_telescope_pc_type mg -mg_coarse_telescope_pc_mg_levels N2 ...". String outputs
+ * are NUL-terminated; a buffer that is too small is a ConfigError naming the size needed. */
+typedef struct tmgx_options_s *tmgx_options;
+int tmgx_options_create(tmgx_options *out);
+int tmgx_options_destroy(tmgx_options o);
+/* parse(argv): "-key [value]" tokens, later keys win, a "-key" followed by
+ * another "-key" or the end is a flag ("true"); malformed token -> ConfigError with position. */
+int tmgx_options_parse(tmgx_options o, int argc, const char *const *argv);
+/* options file text: one "-key value" per line, '#' comments */
+int tmgx_options_parse_file_text(tmgx_options o, const char *text);
+int tmgx_options_set(tmgx_options o, const char *key, const char *value);
+/* *found = 0/1; value copied into buf when found (marks the key used) */
+int tmgx_options_get(tmgx_options o, const char *key, char *buf, int buflen, int *found);
+/* all entries as "-key value" tokens separated by '\n' (reparses to an equal database) */
+int tmgx_options_serialize(tmgx_options o, char *buf, int buflen);
+/* keys never looked up, separated by '\n' (the reference warns on these at teardown) */
+int tmgx_options_unused(tmgx_options o, char *buf, int buflen);
+/* build_solver_tree resolved onto the GPU hierarchy without touching the GPU:
+ * <prefix>ksp_type (default_ksp when unset; NULL = the reference's "gmres"), <prefix>pc_type mg,
+ * MG smoother keys under <prefix>mg_levels_, coarse solver under <prefix>mg_coarse_, telescope
+ * sub-solver under <prefix>mg_coarse_telescope_ (recursively). describe: the resolved tree. */
+int tmgx_options_resolve(tmgx_options o, const char *prefix, const char *default_ksp, tmgx_mg_cfg *mg,
+                         tmgx_ksp_cfg *ksp, char *describe, int describe_len);
+/* resolve + tmgx_solver_create; *ksp receives the outer KSP for tmgx_solve */
+int tmgx_solver_from_options(tmgx_world w, const tmgx_problem *prob, tmgx_options o, const char *prefix,
+                             const char *default_ksp, tmgx_solver *out, tmgx_ksp_cfg *ksp);
+
 /* Counters: kernel launches, halo/telescope bytes moved between processes. */
 typedef struct {
   int64_t kernel_launches;

@@ -4,6 +4,7 @@
 #include <memory>
 #include <string>
 
+#include "tmg_options.hpp"
 #include "tmgx.h"
 #include "tmgx_engine.hpp"
 
@@ -13,6 +14,9 @@ struct tmgx_world_s {
 struct tmgx_solver_s {
   tmgx_world world;
   std::unique_ptr<tmgx::Solver> s;
+};
+struct tmgx_options_s {
+  tmg::OptionsDatabase db;
 };
 
 namespace {
@@ -90,6 +94,44 @@ int check_level(tmgx_solver s, int level) {
   if (!s || !s->s) throw tmg::Error("null solver");
   if (level < 0 || level >= s->s->mgd.nlevels) throw tmg::Error("level out of range");
   return s->s->node_for_level(level);
+}
+}  // namespace
+
+// ---- options database / solver tree (tmg_options.hpp)
+namespace {
+void copy_out(const std::string& v, char* buf, int buflen) {
+  if (!buf) return;
+  if ((int)v.size() + 1 > buflen)
+    throw tmg::ConfigError("output buffer too small: need " + std::to_string(v.size() + 1) + " bytes");
+  std::memcpy(buf, v.c_str(), v.size() + 1);
+}
+std::string lines(const std::vector<std::string>& v) {
+  std::string s;
+  for (size_t i = 0; i < v.size(); ++i) s += (i ? "\n" : "") + v[i];
+  return s;
+}
+void resolved_to_c(const tmg::ResolvedTree& r, tmgx_mg_cfg* mg, tmgx_ksp_cfg* ksp) {
+  if (mg) {
+    std::memset(mg, 0, sizeof(*mg));
+    mg->nlevels = r.nlevels;
+    mg->smooth_its = r.smooth_its;
+    mg->est_mode = r.est_mode;
+    mg->cheb_bounds = nullptr;
+    if ((int)r.stages.size() > TMGX_MAX_TELESCOPE) throw tmg::ConfigError("too many telescope stages");
+    mg->n_telescope = (int)r.stages.size();
+    for (size_t t = 0; t < r.stages.size(); ++t) {
+      mg->telescope[t].level = r.stages[t].level;
+      mg->telescope[t].reduction_factor = r.stages[t].reduction_factor;
+      for (int a = 0; a < 3; ++a) mg->telescope[t].override_[a] = r.stages[t].override_[a];
+    }
+    mg->galerkin = r.galerkin ? 1 : 0;
+  }
+  if (ksp) {
+    ksp->method = r.ksp_method;
+    ksp->rtol = r.rtol;
+    ksp->atol = r.atol;
+    ksp->max_its = r.max_its;
+  }
 }
 }  // namespace
 
@@ -224,6 +266,80 @@ int tmgx_solver_create(tmgx_world w, const tmgx_problem* p, const tmgx_mg_cfg* m
       throw;
     }
     *out = s;
+    return 0;
+  });
+}
+
+
+int tmgx_options_create(tmgx_options* out) {
+  return guard([&] {
+    *out = new tmgx_options_s;
+    return 0;
+  });
+}
+int tmgx_options_destroy(tmgx_options o) {
+  return guard([&] {
+    delete o;
+    return 0;
+  });
+}
+int tmgx_options_parse(tmgx_options o, int argc, const char* const* argv) {
+  return guard([&] {
+    std::vector<std::string> t;
+    for (int i = 0; i < argc; ++i) t.emplace_back(argv[i]);
+    o->db.parse(t);
+    return 0;
+  });
+}
+int tmgx_options_parse_file_text(tmgx_options o, const char* text) {
+  return guard([&] {
+    o->db.parse_file_text(text ? text : "");
+    return 0;
+  });
+}
+int tmgx_options_set(tmgx_options o, const char* key, const char* value) {
+  return guard([&] {
+    o->db.set(key, value ? value : "true");
+    return 0;
+  });
+}
+int tmgx_options_get(tmgx_options o, const char* key, char* buf, int buflen, int* found) {
+  return guard([&] {
+    auto v = o->db.get(key);
+    *found = v ? 1 : 0;
+    if (v) copy_out(*v, buf, buflen);
+    return 0;
+  });
+}
+int tmgx_options_serialize(tmgx_options o, char* buf, int buflen) {
+  return guard([&] {
+    copy_out(lines(o->db.serialize()), buf, buflen);
+    return 0;
+  });
+}
+int tmgx_options_unused(tmgx_options o, char* buf, int buflen) {
+  return guard([&] {
+    copy_out(lines(o->db.unused()), buf, buflen);
+    return 0;
+  });
+}
+int tmgx_options_resolve(tmgx_options o, const char* prefix, const char* default_ksp, tmgx_mg_cfg* mg,
+                         tmgx_ksp_cfg* ksp, char* describe, int describe_len) {
+  return guard([&] {
+    const auto r = tmg::resolve_solver_tree(o->db, prefix ? prefix : "", default_ksp ? default_ksp : "gmres");
+    resolved_to_c(r, mg, ksp);
+    copy_out(r.describe, describe, describe_len);
+    return 0;
+  });
+}
+int tmgx_solver_from_options(tmgx_world w, const tmgx_problem* prob, tmgx_options o, const char* prefix,
+                             const char* default_ksp, tmgx_solver* out, tmgx_ksp_cfg* ksp) {
+  return guard([&] {
+    const auto r = tmg::resolve_solver_tree(o->db, prefix ? prefix : "", default_ksp ? default_ksp : "gmres");
+    tmgx_mg_cfg mg;
+    resolved_to_c(r, &mg, ksp);
+    const int rc = tmgx_solver_create(w, prob, &mg, out);
+    if (rc) throw tmg::ConfigError(g_err);
     return 0;
   });
 }

@@ -85,6 +85,9 @@ EXPORTS = [
     "tmgx_pc_apply", "tmgx_level_apply", "tmgx_level_smooth", "tmgx_level_residual_restrict",
     "tmgx_level_prolong_add", "tmgx_coarse_solve", "tmgx_telescope_gather", "tmgx_telescope_scatter",
     "tmgx_get_counters", "tmgx_parity_build", "tmgx_last_error", "tmgx_bench_kernel", "tmgx_plan_summary",
+    "tmgx_options_create", "tmgx_options_destroy", "tmgx_options_parse", "tmgx_options_parse_file_text",
+    "tmgx_options_set", "tmgx_options_get", "tmgx_options_serialize", "tmgx_options_unused",
+    "tmgx_options_resolve", "tmgx_solver_from_options",
 ]
 
 _libs = {}
@@ -139,6 +142,17 @@ def load(parity: bool = False):
         "tmgx_get_counters": [C.c_void_p, P(_Counters)],
         "tmgx_bench_kernel": [C.c_void_p, C.c_int, C.c_int, C.c_int, D, D],
         "tmgx_plan_summary": [C.c_int, C.c_int, C.c_int, P(_Problem), P(_MG), I64, C.c_int, P(C.c_int)],
+        "tmgx_options_create": [P(C.c_void_p)],
+        "tmgx_options_destroy": [C.c_void_p],
+        "tmgx_options_parse": [C.c_void_p, C.c_int, P(C.c_char_p)],
+        "tmgx_options_parse_file_text": [C.c_void_p, C.c_char_p],
+        "tmgx_options_set": [C.c_void_p, C.c_char_p, C.c_char_p],
+        "tmgx_options_get": [C.c_void_p, C.c_char_p, C.c_char_p, C.c_int, P(C.c_int)],
+        "tmgx_options_serialize": [C.c_void_p, C.c_char_p, C.c_int],
+        "tmgx_options_unused": [C.c_void_p, C.c_char_p, C.c_int],
+        "tmgx_options_resolve": [C.c_void_p, C.c_char_p, C.c_char_p, P(_MG), P(_Ksp), C.c_char_p, C.c_int],
+        "tmgx_solver_from_options": [C.c_void_p, P(_Problem), C.c_void_p, C.c_char_p, C.c_char_p, P(C.c_void_p),
+                                     P(_Ksp)],
     }
     sig["tmgx_repartition_header"] = [H, C.c_int, P(C.c_int), H]
     for name, args in sig.items():
@@ -352,6 +366,110 @@ class MGConfig:
     cheb_bounds: Optional[Sequence[float]] = None
     telescope: List[TelescopeStage] = field(default_factory=list)
     galerkin: bool = False  # -pc_mg_galerkin: 2^-3 P^T A P coarse operators (27-point)
+
+
+# ----------------------------------------------------------------- options
+class OptionsDatabase:
+    """Prefix-keyed options database (the reference's missing options.cpp): ordered
+    key -> string map with the leading dash stripped, flags stored as "true", later
+    insertions winning, and used-key tracking. Backed by the C++ host layer of libtmgx."""
+
+    def __init__(self, tokens: Optional[Sequence[str]] = None, parity: bool = False):
+        self.L = load(parity)
+        h = C.c_void_p()
+        _check(self.L, self.L.tmgx_options_create(C.byref(h)))
+        self.h = h
+        if tokens:
+            self.parse(tokens)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.L.tmgx_options_destroy(self.h)
+            self.h = None
+
+    def parse(self, tokens: Sequence[str]):
+        """parse(argv); ConfigError on a malformed token (with its position)."""
+        arr = (C.c_char_p * max(len(tokens), 1))(*[t.encode() for t in tokens])
+        _check(self.L, self.L.tmgx_options_parse(self.h, len(tokens), arr))
+        return self
+
+    def parse_file_text(self, text: str):
+        _check(self.L, self.L.tmgx_options_parse_file_text(self.h, text.encode()))
+        return self
+
+    @classmethod
+    def from_file(cls, path: str, parity: bool = False):
+        with open(path) as f:
+            return cls(parity=parity).parse_file_text(f.read())
+
+    def set(self, key: str, value: str = "true"):
+        _check(self.L, self.L.tmgx_options_set(self.h, key.encode(), str(value).encode()))
+        return self
+
+    def get(self, key: str) -> Optional[str]:
+        buf = C.create_string_buffer(4096)
+        found = C.c_int()
+        _check(self.L, self.L.tmgx_options_get(self.h, key.encode(), buf, len(buf), C.byref(found)))
+        return buf.value.decode() if found.value else None
+
+    def _lines(self, fn) -> List[str]:
+        n = 1 << 16
+        while True:
+            buf = C.create_string_buffer(n)
+            rc = fn(self.h, buf, n)
+            if rc == 0:
+                v = buf.value.decode()
+                return v.split("\n") if v else []
+            if n > (1 << 26):
+                _check(self.L, rc)
+            n *= 4
+
+    def serialize(self) -> List[str]:
+        """Tokens that reparse to an equal database."""
+        out = []
+        for ln in self._lines(self.L.tmgx_options_serialize):
+            out.append(ln)
+        return out
+
+    def unused(self) -> List[str]:
+        return self._lines(self.L.tmgx_options_unused)
+
+    def items(self):
+        t = self.serialize()
+        return [(t[i][1:], t[i + 1]) for i in range(0, len(t), 2)]
+
+
+@dataclass
+class ResolvedTree:
+    ksp: KrylovConfig
+    mg: MGConfig
+    describe: str
+
+
+def resolve_solver_tree(db: OptionsDatabase, prefix: str = "", default_ksp: Optional[str] = None) -> ResolvedTree:
+    """build_solver_tree resolved onto the GPU hierarchy, host only: the fused
+    level ladder (N1 + N2 - 1 levels), telescope stages, smoother and outer KSP."""
+    mg, ksp = _MG(), _Ksp()
+    buf = C.create_string_buffer(1 << 16)
+    _check(db.L, db.L.tmgx_options_resolve(db.h, prefix.encode(), default_ksp.encode() if default_ksp else None,
+                                           C.byref(mg), C.byref(ksp), buf, len(buf)))
+    stages = []
+    for t in range(mg.n_telescope):
+        st = mg.telescope[t]
+        ov = tuple(int(st.override_[a]) or None for a in range(3))
+        stages.append(TelescopeStage(int(st.level), int(st.reduction_factor), ov))
+    cfg = MGConfig(nlevels=mg.nlevels, smooth_its=mg.smooth_its, est_mode=mg.est_mode, telescope=stages,
+                   galerkin=bool(mg.galerkin))
+    method = {KSP_CG: "cg", KSP_PREONLY: "preonly"}[ksp.method]
+    return ResolvedTree(KrylovConfig(method, ksp.rtol, ksp.atol, ksp.max_its), cfg, buf.value.decode())
+
+
+def build_solver_tree(db: OptionsDatabase, world: "World", problem: "Problem", prefix: str = "",
+                      default_ksp: Optional[str] = None):
+    """Instantiate the GPU solver from the options (KSP/PC tree).
+    Returns (SolverNode, KrylovConfig for SolverNode.solve)."""
+    r = resolve_solver_tree(db, prefix, default_ksp)
+    return SolverNode(world, problem, r.mg), r.ksp
 
 
 def nccl_unique_id(parity=False):

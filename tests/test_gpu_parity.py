@@ -348,3 +348,33 @@ def test_galerkin_decomposed_telescoped_bitwise():
     y8n = np.empty_like(y8)
     y8n[perm] = y8
     assert np.array_equal(y8n, y1)
+
+
+# ---------------------------------------------------------------- options-driven trees
+@pytest.mark.parametrize("n_ranks,opts,direct", [
+    # §3.3.1 truncation box (N = 4 levels here, nc = 4): telescope onto one rank + LU
+    (4, "-pc_type mg -pc_mg_levels 4 -mg_coarse_pc_type telescope -mg_coarse_pc_telescope_reduction_factor 4 "
+        "-mg_coarse_telescope_pc_type lu", dict(nlevels=4, telescope=[T.TelescopeStage(0, 4)])),
+    # §3.3.2 repartitioned coarse grid (N1 = 2, N2 = 3, r = 8): 4 fused levels, Galerkin
+    (8, "-pc_type mg -pc_mg_levels 2 -pc_mg_galerkin -mg_coarse_pc_type telescope "
+        "-mg_coarse_pc_telescope_reduction_factor 8 -mg_coarse_telescope_pc_type mg "
+        "-mg_coarse_telescope_pc_mg_levels 3 -mg_coarse_telescope_pc_mg_galerkin",
+     dict(nlevels=4, telescope=[T.TelescopeStage(2, 8)], galerkin=True)),
+])
+def test_options_tree_solve_matches_direct(n_ranks, opts, direct):
+    """build_solver_tree on the paper's boxes drives the same GPU hierarchy as the direct
+    configuration: bitwise-identical solves in the parity build (SPEC.md:646 'instantiate without
+    error and solve the 3D Poisson fixture to rtol 1e-8')."""
+    np3 = (33, 33, 33)
+    dbo = T.OptionsDatabase(("-ksp_type cg -ksp_rtol 1e-8 " + opts).split(), parity=True)
+    w = T.World(n_ranks=n_ranks, parity=True)
+    s_opt, ksp = T.build_solver_tree(dbo, w, T.Problem(np3))
+    assert dbo.unused() == []
+    s_dir = T.SolverNode(w, T.Problem(np3), T.MGConfig(smooth_its=2, est_mode=T.EST_LANCZOS, **direct))
+    h, _ = s_opt.level_info(direct["nlevels"] - 1)
+    perm = T.rank_block_to_natural(h)
+    b = O.rhs(np3, 42)[perm]
+    x1, r1 = s_opt.solve(b, cfg=ksp)
+    x2, r2 = s_dir.solve(b, cfg=T.KrylovConfig("cg", rtol=1e-8))
+    assert r1.converged() and r1.iterations == r2.iterations
+    assert np.array_equal(x1, x2)
