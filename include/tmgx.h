@@ -221,6 +221,13 @@ typedef struct {
 } tmgx_counters;
 int tmgx_get_counters(tmgx_solver s, tmgx_counters *c);
 
+/* Telescope timing in the paper's Table 1/2 schema: T_setup = host time of
+ * the stage's plan construction (P-hat / ScatterPlan analogue) + upload during solver setup;
+ * T_apply = device time of one gather + one scatter of the stage's level vector, averaged over
+ * `reps`; bytes_per_apply = 2 x 8 x level size. */
+int tmgx_telescope_timing(tmgx_solver s, int stage, int reps, double *t_setup_s, double *t_apply_s,
+                          int64_t *bytes_per_apply);
+
 /* Host-only (no GPU): the data-movement plans process `proc` of `nproc` would build for this
  * problem/hierarchy. One record of 6 int64 per (plan, peer): {plan_id (3*node + 0 halo,
  * +1 telescope gather, +2 telescope scatter), kind (0 send, 1 recv, 2 local copy), peer

@@ -534,6 +534,38 @@ int tmgx_telescope_scatter(tmgx_solver s, int stage, const double* ys, double* y
   });
 }
 
+int tmgx_telescope_timing(tmgx_solver s, int stage, int reps, double* t_setup_s, double* t_apply_s,
+                          int64_t* bytes_per_apply) {
+  return guard([&] {
+    auto& S = *s->s;
+    if (stage < 0 || stage >= (int)S.stage_node.size()) throw tmg::Error("no such telescope stage");
+    if (reps < 1) throw tmg::ConfigError("reps must be >= 1");
+    const int i = S.stage_node[stage];
+    auto& nd = S.nodes[i];
+    auto apply = [&] {  // TelescopePC::apply data movement: gather of b, scatter of x
+      tmgx::run_plan(S.W, nd.gather, nd.b, S.nodes[i + 1].b, true);
+      tmgx::run_plan(S.W, nd.scatter, S.nodes[i + 1].x, nd.x, true);
+    };
+    apply();
+    tmgx::cuda_check(cudaStreamSynchronize(S.W.stream), "sync");
+    cudaEvent_t e0, e1;
+    tmgx::cuda_check(cudaEventCreate(&e0), "event");
+    tmgx::cuda_check(cudaEventCreate(&e1), "event");
+    tmgx::cuda_check(cudaEventRecord(e0, S.W.stream), "record");
+    for (int r = 0; r < reps; ++r) apply();
+    tmgx::cuda_check(cudaEventRecord(e1, S.W.stream), "record");
+    tmgx::cuda_check(cudaEventSynchronize(e1), "sync");
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (t_setup_s) *t_setup_s = nd.t_setup_s;
+    if (t_apply_s) *t_apply_s = ms * 1e-3 / reps;
+    if (bytes_per_apply) *bytes_per_apply = 2 * 8 * (int64_t)nd.dist->h.n_unknowns();
+    return 0;
+  });
+}
+
 int tmgx_plan_summary(int n_ranks, int nproc, int proc, const tmgx_problem* p, const tmgx_mg_cfg* m, int64_t* out,
                       int max_records, int* n_records) {
   return guard([&] {

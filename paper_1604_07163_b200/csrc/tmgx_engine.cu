@@ -1,6 +1,8 @@
 // Host orchestration of the MG-CG path; see tmgx_engine.hpp for the reference map.
 #include "tmgx_engine.hpp"
 
+#include <chrono>
+
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -505,9 +507,12 @@ void Solver::build_nodes() {
     nd.halo = upload_plan(arena, halo_plan_host(W, D));
   }
   for (size_t i = 0; i < nodes.size(); ++i)
-    if (nodes[i].kind == TELESCOPE) {
+    if (nodes[i].kind == TELESCOPE) {  // TelescopePC setup: the P-hat^T / ScatterPlan data movement
+      const auto t0 = std::chrono::steady_clock::now();
       nodes[i].gather = upload_plan(arena, transfer_plan_host(W, *nodes[i].dist, *nodes[i + 1].dist));
       nodes[i].scatter = upload_plan(arena, transfer_plan_host(W, *nodes[i + 1].dist, *nodes[i].dist));
+      CK(cudaStreamSynchronize(W.stream));
+      nodes[i].t_setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     }
   part = arena.alloc((long long)nloc_max * 2 * nblk_max);
   for (int q = 0; q < nloc_max; ++q) part_off.push_back((long long)q * 2 * nblk_max);

@@ -172,6 +172,7 @@ struct Node {
   double lo = 0.1, hi = 1.1;
   // telescope
   RegionPlan gather, scatter;
+  double t_setup_s = 0.0;  // host time of the stage's plan construction + upload
   // coarse
   int nc = 0;
   double* A_dev = nullptr;  // Ainv (perf) or LU (parity)

@@ -87,7 +87,7 @@ EXPORTS = [
     "tmgx_get_counters", "tmgx_parity_build", "tmgx_last_error", "tmgx_bench_kernel", "tmgx_plan_summary",
     "tmgx_options_create", "tmgx_options_destroy", "tmgx_options_parse", "tmgx_options_parse_file_text",
     "tmgx_options_set", "tmgx_options_get", "tmgx_options_serialize", "tmgx_options_unused",
-    "tmgx_options_resolve", "tmgx_solver_from_options",
+    "tmgx_options_resolve", "tmgx_solver_from_options", "tmgx_telescope_timing",
 ]
 
 _libs = {}
@@ -151,6 +151,7 @@ def load(parity: bool = False):
         "tmgx_options_serialize": [C.c_void_p, C.c_char_p, C.c_int],
         "tmgx_options_unused": [C.c_void_p, C.c_char_p, C.c_int],
         "tmgx_options_resolve": [C.c_void_p, C.c_char_p, C.c_char_p, P(_MG), P(_Ksp), C.c_char_p, C.c_int],
+        "tmgx_telescope_timing": [C.c_void_p, C.c_int, C.c_int, D, D, I64],
         "tmgx_solver_from_options": [C.c_void_p, P(_Problem), C.c_void_p, C.c_char_p, C.c_char_p, P(C.c_void_p),
                                      P(_Ksp)],
     }
@@ -573,6 +574,12 @@ class SolverNode:
             pass
 
     # --- introspection
+    def telescope_timing(self, stage=0, reps=20):
+        """(T_setup s, T_apply s, bytes per apply) of telescope stage `stage` (Table 1)."""
+        ts, ta, by = C.c_double(), C.c_double(), C.c_int64()
+        _check(self.L, self.L.tmgx_telescope_timing(self.h, stage, reps, C.byref(ts), C.byref(ta), C.byref(by)))
+        return ts.value, ta.value, by.value
+
     def level_info(self, level):
         h = Header()
         n = C.c_int64()
