@@ -217,6 +217,7 @@ def main():
                      T.MGConfig(nlevels, m, est, telescope=tele, galerkin=galerkin))
     t_setup = time.perf_counter() - t0
     cfg = T.KrylovConfig("cg", rtol=rtol)
+    cfg_e2e = T.KrylovConfig("cg", rtol=rtol, initial_guess_nonzero=False)  # x0 = 0: x is output only
     n_local = s.local_size()
     n_dof = np3[0] * np3[1] * np3[2]
 
@@ -258,13 +259,13 @@ def main():
     b_host.numpy()[:] = b_np
     for _ in range(max(args.warmup, 1)):
         x_host.zero_()
-        s.solve_ptr(b_host.data_ptr(), x_host.data_ptr(), False, cfg)
+        s.solve_ptr(b_host.data_ptr(), x_host.data_ptr(), False, cfg_e2e)
     barrier()
     e2e_t = 0.0
     for _ in range(args.steps):
         x_host.zero_()
         t0 = time.perf_counter()
-        rep_e = s.solve_ptr(b_host.data_ptr(), x_host.data_ptr(), False, cfg)
+        rep_e = s.solve_ptr(b_host.data_ptr(), x_host.data_ptr(), False, cfg_e2e)
         e2e_t += time.perf_counter() - t0
     barrier()
     e2e_t = max_over_ranks(e2e_t)
@@ -317,7 +318,7 @@ def main():
                        "l2": "inputs larger than L2 (one fine vector = %.0f MB)" % (n_dof * 8 / 1e6),
                        "iterations": its[-1] if its else None, "t_setup_s": t_setup,
                        "wall_ms_per_step": t_wall / args.steps * 1e3},
-            "e2e": {"value": e2e, "unit": "DOF/s", "h2d_bytes_per_step": 2 * 8 * n_dof,
+            "e2e": {"value": e2e, "unit": "DOF/s", "h2d_bytes_per_step": 8 * n_dof,
                     "d2h_bytes_per_step": 8 * n_dof},
             "gpu_launches": launches,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -130,6 +130,8 @@ typedef struct {
   double rtol;
   double atol;
   int max_its;
+  int zero_initial_guess; /* 1: x is output only (PETSc's default, x0 = 0 without reading x);
+                             0: x is the initial guess (the reference's krylov_solve) */
 } tmgx_ksp_cfg;
 
 /* SolveReport (solver.hpp:39-52) + timings. */

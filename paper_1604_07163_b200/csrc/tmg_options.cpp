@@ -263,6 +263,8 @@ ResolvedTree resolve_solver_tree(const OptionsDatabase& db, const std::string& p
   r.rtol = db.get_real(prefix + "ksp_rtol", 1e-8);
   r.atol = db.get_real(prefix + "ksp_atol", 1e-50);
   r.max_its = (int)db.get_int(prefix + "ksp_max_it", 10000);
+  // PETSc's KSPSetInitialGuessNonzero; the reference's krylov_solve reads x, so nonzero by default
+  r.zero_initial_guess = !db.get_bool(prefix + "ksp_initial_guess_nonzero", true);
   b.desc << "ksp " << kt << " (rtol " << r.rtol << ", atol " << r.atol << ", max_it " << r.max_its << ")\n";
   b.pc(prefix, 1, false);
 

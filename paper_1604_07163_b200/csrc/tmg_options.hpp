@@ -61,6 +61,7 @@ struct ResolvedTree {
   int ksp_method = 2;  // TMGX_KSP_CG / TMGX_KSP_PREONLY
   double rtol = 1e-8, atol = 1e-50;
   int max_its = 10000;
+  bool zero_initial_guess = false;  // -ksp_initial_guess_nonzero false
   int nlevels = 1;
   int smooth_its = 2;
   int est_mode = 1;  // TMGX_EST_LANCZOS

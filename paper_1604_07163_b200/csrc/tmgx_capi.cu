@@ -131,6 +131,7 @@ void resolved_to_c(const tmg::ResolvedTree& r, tmgx_mg_cfg* mg, tmgx_ksp_cfg* ks
     ksp->rtol = r.rtol;
     ksp->atol = r.atol;
     ksp->max_its = r.max_its;
+    ksp->zero_initial_guess = r.zero_initial_guess ? 1 : 0;
   }
 }
 }  // namespace
@@ -391,7 +392,7 @@ int tmgx_solve(tmgx_solver s, const double* b, double* x, int on_device, const t
     int reason, its;
     double n0, nf;
     const int rc = S.solve(b, x, on_device != 0, cfg->method, cfg->rtol, cfg->atol, cfg->max_its, history, &reason,
-                           &its, &n0, &nf, &t_ms, false, 0);
+                           &its, &n0, &nf, &t_ms, false, 0, cfg->zero_initial_guess == 0);
     rep->reason = reason;
     rep->iterations = its;
     rep->norm0 = n0;

@@ -1101,7 +1101,7 @@ Solver::~Solver() {
 
 int Solver::solve(const double* b, double* x, bool on_device, int method, double rtol, double atol, int max_its,
                   double* hist, int* reason, int* its, double* norm0, double* normf, double* t_ms, bool seeded,
-                  unsigned long long seed) {
+                  unsigned long long seed, bool x0_nonzero) {
   CK(cudaSetDevice(W.device));
   Node& top = nodes[0];
   const Dist& D = *top.dist;
@@ -1127,7 +1127,7 @@ int Solver::solve(const double* b, double* x, bool on_device, int method, double
     *its = 1;
     *norm0 = *normf = 0.0;
   } else {
-    if (x && !seeded)
+    if (x && !seeded && x0_nonzero)
       upload(0, cx, x, on_device);
     else
       for (size_t q = 0; q < nb; ++q) CK(cudaMemsetAsync(cx.p[q], 0, sizeof(double) * D.geo[q].total, W.stream));

@@ -231,7 +231,7 @@ class Solver {
 
   int solve(const double* b, double* x, bool on_device, int method, double rtol, double atol, int max_its,
             double* hist, int* reason, int* its, double* norm0, double* normf, double* t_ms, bool seeded,
-            unsigned long long seed);
+            unsigned long long seed, bool x0_nonzero = true);
 
   // CG iteration as one CUDA graph (TMGX_GRAPHS=0 disables capture)
   bool use_graphs = true;

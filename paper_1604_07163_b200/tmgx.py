@@ -62,7 +62,8 @@ class _MG(C.Structure):
 
 
 class _Ksp(C.Structure):
-    _fields_ = [("method", C.c_int), ("rtol", C.c_double), ("atol", C.c_double), ("max_its", C.c_int)]
+    _fields_ = [("method", C.c_int), ("rtol", C.c_double), ("atol", C.c_double), ("max_its", C.c_int),
+                ("zero_initial_guess", C.c_int)]
 
 
 class _Report(C.Structure):
@@ -323,6 +324,7 @@ class KrylovConfig:
     rtol: float = 1e-8
     atol: float = 1e-50
     max_its: int = 10000
+    initial_guess_nonzero: bool = True  # False: x is output only (x0 = 0, not uploaded)
 
 
 @dataclass
@@ -462,7 +464,8 @@ def resolve_solver_tree(db: OptionsDatabase, prefix: str = "", default_ksp: Opti
     cfg = MGConfig(nlevels=mg.nlevels, smooth_its=mg.smooth_its, est_mode=mg.est_mode, telescope=stages,
                    galerkin=bool(mg.galerkin))
     method = {KSP_CG: "cg", KSP_PREONLY: "preonly"}[ksp.method]
-    return ResolvedTree(KrylovConfig(method, ksp.rtol, ksp.atol, ksp.max_its), cfg, buf.value.decode())
+    return ResolvedTree(KrylovConfig(method, ksp.rtol, ksp.atol, ksp.max_its, not ksp.zero_initial_guess), cfg,
+                        buf.value.decode())
 
 
 def build_solver_tree(db: OptionsDatabase, world: "World", problem: "Problem", prefix: str = "",
@@ -611,6 +614,7 @@ class SolverNode:
         if k.method < 0:
             raise ConfigError(f"unknown ksp_type '{cfg.method}' on this path (valid: cg, preonly)")
         k.rtol, k.atol, k.max_its = cfg.rtol, cfg.atol, cfg.max_its
+        k.zero_initial_guess = 0 if cfg.initial_guess_nonzero else 1
         return k
 
     def _report(self, rep, hist, cfg):

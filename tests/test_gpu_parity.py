@@ -378,3 +378,14 @@ def test_options_tree_solve_matches_direct(n_ranks, opts, direct):
     x2, r2 = s_dir.solve(b, cfg=T.KrylovConfig("cg", rtol=1e-8))
     assert r1.converged() and r1.iterations == r2.iterations
     assert np.array_equal(x1, x2)
+
+
+def test_zero_initial_guess_ignores_x():
+    """ksp_initial_guess_nonzero false (PETSc's default): x is output only, never read."""
+    np3 = (33, 33, 33)
+    w, s = make(np3, 4, parity=True)
+    b = O.rhs(np3, 42)
+    x0, r0 = s.solve(b, cfg=T.KrylovConfig("cg", rtol=1e-8))
+    junk = np.full_like(b, np.nan)
+    x1, r1 = s.solve(b, x=junk, cfg=T.KrylovConfig("cg", rtol=1e-8, initial_guess_nonzero=False))
+    assert r1.iterations == r0.iterations and np.array_equal(x0, x1)

@@ -167,3 +167,10 @@ def test_smoother_side_telescope_boxes_are_out_of_scope(box):
     (SURVEY.md §2); the builder says so instead of silently ignoring the keys."""
     with pytest.raises(T.ConfigError, match="out of the GPU hot path"):
         T.resolve_solver_tree(db("-ksp_type cg -pc_type mg " + box))
+
+
+def test_initial_guess_key():
+    r = T.resolve_solver_tree(db("-ksp_type cg -ksp_initial_guess_nonzero false -pc_type mg -pc_mg_levels 2"))
+    assert r.ksp.initial_guess_nonzero is False
+    r = T.resolve_solver_tree(db("-ksp_type cg -pc_type mg -pc_mg_levels 2"))
+    assert r.ksp.initial_guess_nonzero is True  # the reference's krylov_solve reads x
