@@ -214,6 +214,24 @@ int tmgx_options_resolve(tmgx_options o, const char *prefix, const char *default
 int tmgx_solver_from_options(tmgx_world w, const tmgx_problem *prob, tmgx_options o, const char *prefix,
                              const char *default_ksp, tmgx_solver *out, tmgx_ksp_cfg *ksp);
 
+/* Q1 hexahedral linear elasticity MG-CG (BASELINE configs[4]; no reference implementation,
+ * discretisation defined in tmgx_elast.cu / oracle/tmg_elast_oracle.c): N^3 vertices x 3 dofs,
+ * E_e = 10^(3 u(seed_e, e)) per element, nu, clamped x = 0 face, body force (0, 0, -1),
+ * point-block Jacobi Chebyshev V(m,m), rediscretised coarse levels, LU on level 0. One box
+ * on one GPU. Vectors: natural vertex order, 3 interleaved dofs (host or device memory). */
+typedef struct tmgx_elast_s *tmgx_elast;
+int tmgx_elast_create(tmgx_world w, const int64_t np[3], int nlevels, int smooth_its, int est_mode, uint64_t seed_e,
+                      double nu, tmgx_elast *out);
+int tmgx_elast_destroy(tmgx_elast e);
+int tmgx_elast_kref(double nu, double *k576);      /* 24x24 reference stiffness (E = 1, unit cube) */
+int tmgx_elast_level_info(tmgx_elast e, int level, int64_t np[3], double *lo, double *hi);
+int tmgx_elast_rhs(tmgx_elast e, double *b);       /* body-force load of the finest level (host) */
+int tmgx_elast_level_apply(tmgx_elast e, int level, const double *x, double *y);
+int tmgx_elast_level_smooth(tmgx_elast e, int level, const double *b, double *x); /* x in/out */
+int tmgx_elast_pc_apply(tmgx_elast e, const double *x, double *y);                /* one V-cycle */
+int tmgx_elast_solve(tmgx_elast e, const double *b, double *x, const tmgx_ksp_cfg *cfg, double *history,
+                     tmgx_report *rep);
+
 /* Counters: kernel launches, halo/telescope bytes moved between processes. */
 typedef struct {
   int64_t kernel_launches;

@@ -56,6 +56,11 @@ class MGCfg(C.Structure):
     ]
 
 
+class ElCfg(C.Structure):
+    _fields_ = [("np", C.c_int64 * 3), ("nlevels", C.c_int), ("smooth_its", C.c_int), ("est_mode", C.c_int),
+                ("seed_e", C.c_uint64), ("nu", C.c_double)]
+
+
 class Report(C.Structure):
     _fields_ = [("reason", C.c_int), ("iterations", C.c_int), ("norm0", C.c_double),
                 ("norm_final", C.c_double)]
@@ -113,6 +118,20 @@ def lib():
         L.orc_mgcg_solve.argtypes = [C.c_void_p, D, D, C.c_double, C.c_double, C.c_int, D, C.POINTER(Report)]
         L.orc_estimate_dense.restype = C.c_double
         L.orc_estimate_dense.argtypes = [C.c_int, D, C.c_int, C.c_int]
+        L.orc_el_kref.argtypes = [C.c_double, D]
+        L.orc_el_create.restype = C.c_void_p
+        L.orc_el_create.argtypes = [C.POINTER(ElCfg)]
+        L.orc_el_destroy.argtypes = [C.c_void_p]
+        L.orc_el_level_nv.restype = C.c_int64
+        L.orc_el_level_nv.argtypes = [C.c_void_p, C.c_int]
+        L.orc_el_bounds.argtypes = [C.c_void_p, C.c_int, D, D]
+        L.orc_el_elements.argtypes = [C.c_void_p, C.c_int, D]
+        for fn in ("orc_el_apply", "orc_el_jacobi", "orc_el_smooth", "orc_el_restrict", "orc_el_prolong_add",
+                   "orc_el_vcycle"):
+            getattr(L, fn).argtypes = [C.c_void_p, C.c_int, D, D]
+        L.orc_el_coarse_solve.argtypes = [C.c_void_p, D, D]
+        L.orc_el_rhs.argtypes = [I64, D]
+        L.orc_el_solve.argtypes = [C.c_void_p, D, D, C.c_double, C.c_double, C.c_int, D, C.POINTER(Report)]
         _lib = L
     return _lib
 
@@ -324,3 +343,99 @@ def dot(x, y):
 def estimate_dense(A, jacobi=False, mode=EST_LANCZOS):
     A = np.ascontiguousarray(A, dtype=np.float64)
     return lib().orc_estimate_dense(A.shape[0], _dp(A), int(jacobi), mode)
+
+
+# ---------------------------------------------------------------- Q1 elasticity (tmg_elast_oracle.c)
+def el_kref(nu=0.3):
+    K = np.zeros(576)
+    lib().orc_el_kref(nu, _dp(K))
+    return K.reshape(24, 24)
+
+
+def el_rhs(np3):
+    n = int(np3[0] * np3[1] * np3[2])
+    b = np.zeros(3 * n)
+    npa = np.array(np3, dtype=np.int64)
+    lib().orc_el_rhs(_ip64(npa), _dp(b))
+    return b
+
+
+class ElastMG:
+    """Q1 elasticity MG hierarchy (3 interleaved dofs per vertex; level 0 = coarsest, LU)."""
+
+    def __init__(self, np3, nlevels, smooth_its=2, est_mode=EST_LANCZOS, seed_e=11, nu=0.3):
+        cfg = ElCfg()
+        cfg.np = (C.c_int64 * 3)(*np3)
+        cfg.nlevels, cfg.smooth_its, cfg.est_mode, cfg.seed_e, cfg.nu = nlevels, smooth_its, est_mode, seed_e, nu
+        self.cfg = cfg
+        self.nlevels = nlevels
+        self.np3 = tuple(np3)
+        self.h = lib().orc_el_create(C.byref(cfg))
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().orc_el_destroy(self.h)
+            self.h = None
+
+    def level_nv(self, level):
+        return int(lib().orc_el_level_nv(self.h, level))
+
+    def level_size(self, level):
+        return 3 * self.level_nv(level)
+
+    def bounds(self, level):
+        lo, hi = C.c_double(), C.c_double()
+        lib().orc_el_bounds(self.h, level, C.byref(lo), C.byref(hi))
+        return lo.value, hi.value
+
+    def elements(self, level):
+        n = round(self.level_nv(level) ** (1 / 3))
+        out = np.zeros((n - 1) ** 3)
+        lib().orc_el_elements(self.h, level, _dp(out))
+        return out
+
+    def _lv(self, fn, level, x, out=None):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.zeros(self.level_size(level)) if out is None else out
+        getattr(lib(), fn)(self.h, level, _dp(x), _dp(y))
+        return y
+
+    def apply(self, level, x):
+        return self._lv("orc_el_apply", level, x)
+
+    def jacobi(self, level, x):
+        return self._lv("orc_el_jacobi", level, x)
+
+    def smooth(self, level, b, x0=None):
+        x = np.zeros(self.level_size(level)) if x0 is None else np.array(x0, dtype=np.float64)
+        return self._lv("orc_el_smooth", level, b, x)
+
+    def restrict(self, fine_level, r):
+        r = np.ascontiguousarray(r, dtype=np.float64)
+        out = np.zeros(self.level_size(fine_level - 1))
+        lib().orc_el_restrict(self.h, fine_level, _dp(r), _dp(out))
+        return out
+
+    def prolong_add(self, fine_level, xc, xf):
+        xc = np.ascontiguousarray(xc, dtype=np.float64)
+        xf = np.array(xf, dtype=np.float64)
+        lib().orc_el_prolong_add(self.h, fine_level, _dp(xc), _dp(xf))
+        return xf
+
+    def vcycle(self, level, b):
+        return self._lv("orc_el_vcycle", level, b)
+
+    def coarse_solve(self, b):
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        x = np.zeros(self.level_size(0))
+        lib().orc_el_coarse_solve(self.h, _dp(b), _dp(x))
+        return x
+
+    def solve(self, b, rtol=1e-6, atol=1e-50, max_its=10000, x0=None):
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        x = np.zeros_like(b) if x0 is None else np.array(x0, dtype=np.float64)
+        hist = np.zeros(max_its + 1)
+        rep = Report()
+        lib().orc_el_solve(self.h, _dp(b), _dp(x), rtol, atol, max_its, _dp(hist), C.byref(rep))
+        return x, {"reason": REASONS[rep.reason], "iterations": rep.iterations, "norm0": rep.norm0,
+                   "norm_final": rep.norm_final, "history": hist[: rep.iterations + 1].copy()}

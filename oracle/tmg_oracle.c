@@ -552,12 +552,12 @@ static double tridiag_eig_max(int n, const double *d, const double *e) {
   return 0.5 * (lo + hi);
 }
 
-typedef void (*op_fn)(const void *ctx, const double *x, double *y);
+typedef orc_op_fn op_fn;
 
 /* chebyshev_bounds_estimate, solver.cpp:520-581. mode REFERENCE reproduces the
  * shipped loop (p never updated, :537-561); LANCZOS adds p = z + beta p. */
-static int estimate_generic(int64_t n, op_fn A, op_fn M, const void *ctx, const double *b0, int mode,
-                            double *lo_out, double *hi_out) {
+int orc_estimate_generic(int64_t n, op_fn A, op_fn M, const void *ctx, const double *b0, int mode,
+                         double *lo_out, double *hi_out) {
   const int kSteps = 10;
   double *r = malloc(sizeof(double) * n), *z = malloc(sizeof(double) * n);
   double *p = malloc(sizeof(double) * n), *w = malloc(sizeof(double) * n);
@@ -621,7 +621,7 @@ int orc_estimate(const orc_mg *mg, int level, int mode, double *lo, double *hi) 
   const orc_level *L = &mg->lev[level];
   double *b = malloc(sizeof(double) * L->nv);
   orc_fill_random(L->nv, 0x5eedbeefULL, b);
-  const int rc = estimate_generic(L->nv, lvl_A, lvl_M, L, b, mode, lo, hi);
+  const int rc = orc_estimate_generic(L->nv, lvl_A, lvl_M, L, b, mode, lo, hi);
   free(b);
   return rc;
 }
@@ -649,7 +649,7 @@ double orc_estimate_dense(int n, const double *A, int jacobi, int mode) {
   double *b = malloc(sizeof(double) * n);
   orc_fill_random(n, 0x5eedbeefULL, b);
   double lo, hi;
-  estimate_generic(n, dn_A, dn_M, &c, b, mode, &lo, &hi);
+  orc_estimate_generic(n, dn_A, dn_M, &c, b, mode, &lo, &hi);
   free(b);
   return hi / 1.1;
 }

@@ -111,6 +111,38 @@ int orc_mgcg_solve(const orc_mg *mg, const double *b, double *x, double rtol, do
 /* Dense-matrix estimator check: diag(values) with identity or Jacobi PC. */
 double orc_estimate_dense(int n, const double *A, int jacobi, int mode);
 
+/* chebyshev_bounds_estimate (solver.cpp:520-581) on any operator / preconditioner pair */
+typedef void (*orc_op_fn)(const void *ctx, const double *x, double *y);
+int orc_estimate_generic(int64_t n, orc_op_fn A, orc_op_fn M, const void *ctx, const double *b0, int mode,
+                         double *lo_out, double *hi_out);
+
+/* ---- Q1 elasticity (BASELINE configs[4]; tmg_elast_oracle.c, parity unpinned by the reference) ---- */
+typedef struct {
+  int64_t np[3];      /* vertices per axis (2M+1) */
+  int nlevels;        /* level 0 = coarsest (LU) */
+  int smooth_its;     /* V(m,m) */
+  int est_mode;       /* ORC_EST_* */
+  uint64_t seed_e;    /* E_e = 10^(3 u(seed_e, e)) */
+  double nu;          /* 0.3 */
+} orc_el_cfg;
+typedef struct orc_el_mg orc_el_mg;
+void orc_el_kref(double nu, double *K576);
+orc_el_mg *orc_el_create(const orc_el_cfg *cfg);
+void orc_el_destroy(orc_el_mg *mg);
+int64_t orc_el_level_nv(const orc_el_mg *mg, int level);
+void orc_el_bounds(const orc_el_mg *mg, int level, double *lo, double *hi);
+void orc_el_elements(const orc_el_mg *mg, int level, double *E);
+void orc_el_apply(const orc_el_mg *mg, int level, const double *x, double *y);
+void orc_el_jacobi(const orc_el_mg *mg, int level, const double *x, double *y);
+void orc_el_smooth(const orc_el_mg *mg, int level, const double *b, double *x);
+void orc_el_restrict(const orc_el_mg *mg, int fine_level, const double *rf, double *bc);
+void orc_el_prolong_add(const orc_el_mg *mg, int fine_level, const double *xc, double *xf);
+void orc_el_coarse_solve(const orc_el_mg *mg, const double *b, double *x);
+void orc_el_vcycle(const orc_el_mg *mg, int level, const double *b, double *x);
+void orc_el_rhs(const int64_t np[3], double *b);
+int orc_el_solve(const orc_el_mg *mg, const double *b, double *x, double rtol, double atol, int max_its,
+                 double *history, orc_report *rep);
+
 #ifdef __cplusplus
 }
 #endif

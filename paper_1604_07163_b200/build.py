@@ -16,7 +16,7 @@ from concurrent.futures import ThreadPoolExecutor
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = ["tmg_grid.cpp", "tmg_options.cpp", "tmgx_kernels.cu", "tmgx_engine.cu", "tmgx_capi.cu"]
+SOURCES = ["tmg_grid.cpp", "tmg_options.cpp", "tmgx_kernels.cu", "tmgx_engine.cu", "tmgx_elast.cu", "tmgx_capi.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -6,6 +6,7 @@
 
 #include "tmg_options.hpp"
 #include "tmgx.h"
+#include "tmgx_elast.hpp"
 #include "tmgx_engine.hpp"
 
 struct tmgx_world_s {
@@ -14,6 +15,10 @@ struct tmgx_world_s {
 struct tmgx_solver_s {
   tmgx_world world;
   std::unique_ptr<tmgx::Solver> s;
+};
+struct tmgx_elast_s {
+  tmgx_world world;
+  std::unique_ptr<tmgx::ElastSolver> s;
 };
 struct tmgx_options_s {
   tmg::OptionsDatabase db;
@@ -564,6 +569,124 @@ int tmgx_telescope_timing(tmgx_solver s, int stage, int reps, double* t_setup_s,
     if (t_apply_s) *t_apply_s = ms * 1e-3 / reps;
     if (bytes_per_apply) *bytes_per_apply = 2 * 8 * (int64_t)nd.dist->h.n_unknowns();
     return 0;
+  });
+}
+
+// ---- Q1 elasticity (tmgx_elast.cu)
+int tmgx_elast_create(tmgx_world w, const int64_t np[3], int nlevels, int smooth_its, int est_mode, uint64_t seed_e,
+                      double nu, tmgx_elast* out) {
+  return guard([&] {
+    auto e = new tmgx_elast_s;
+    e->world = w;
+    try {
+      e->s = std::make_unique<tmgx::ElastSolver>(*w->w, np, nlevels, smooth_its, est_mode, seed_e, nu);
+    } catch (...) {
+      delete e;
+      throw;
+    }
+    *out = e;
+    return 0;
+  });
+}
+int tmgx_elast_destroy(tmgx_elast e) {
+  return guard([&] {
+    delete e;
+    return 0;
+  });
+}
+int tmgx_elast_kref(double nu, double* k576) {
+  return guard([&] {
+    tmgx::q1_kref(nu, k576);
+    return 0;
+  });
+}
+static int el_check(tmgx_elast e, int level) {
+  if (level < 0 || level >= (int)e->s->L.size()) throw tmg::ConfigError("elasticity: no such level");
+  return level;
+}
+int tmgx_elast_level_info(tmgx_elast e, int level, int64_t np[3], double* lo, double* hi) {
+  return guard([&] {
+    const auto& L = e->s->L[el_check(e, level)];
+    if (np) np[0] = L.g.ex, np[1] = L.g.ey, np[2] = L.g.ez;
+    if (lo) *lo = L.lo;
+    if (hi) *hi = L.hi;
+    return 0;
+  });
+}
+int tmgx_elast_rhs(tmgx_elast e, double* b) {
+  return guard([&] {
+    // b_z(v) = sum over incident elements of -h^3/8 (exact: powers of two), 0 on clamped dofs
+    const auto& g = e->s->L.back().g;
+    const double h = e->s->L.back().h, q = -(h * h * h) / 8.0;
+    for (int k = 0; k < g.ez; ++k)
+      for (int j = 0; j < g.ey; ++j)
+        for (int i = 0; i < g.ex; ++i) {
+          double acc = 0.0;
+          for (int ez = -1; ez <= 0; ++ez)
+            for (int ey = -1; ey <= 0; ++ey)
+              for (int ex = -1; ex <= 0; ++ex) {
+                const int ei = i + ex, ej = j + ey, ek = k + ez;
+                if (ei < 0 || ej < 0 || ek < 0 || ei >= g.ex - 1 || ej >= g.ey - 1 || ek >= g.ez - 1) continue;
+                acc += q;
+              }
+          const long long v = i + (long long)g.ex * (j + (long long)g.ey * k);
+          b[3 * v + 0] = 0.0;
+          b[3 * v + 1] = 0.0;
+          b[3 * v + 2] = i == 0 ? 0.0 : acc;
+        }
+    return 0;
+  });
+}
+int tmgx_elast_level_apply(tmgx_elast e, int level, const double* x, double* y) {
+  return guard([&] {
+    auto& S = *e->s;
+    auto& L = S.L[el_check(e, level)];
+    S.upload(level, x, L.x);
+    S.apply(level, L.x, L.ad);
+    S.download(level, L.ad, y);
+    return 0;
+  });
+}
+int tmgx_elast_level_smooth(tmgx_elast e, int level, const double* b, double* x) {
+  return guard([&] {
+    auto& S = *e->s;
+    auto& L = S.L[el_check(e, level)];
+    if (level == 0) throw tmg::ConfigError("elasticity: level 0 is the LU level");
+    S.upload(level, b, L.b);
+    S.upload(level, x, L.x);
+    S.smooth(level, L.b, L.x);
+    S.download(level, L.x, x);
+    return 0;
+  });
+}
+int tmgx_elast_pc_apply(tmgx_elast e, const double* x, double* y) {
+  return guard([&] {
+    auto& S = *e->s;
+    const int top = (int)S.L.size() - 1;
+    S.upload(top, x, S.cr);
+    S.vcycle(top, S.cr, S.cz);
+    S.download(top, S.cz, y);
+    return 0;
+  });
+}
+int tmgx_elast_solve(tmgx_elast e, const double* b, double* x, const tmgx_ksp_cfg* cfg, double* history,
+                     tmgx_report* rep) {
+  return guard([&] {
+    if (cfg->method != TMGX_KSP_CG) throw tmg::ConfigError("elasticity: ksp_type must be cg");
+    auto& S = *e->s;
+    const long long l0 = S.launches;
+    double t_ms = 0;
+    int reason = 2, its = 0;
+    double n0 = 0, nf = 0;
+    const int rc = S.solve(b, x, cfg->rtol, cfg->atol, cfg->max_its, cfg->zero_initial_guess == 0, history, &reason,
+                           &its, &n0, &nf, &t_ms);
+    rep->reason = reason;
+    rep->iterations = its;
+    rep->norm0 = n0;
+    rep->norm_final = nf;
+    rep->t_solve_s = t_ms * 1e-3;
+    rep->kernel_launches = S.launches - l0;
+    return rc;
   });
 }
 

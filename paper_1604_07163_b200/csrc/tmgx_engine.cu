@@ -309,13 +309,13 @@ void run_plan(World& W, const RegionPlan& plan, const Field& src, const Field& d
 // Solver setup
 // ------------------------------------------------------------------------------------------
 
-static unsigned long long splitmix64_h(unsigned long long x) {
+unsigned long long splitmix64_h(unsigned long long x) {
   x += 0x9e3779b97f4a7c15ULL;
   x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
   x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
   return x ^ (x >> 31);
 }
-static double hashed_uniform_h(unsigned long long seed, unsigned long long idx) {
+double hashed_uniform_h(unsigned long long seed, unsigned long long idx) {
   return (double)(splitmix64_h(seed ^ splitmix64_h(idx)) >> 11) * 0x1.0p-53;
 }
 static double harm_h(double a, double b) { return 2.0 * a * b / (a + b); }
@@ -579,6 +579,67 @@ void Solver::build_galerkin() {
 
 // LUPC (precond.cpp:220-229): dense LU of the coarse operator, factored on the host with
 // DenseLU::factor's partial pivoting (precond.cpp:11-48).
+// DenseLU::factor (precond.cpp:11-48) of a dense row-major matrix and its device copy: the
+// factors + pivots for the parity build's substitution (k_lu_solve), or the explicit inverse
+// built from the same factors for the performance build (k_dense_matvec). map[c] = device
+// offset of compact unknown c.
+void dense_lu_setup(DeviceArena& arena, std::vector<double> a, int n, const std::vector<long long>& map,
+                    double** A_dev, long long** piv_dev, long long** map_dev) {
+  std::vector<long long> piv((size_t)n);
+  for (int kk2 = 0; kk2 < n; ++kk2) {  // precond.cpp:26-46
+    int p = kk2;
+    double best = std::fabs(a[(size_t)kk2 * n + kk2]);
+    for (int i = kk2 + 1; i < n; ++i)
+      if (std::fabs(a[(size_t)i * n + kk2]) > best) {
+        best = std::fabs(a[(size_t)i * n + kk2]);
+        p = i;
+      }
+    if (best == 0.0) throw tmg::Error("lu factorization: matrix is singular at column " + std::to_string(kk2));
+    piv[(size_t)kk2] = p;
+    if (p != kk2)
+      for (int j = 0; j < n; ++j) std::swap(a[(size_t)kk2 * n + j], a[(size_t)p * n + j]);
+    const double pivot = a[(size_t)kk2 * n + kk2];
+    for (int i = kk2 + 1; i < n; ++i) {
+      const double m = a[(size_t)i * n + kk2] / pivot;
+      a[(size_t)i * n + kk2] = m;
+      if (m == 0.0) continue;
+      for (int j = kk2 + 1; j < n; ++j) {
+        volatile double t = m * a[(size_t)kk2 * n + j];
+        a[(size_t)i * n + j] = a[(size_t)i * n + j] - t;
+      }
+    }
+  }
+  *map_dev = arena.alloc_t<long long>(n);
+  CK(cudaMemcpy(*map_dev, map.data(), sizeof(long long) * n, cudaMemcpyHostToDevice));
+  *A_dev = arena.alloc((long long)n * n);
+  if (parity_build()) {
+    *piv_dev = arena.alloc_t<long long>(n);
+    CK(cudaMemcpy(*piv_dev, piv.data(), sizeof(long long) * n, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(*A_dev, a.data(), sizeof(double) * (size_t)n * n, cudaMemcpyHostToDevice));
+  } else {
+    // Performance build: explicit inverse from the same factors (columns = DenseLU::solve(e_c)),
+    // applied as one warp-per-row matvec instead of a 2n-step dependent substitution chain.
+    std::vector<double> inv((size_t)n * n), y((size_t)n), x((size_t)n);
+    for (int c = 0; c < n; ++c) {
+      std::fill(y.begin(), y.end(), 0.0);
+      y[(size_t)c] = 1.0;
+      for (int k = 0; k < n; ++k) {
+        const long long p = piv[(size_t)k];
+        if (p != k) std::swap(y[(size_t)k], y[(size_t)p]);
+        for (int j = 0; j < k; ++j) y[(size_t)k] -= a[(size_t)k * n + j] * y[(size_t)j];
+      }
+      for (int k = n - 1; k >= 0; --k) {
+        double acc = y[(size_t)k];
+        for (int j = k + 1; j < n; ++j) acc -= a[(size_t)k * n + j] * x[(size_t)j];
+        x[(size_t)k] = acc / a[(size_t)k * n + k];
+      }
+      for (int r = 0; r < n; ++r) inv[(size_t)r * n + c] = x[(size_t)r];
+    }
+    CK(cudaMemcpy(*A_dev, inv.data(), sizeof(double) * (size_t)n * n, cudaMemcpyHostToDevice));
+  }
+}
+
+
 void Solver::setup_coarse(Node& nd) {
   const Dist& D = *nd.dist;
   if (D.local.empty()) return;
@@ -637,62 +698,11 @@ void Solver::setup_coarse(Node& nd) {
         if (j + 1 < ny - 1) row[v + nx] = -fyp;
         if (k + 1 < nz - 1) row[v + nx * ny] = -fzp;
       }
-  std::vector<long long> piv((size_t)n);
-  for (int kk2 = 0; kk2 < n; ++kk2) {  // precond.cpp:26-46
-    int p = kk2;
-    double best = std::fabs(a[(size_t)kk2 * n + kk2]);
-    for (int i = kk2 + 1; i < n; ++i)
-      if (std::fabs(a[(size_t)i * n + kk2]) > best) {
-        best = std::fabs(a[(size_t)i * n + kk2]);
-        p = i;
-      }
-    if (best == 0.0) throw tmg::Error("lu factorization: matrix is singular at column " + std::to_string(kk2));
-    piv[(size_t)kk2] = p;
-    if (p != kk2)
-      for (int j = 0; j < n; ++j) std::swap(a[(size_t)kk2 * n + j], a[(size_t)p * n + j]);
-    const double pivot = a[(size_t)kk2 * n + kk2];
-    for (int i = kk2 + 1; i < n; ++i) {
-      const double m = a[(size_t)i * n + kk2] / pivot;
-      a[(size_t)i * n + kk2] = m;
-      if (m == 0.0) continue;
-      for (int j = kk2 + 1; j < n; ++j) {
-        volatile double t = m * a[(size_t)kk2 * n + j];
-        a[(size_t)i * n + j] = a[(size_t)i * n + j] - t;
-      }
-    }
-  }
   std::vector<long long> map((size_t)n);
   for (int k = 0; k < nz; ++k)
     for (int j = 0; j < ny; ++j)
       for (int i = 0; i < nx; ++i) map[(size_t)(i + nx * (j + ny * k))] = g.base + i + g.px * j + g.pxy * k;
-  nd.map_dev = arena.alloc_t<long long>(n);
-  CK(cudaMemcpy(nd.map_dev, map.data(), sizeof(long long) * n, cudaMemcpyHostToDevice));
-  nd.A_dev = arena.alloc((long long)n * n);
-  if (parity_build()) {
-    nd.piv_dev = arena.alloc_t<long long>(n);
-    CK(cudaMemcpy(nd.piv_dev, piv.data(), sizeof(long long) * n, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(nd.A_dev, a.data(), sizeof(double) * (size_t)n * n, cudaMemcpyHostToDevice));
-  } else {
-    // Performance build: explicit inverse from the same factors (columns = DenseLU::solve(e_c)),
-    // applied as one warp-per-row matvec instead of a 2n-step dependent substitution chain.
-    std::vector<double> inv((size_t)n * n), y((size_t)n), x((size_t)n);
-    for (int c = 0; c < n; ++c) {
-      std::fill(y.begin(), y.end(), 0.0);
-      y[(size_t)c] = 1.0;
-      for (int k = 0; k < n; ++k) {
-        const long long p = piv[(size_t)k];
-        if (p != k) std::swap(y[(size_t)k], y[(size_t)p]);
-        for (int j = 0; j < k; ++j) y[(size_t)k] -= a[(size_t)k * n + j] * y[(size_t)j];
-      }
-      for (int k = n - 1; k >= 0; --k) {
-        double acc = y[(size_t)k];
-        for (int j = k + 1; j < n; ++j) acc -= a[(size_t)k * n + j] * x[(size_t)j];
-        x[(size_t)k] = acc / a[(size_t)k * n + k];
-      }
-      for (int r = 0; r < n; ++r) inv[(size_t)r * n + c] = x[(size_t)r];
-    }
-    CK(cudaMemcpy(nd.A_dev, inv.data(), sizeof(double) * (size_t)n * n, cudaMemcpyHostToDevice));
-  }
+  dense_lu_setup(arena, a, n, map, &nd.A_dev, &nd.piv_dev, &nd.map_dev);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -890,7 +900,7 @@ std::array<double, 2> Solver::collect2(int i, int nslots, const Field* a, const 
   return s;
 }
 
-static double tridiag_eig_max(const std::vector<double>& d, const std::vector<double>& e) {
+double tridiag_eig_max(const std::vector<double>& d, const std::vector<double>& e) {
   // solver.cpp:488-516 (Sturm bisection)
   const size_t n = d.size();
   double lo = d[0], hi = d[0];

@@ -89,6 +89,10 @@ class DeviceArena {
 };
 
 Field make_field(DeviceArena& A, const Dist& D);
+double hashed_uniform_h(unsigned long long seed, unsigned long long idx);  // common.hpp:50-53
+double tridiag_eig_max(const std::vector<double>& d, const std::vector<double>& e);  // solver.cpp:488-516
+void dense_lu_setup(DeviceArena& arena, std::vector<double> a, int n, const std::vector<long long>& map,
+                    double** A_dev, long long** piv_dev, long long** map_dev);
 
 // Region copies between two distributions (halo: same dist, box halo incl. corners).
 struct RegionPlan {

@@ -1198,7 +1198,7 @@ __global__ void k_zero(double* p, long long n) {
 // ------------------------------------------------------------------------------------------
 
 // bc[I] = 0.125 * sum_{fine f near 2I, ascending natural order} w_f r_f   (R = 2^-3 P^T)
-__global__ void k_restrict(BoxGeo F, BoxGeo Cg, const double* __restrict__ rf, double* __restrict__ bc) {
+__global__ void k_restrict(BoxGeo F, BoxGeo Cg, const double* __restrict__ rf, double* __restrict__ bc, double scale) {
   const int I = blockIdx.x * blockDim.x + threadIdx.x, J = blockIdx.y * blockDim.y + threadIdx.y;
   const int K = blockIdx.z;
   if (I >= Cg.ex || J >= Cg.ey) return;
@@ -1225,7 +1225,7 @@ __global__ void k_restrict(BoxGeo F, BoxGeo Cg, const double* __restrict__ rf, d
       }
     }
   }
-  bc[vidx(Cg, I, J, K)] = 0.125 * acc;
+  bc[vidx(Cg, I, J, K)] = scale * acc;  // 2^-3 (FD scaling) or 1 (finite elements, R = P^T)
 }
 
 // xf += P xc : per axis coincident (w 1) or midpoint (w 1/2, 1/2); columns ascending.
@@ -1653,8 +1653,14 @@ int launch_prolong_to(const BoxGeo& fine, const BoxGeo& coarse, const double* xc
   return 1;
 }
 
+int launch_restrict_scaled(const BoxGeo& fine, const BoxGeo& coarse, const double* rf, double* bc, double scale,
+                           cudaStream_t s) {
+  k_restrict<<<plane_grid(coarse, 0), dim3(32, 4), 0, s>>>(fine, coarse, rf, bc, scale);
+  return 1;
+}
+
 int launch_restrict(const BoxGeo& fine, const BoxGeo& coarse, const double* rf, double* bc, cudaStream_t s) {
-  k_restrict<<<plane_grid(coarse, 0), dim3(32, 4), 0, s>>>(fine, coarse, rf, bc);
+  k_restrict<<<plane_grid(coarse, 0), dim3(32, 4), 0, s>>>(fine, coarse, rf, bc, 0.125);
   return 1;
 }
 

@@ -110,6 +110,9 @@ int launch_resid_restrict(const BoxGeo& fine, const OpParams& op, const BoxGeo& 
                           const double* x, double* bc, cudaStream_t s);
 // bc = 2^-3 P^T rf over the coarse box (rf needs a box halo incl. corners).
 int launch_restrict(const BoxGeo& fine, const BoxGeo& coarse, const double* rf, double* bc, cudaStream_t s);
+// bc = scale P^T rf (scale 1: finite-element restriction of the elasticity path)
+int launch_restrict_scaled(const BoxGeo& fine, const BoxGeo& coarse, const double* rf, double* bc, double scale,
+                           cudaStream_t s);
 // xf += P xc (xc needs a box halo incl. corners).
 int launch_prolong_add(const BoxGeo& fine, const BoxGeo& coarse, const double* xc, double* xf, cudaStream_t s);
 

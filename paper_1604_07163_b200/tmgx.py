@@ -89,6 +89,8 @@ EXPORTS = [
     "tmgx_options_create", "tmgx_options_destroy", "tmgx_options_parse", "tmgx_options_parse_file_text",
     "tmgx_options_set", "tmgx_options_get", "tmgx_options_serialize", "tmgx_options_unused",
     "tmgx_options_resolve", "tmgx_solver_from_options", "tmgx_telescope_timing",
+    "tmgx_elast_create", "tmgx_elast_destroy", "tmgx_elast_kref", "tmgx_elast_level_info", "tmgx_elast_rhs",
+    "tmgx_elast_level_apply", "tmgx_elast_level_smooth", "tmgx_elast_pc_apply", "tmgx_elast_solve",
 ]
 
 _libs = {}
@@ -153,6 +155,15 @@ def load(parity: bool = False):
         "tmgx_options_unused": [C.c_void_p, C.c_char_p, C.c_int],
         "tmgx_options_resolve": [C.c_void_p, C.c_char_p, C.c_char_p, P(_MG), P(_Ksp), C.c_char_p, C.c_int],
         "tmgx_telescope_timing": [C.c_void_p, C.c_int, C.c_int, D, D, I64],
+        "tmgx_elast_create": [C.c_void_p, I64, C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_double, P(C.c_void_p)],
+        "tmgx_elast_destroy": [C.c_void_p],
+        "tmgx_elast_kref": [C.c_double, D],
+        "tmgx_elast_level_info": [C.c_void_p, C.c_int, I64, D, D],
+        "tmgx_elast_rhs": [C.c_void_p, D],
+        "tmgx_elast_level_apply": [C.c_void_p, C.c_int, D, D],
+        "tmgx_elast_level_smooth": [C.c_void_p, C.c_int, D, D],
+        "tmgx_elast_pc_apply": [C.c_void_p, D, D],
+        "tmgx_elast_solve": [C.c_void_p, C.c_void_p, C.c_void_p, P(_Ksp), D, P(_Report)],
         "tmgx_solver_from_options": [C.c_void_p, P(_Problem), C.c_void_p, C.c_char_p, C.c_char_p, P(C.c_void_p),
                                      P(_Ksp)],
     }
@@ -723,3 +734,91 @@ def rank_block_to_natural(h: GridHeader, ranks=None):
                               indexing="ij")
         out.append((i + h.npoints[0] * (j + h.npoints[1] * k)).ravel())
     return np.concatenate(out) if out else np.zeros(0, dtype=np.int64)
+
+
+# ----------------------------------------------------------------- Q1 elasticity (configs[4])
+def elast_kref(nu=0.3, parity=False):
+    """24x24 reference stiffness of the unit-cube Q1 element (E = 1), host computed."""
+    L = load(parity)
+    K = np.zeros(576)
+    _check(L, L.tmgx_elast_kref(nu, _dp(K)))
+    return K.reshape(24, 24)
+
+
+class ElastSolver:
+    """Q1 hexahedral elasticity MG-CG on one GPU (tmgx_elast.cu): N^3 vertices x 3 dofs,
+    log-uniform E per element, clamped x = 0, body force (0, 0, -1), point-block Jacobi
+    Chebyshev V(m,m), rediscretised coarse levels, LU on level 0. Vectors in natural vertex
+    order with 3 interleaved dofs."""
+
+    def __init__(self, world: World, npoints, nlevels, smooth_its=2, est_mode=EST_LANCZOS, seed_e=11, nu=0.3):
+        self.world, self.L = world, world.L
+        self.nlevels = nlevels
+        npa = np.array(npoints, dtype=np.int64)
+        h = C.c_void_p()
+        _check(self.L, self.L.tmgx_elast_create(world.h, _i64(npa), nlevels, smooth_its, est_mode, seed_e, nu,
+                                                C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.L.tmgx_elast_destroy(self.h)
+            self.h = None
+
+    def level_shape(self, level):
+        n = np.zeros(3, dtype=np.int64)
+        lo, hi = C.c_double(), C.c_double()
+        _check(self.L, self.L.tmgx_elast_level_info(self.h, level, _i64(n), C.byref(lo), C.byref(hi)))
+        return tuple(int(v) for v in n)
+
+    def level_size(self, level):
+        s = self.level_shape(level)
+        return 3 * s[0] * s[1] * s[2]
+
+    def bounds(self, level):
+        n = np.zeros(3, dtype=np.int64)
+        lo, hi = C.c_double(), C.c_double()
+        _check(self.L, self.L.tmgx_elast_level_info(self.h, level, _i64(n), C.byref(lo), C.byref(hi)))
+        return lo.value, hi.value
+
+    def rhs(self):
+        b = np.zeros(self.level_size(self.nlevels - 1))
+        _check(self.L, self.L.tmgx_elast_rhs(self.h, _dp(b)))
+        return b
+
+    def level_apply(self, level, x):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.zeros_like(x)
+        _check(self.L, self.L.tmgx_elast_level_apply(self.h, level, _dp(x), _dp(y)))
+        return y
+
+    def level_smooth(self, level, b, x0=None):
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        x = np.zeros_like(b) if x0 is None else np.array(x0, dtype=np.float64)
+        _check(self.L, self.L.tmgx_elast_level_smooth(self.h, level, _dp(b), _dp(x)))
+        return x
+
+    def pc_apply(self, x):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.zeros_like(x)
+        _check(self.L, self.L.tmgx_elast_pc_apply(self.h, _dp(x), _dp(y)))
+        return y
+
+    def solve(self, b, x=None, cfg: KrylovConfig = KrylovConfig(rtol=1e-6)):
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        if x is None:
+            x = np.zeros_like(b)
+        k = SolverNode._ksp(None, cfg)
+        hist = np.zeros(cfg.max_its + 1)
+        rep = _Report()
+        _check(self.L, self.L.tmgx_elast_solve(self.h, b.ctypes.data, x.ctypes.data, C.byref(k), _dp(hist),
+                                               C.byref(rep)))
+        return x, SolverNode._report(None, rep, hist, cfg)
+
+    def solve_ptr(self, b_ptr, x_ptr, cfg: KrylovConfig = KrylovConfig(rtol=1e-6)):
+        k = SolverNode._ksp(None, cfg)
+        hist = np.zeros(cfg.max_its + 1)
+        rep = _Report()
+        _check(self.L, self.L.tmgx_elast_solve(self.h, C.c_void_p(b_ptr), C.c_void_p(x_ptr), C.byref(k), _dp(hist),
+                                               C.byref(rep)))
+        return SolverNode._report(None, rep, hist, cfg)

@@ -389,3 +389,49 @@ def test_zero_initial_guess_ignores_x():
     junk = np.full_like(b, np.nan)
     x1, r1 = s.solve(b, x=junk, cfg=T.KrylovConfig("cg", rtol=1e-8, initial_guess_nonzero=False))
     assert r1.iterations == r0.iterations and np.array_equal(x0, x1)
+
+
+# ---------------------------------------------------------------- Q1 elasticity (configs[4])
+def _elast(parity, n=17, nl=3, m=2):
+    w = T.World(1, parity=parity)
+    return w, T.ElastSolver(w, (n,) * 3, nl, smooth_its=m), O.ElastMG((n,) * 3, nl, smooth_its=m)
+
+
+@pytest.mark.parametrize("parity", [True, False])
+def test_elast_kernels(parity):
+    w, s, om = _elast(parity)
+    rng = np.random.default_rng(5)
+    for level in range(3):
+        x = rng.standard_normal(om.level_size(level))
+        check(s.level_apply(level, x), om.apply(level, x), parity)
+    for level in (1, 2):
+        lo, hi = s.bounds(level)
+        olo, ohi = om.bounds(level)
+        if parity:
+            assert (lo, hi) == (olo, ohi)
+        else:
+            assert abs(hi - ohi) / ohi < 1e-10
+    b = rng.standard_normal(om.level_size(2))
+    assert np.array_equal(s.rhs(), O.el_rhs((17,) * 3))
+    if parity:
+        check(s.level_smooth(2, b), om.smooth(2, b), True)
+        check(s.pc_apply(b), om.vcycle(2, b), True)
+    else:
+        assert rel(s.level_smooth(2, b), om.smooth(2, b)) < 1e-11
+        assert rel(s.pc_apply(b), om.vcycle(2, b)) < 1e-10
+
+
+@pytest.mark.parametrize("parity", [True, False])
+def test_elast_solve(parity):
+    w, s, om = _elast(parity, n=33, nl=4)
+    b = O.el_rhs((33,) * 3)
+    x, rep = s.solve(b, cfg=T.KrylovConfig("cg", rtol=1e-6))
+    xo, orep = om.solve(b, rtol=1e-6)
+    assert rep.converged()
+    if parity:
+        assert rep.iterations == orep["iterations"] and np.array_equal(x, xo)
+    else:
+        assert abs(rep.iterations - orep["iterations"]) <= 1
+        if rep.iterations != orep["iterations"]:
+            xo, orep = om.solve(b, rtol=0.0, max_its=rep.iterations)
+        assert rel(x, xo) < TOL_SOLUTION
