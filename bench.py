@@ -30,6 +30,8 @@ CONFIGS = {
     "cfg2": ((257, 257, 257), 7, 2, 0, 3, 1e-8),
     "cfg3": ((513, 513, 513), 8, 3, 1, 4, 1e-8),
     "cfg4w": ((257, 257, 257), 7, 2, 0, 4, 1e-8),
+    # Q1 elasticity, 3 dof/vertex (kind 2): one GPU, no telescope on this path yet
+    "cfg5": ((129, 129, 129), 6, 2, 2, None, 1e-6),
 }
 # Coarse operators: rediscretised (reference default) for constant k;
 # Galerkin 2^-3 P^T A P for the 1e4-contrast problem (with rediscretisation the reference
@@ -165,6 +167,69 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def run_elast(args, world, rank, np3, nlevels, m, rtol, dist):
+    """BASELINE configs[4]: Q1 elasticity MG-CG, one GPU (ElastSolver). value = DOF/s with b, x
+    resident in HBM; e2e through tmgx_elast_solve with pinned host b / x."""
+    import torch
+
+    from paper_1604_07163_b200 import tmgx as T
+
+    if world > 1:
+        if rank == 0:
+            print(json.dumps({"metric": "MG-CG DOF/s (time-to-solution)", "unavailable":
+                              "elasticity path runs on one GPU (no box split / telescope yet)"}))
+        return
+    w = T.World(1)
+    t0 = time.perf_counter()
+    s = T.ElastSolver(w, np3, nlevels, smooth_its=m)
+    t_setup = time.perf_counter() - t0
+    b_np = s.rhs()
+    n_dof = b_np.size
+    cfg = T.KrylovConfig("cg", rtol=rtol, initial_guess_nonzero=False)
+    b_dev = torch.from_numpy(b_np).cuda()
+    x_dev = torch.zeros_like(b_dev)
+    for _ in range(max(args.warmup, 0)):
+        rep = s.solve_ptr(b_dev.data_ptr(), x_dev.data_ptr(), cfg)
+    torch.cuda.synchronize()
+    dev_t, its = 0.0, 0
+    with ClockSampler(0) as clk:
+        for _ in range(args.steps):
+            rep = s.solve_ptr(b_dev.data_ptr(), x_dev.data_ptr(), cfg)
+            dev_t += rep.t_solve_s
+            its = rep.iterations
+        torch.cuda.synchronize()
+    b_host = torch.from_numpy(b_np).pin_memory()
+    x_host = torch.zeros(n_dof, dtype=torch.float64).pin_memory()
+    s.solve_ptr(b_host.data_ptr(), x_host.data_ptr(), cfg)
+    e2e_t = 0.0
+    for _ in range(args.steps):
+        t1 = time.perf_counter()
+        s.solve_ptr(b_host.data_ptr(), x_host.data_ptr(), cfg)
+        e2e_t += time.perf_counter() - t1
+    ms, by, fl = s.bench_apply(20)
+    peak, peak_kind = read_peaks()
+    line = {
+        "metric": "MG-CG DOF/s (time-to-solution)", "value": n_dof * args.steps / dev_t, "unit": "DOF/s",
+        "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_t / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded log-uniform element moduli, body force)",
+        "config": {"workload": f"cfg5: {np3[0]}^3 Q1 elasticity x3 dof {nlevels}-level MG V({m},{m}) "
+                               f"Cheb-point-block-Jacobi CG rtol {rtol:g}", "global_batch": 1,
+                   "seq_len": np3[0], "parallelism": "box1", "iterations": its, "t_setup_s": t_setup,
+                   "l2": "inputs larger than L2 (b, x 155 MB each)"},
+        "e2e": {"value": n_dof * args.steps / e2e_t, "unit": "DOF/s", "h2d_bytes_per_step": 8 * n_dof,
+                "d2h_bytes_per_step": 8 * n_dof},
+        "gpu_launches": rep.kernel_launches * args.steps,
+        "roofline": {"bound": "hbm", "achieved": by / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                     "frac": by / (ms * 1e-3) / 1e9 / peak, "traffic": None, "peak_kind": peak_kind,
+                     "kernel": "k_el_apply (Q1 elasticity operator, fine level)", "ms_per_launch": ms,
+                     "bytes_per_launch": by, "fp64_tflops": fl / (ms * 1e-3) / 1e12},
+        "cpu_baseline": None,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -202,6 +267,9 @@ def main():
 
     torch.cuda.set_device(local)
     np3, nlevels, m, kind, tele_level, rtol = CONFIGS[args.config]
+    if kind == 2:
+        run_elast(args, world, rank, np3, nlevels, m, rtol, dist)
+        return
     est = T.EST_LANCZOS if args.est == "lanczos" else T.EST_REFERENCE
 
     nccl_id = None

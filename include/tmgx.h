@@ -231,6 +231,10 @@ int tmgx_elast_level_smooth(tmgx_elast e, int level, const double *b, double *x)
 int tmgx_elast_pc_apply(tmgx_elast e, const double *x, double *y);                /* one V-cycle */
 int tmgx_elast_solve(tmgx_elast e, const double *b, double *x, const tmgx_ksp_cfg *cfg, double *history,
                      tmgx_report *rep);
+/* live timing of the finest-level operator apply (bench.py roofline): ms, algorithmic bytes
+ * (x, y: 24 B each, E: 8 B per vertex) and flops (576 FMAs per vertex) per launch */
+int tmgx_elast_bench_apply(tmgx_elast e, int iters, double *ms_per_launch, double *bytes_per_launch,
+                           double *flops_per_launch);
 
 /* Counters: kernel launches, halo/telescope bytes moved between processes. */
 typedef struct {

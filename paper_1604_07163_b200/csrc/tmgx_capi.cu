@@ -690,6 +690,32 @@ int tmgx_elast_solve(tmgx_elast e, const double* b, double* x, const tmgx_ksp_cf
   });
 }
 
+int tmgx_elast_bench_apply(tmgx_elast e, int iters, double* ms_per_launch, double* bytes_per_launch,
+                            double* flops_per_launch) {
+  return guard([&] {
+    auto& S = *e->s;
+    const int top = (int)S.L.size() - 1;
+    auto& L = S.L[top];
+    for (int w = 0; w < 3; ++w) S.apply(top, L.x, L.ad);
+    cudaEvent_t e0, e1;
+    tmgx::cuda_check(cudaEventCreate(&e0), "event");
+    tmgx::cuda_check(cudaEventCreate(&e1), "event");
+    tmgx::cuda_check(cudaEventRecord(e0, S.W.stream), "record");
+    for (int it = 0; it < iters; ++it) S.apply(top, L.x, L.ad);
+    tmgx::cuda_check(cudaEventRecord(e1, S.W.stream), "record");
+    tmgx::cuda_check(cudaEventSynchronize(e1), "sync");
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    const double nv = (double)L.g.ex * L.g.ey * L.g.ez;
+    *ms_per_launch = ms / iters;
+    *bytes_per_launch = nv * (24.0 + 24.0 + 8.0);     // x in, y out, one modulus per element
+    *flops_per_launch = nv * 576.0 * 2.0;               // 8 elements x 8 vertices x 3 x 3 FMAs
+    return 0;
+  });
+}
+
 int tmgx_plan_summary(int n_ranks, int nproc, int proc, const tmgx_problem* p, const tmgx_mg_cfg* m, int64_t* out,
                       int max_records, int* n_records) {
   return guard([&] {

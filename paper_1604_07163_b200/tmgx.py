@@ -91,6 +91,7 @@ EXPORTS = [
     "tmgx_options_resolve", "tmgx_solver_from_options", "tmgx_telescope_timing",
     "tmgx_elast_create", "tmgx_elast_destroy", "tmgx_elast_kref", "tmgx_elast_level_info", "tmgx_elast_rhs",
     "tmgx_elast_level_apply", "tmgx_elast_level_smooth", "tmgx_elast_pc_apply", "tmgx_elast_solve",
+    "tmgx_elast_bench_apply",
 ]
 
 _libs = {}
@@ -164,6 +165,7 @@ def load(parity: bool = False):
         "tmgx_elast_level_smooth": [C.c_void_p, C.c_int, D, D],
         "tmgx_elast_pc_apply": [C.c_void_p, D, D],
         "tmgx_elast_solve": [C.c_void_p, C.c_void_p, C.c_void_p, P(_Ksp), D, P(_Report)],
+        "tmgx_elast_bench_apply": [C.c_void_p, C.c_int, D, D, D],
         "tmgx_solver_from_options": [C.c_void_p, P(_Problem), C.c_void_p, C.c_char_p, C.c_char_p, P(C.c_void_p),
                                      P(_Ksp)],
     }
@@ -814,6 +816,11 @@ class ElastSolver:
         _check(self.L, self.L.tmgx_elast_solve(self.h, b.ctypes.data, x.ctypes.data, C.byref(k), _dp(hist),
                                                C.byref(rep)))
         return x, SolverNode._report(None, rep, hist, cfg)
+
+    def bench_apply(self, iters=20):
+        ms, by, fl = C.c_double(), C.c_double(), C.c_double()
+        _check(self.L, self.L.tmgx_elast_bench_apply(self.h, iters, C.byref(ms), C.byref(by), C.byref(fl)))
+        return ms.value, by.value, fl.value
 
     def solve_ptr(self, b_ptr, x_ptr, cfg: KrylovConfig = KrylovConfig(rtol=1e-6)):
         k = SolverNode._ksp(None, cfg)
