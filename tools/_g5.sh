@@ -1,2 +1,1 @@
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -5 > gpurun_out/g5_pytest.log
-timeout 900 python bench.py --config cfg5 --steps 3 --warmup 1 > gpurun_out/g5_cfg5.log 2>&1
+for v in mb4 pf2mb5; do TMGX_LIB=libtmgx_$v.so timeout 300 python tools/tb_ab.py cfg2 >> gpurun_out/g5_ab.log 2>&1; done
