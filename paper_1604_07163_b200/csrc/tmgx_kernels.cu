@@ -735,8 +735,10 @@ __global__ void __launch_bounds__(kTBNT, NR >= 4 ? 2 : (NR == 2 ? TMGX_TB_MINB2 
     if (++sl == NS) sl = 0, ph ^= 1u;
     if (++isl == NS) isl = 0;
   }
-  if (DOTS) {
-    __shared__ double sh[32];
+  if (DOTS) {  // block reduction through the (now idle) d buffer: no extra shared memory, so the
+               // dots variant keeps the plain kernel's 4 blocks per SM
+    __syncthreads();
+    double* sh = &S.d[0][0][0];
     const double s0 = block_sum(dot_bz, sh);
     const double s1 = block_sum(dot_zz, sh);
     if (tid == 0) {
