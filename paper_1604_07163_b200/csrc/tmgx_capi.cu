@@ -775,6 +775,9 @@ extern "C" int tmgx_bench_kernel(tmgx_solver s, int which, int level, int iters,
     long long n = D.local_unknowns();
     double per_pt = 0.0;
     tmgx::ChebStep cs{0.5, 0.25};
+    if ((which == 8 || which == 9 || which == 11) &&
+        (D.h.n_ranks() != 1 || D.local.size() != 1 || !tmgx::cheb2_tb_supported(D.geo[0])))
+      throw tmg::ConfigError("bench_kernel: blocked / fused single-box kernels need a single-box level >= 33 wide");
     auto launch = [&]() {
       for (size_t q = 0; q < D.local.size(); ++q) {
         const auto& g = D.geo[q];

@@ -253,6 +253,10 @@ __global__ void k_fill_rhs(BoxGeo g, double* __restrict__ b, unsigned long long 
 // and optionally two dot-product partials (block-reduced at the end).
 // ------------------------------------------------------------------------------------------
 
+#ifndef TMGX_PSPMV_MINB
+#define TMGX_PSPMV_MINB 1
+#endif
+
 // Stencil input loaders: one array, or u = z + beta p (the CG direction update fused into the
 // operator apply; same expression as k_p_update, evaluated identically at every neighbour; the
 // new p goes to a different buffer, so neighbours always read the old one).
@@ -272,8 +276,20 @@ struct UPDir {
   __device__ double one(long long o) const { return __ldg(z + o) + beta * __ldg(p + o); }
 };
 
+// resident blocks per SM requested from ptxas (register cap) per functor: the fused CG update
+// needs 96 registers unconstrained (5 blocks/SM, latency bound); capped at 64 it runs 8
+template <class F>
+struct MarchMinBlocks {
+  static constexpr int v = 1;
+};
+struct FSpmvDotP;
+template <>
+struct MarchMinBlocks<FSpmvDotP> {
+  static constexpr int v = TMGX_PSPMV_MINB;
+};
+
 template <bool VAR, class F, class U = ULoad>
-__global__ void __launch_bounds__(kBX* kBY)
+__global__ void __launch_bounds__(kBX* kBY, MarchMinBlocks<F>::v)
     k_march(BoxGeo g, OpParams op, U u, F f, const double* __restrict__ scal, int beta_slot) {
   if constexpr (!std::is_same<U, ULoad>::value) u.beta = scal[beta_slot];
   __shared__ double sh[32];
