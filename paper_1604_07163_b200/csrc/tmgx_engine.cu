@@ -364,6 +364,7 @@ Solver::Solver(World& W_, const ProblemDesc& P, const MGDesc& M) : W(W_), prob(P
   if (const char* e = std::getenv("TMGX_GRAPHS")) use_graphs = std::string(e) != "0";
   if (const char* e = std::getenv("TMGX_TB")) tb_enabled = std::string(e) != "0";
   if (const char* e = std::getenv("TMGX_FUSE_CG")) fuse_cg = std::string(e) != "0";
+  if (const char* e = std::getenv("TMGX_TB_MIN")) tb_min_extent = std::atoi(e);
   if (const char* e = std::getenv("TMGX_FUSE_DOTS")) fuse_dots = std::string(e) != "0";
   if (const char* e = std::getenv("TMGX_FUSE_RR")) fuse_rr = std::string(e) != "0";
   if (mgd.nlevels < 1) throw tmg::ConfigError("mg: number of levels must be >= 1");
@@ -859,7 +860,7 @@ ChebStep Solver::cheb_first_step(const Node& nd) const {
 bool Solver::use_tb(int i) const {
   const Node& nd = nodes[i];
   return tb_enabled && mgd.m == 2 && nd.kind == SMOOTH && nd.dist->h.n_ranks() == 1 && !nd.dist->local.empty() &&
-         nd.op[0].S == nullptr && cheb2_tb_supported(nd.dist->geo[0]);
+         nd.op[0].S == nullptr && cheb2_tb_supported(nd.dist->geo[0]) && nd.dist->geo[0].ex >= tb_min_extent;
 }
 
 void Solver::device_allreduce_ranksums(int nslots) {

@@ -240,6 +240,7 @@ class Solver {
   // CG iteration as one CUDA graph (TMGX_GRAPHS=0 disables capture)
   bool use_graphs = true;
   bool tb_enabled = true;  // temporally blocked V(2,2) smoother (TMGX_TB=0 disables)
+  int tb_min_extent = 0;    // blocked smoother only on levels at least this wide (TMGX_TB_MIN)
   bool fuse_dots = true;   // CG r.z, z.z from the finest blocked post-smooth (TMGX_FUSE_DOTS=0)
   int dots_nblk = 0;       // partials written by the last finest post-smooth (0: none)
   bool fuse_cg = true;     // p update fused into w = A p on single-box fine levels (TMGX_FUSE_CG=0)
