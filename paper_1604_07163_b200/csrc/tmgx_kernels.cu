@@ -253,6 +253,9 @@ __global__ void k_fill_rhs(BoxGeo g, double* __restrict__ b, unsigned long long 
 // and optionally two dot-product partials (block-reduced at the end).
 // ------------------------------------------------------------------------------------------
 
+#ifndef TMGX_TB_WAIT_ALL
+#define TMGX_TB_WAIT_ALL 1
+#endif
 #ifndef TMGX_PSPMV_MINB
 #define TMGX_PSPMV_MINB 1
 #endif
@@ -662,8 +665,12 @@ __global__ void __launch_bounds__(kTBNT, NR >= 4 ? 2 : (NR == 2 ? TMGX_TB_MINB2 
   double dot_bz = 0.0, dot_zz = 0.0;
   for (int t = T0; t <= T1; ++t, outp += g.pxy) {
     const int p1 = t - LAG1, p2 = p1 - 1;  // pass-1 and pass-2 planes
+#if TMGX_TB_WAIT_ALL
     mbar_wait(sbar + 8 * sl, ph);
-    __syncthreads();  // slot of group t+kTBPF-NS and the d buffer of step t-2 are free
+#else
+    if (ty == 0) mbar_wait(sbar + 8 * sl, ph);  // one warp polls; the others sleep in bar.sync
+#endif
+    __syncthreads();  // group t visible to all; slot of group t+kTBPF-NS and the d buffer of step t-2 free
     if (tid == 0) {
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
       issue(t + kTBPF, isl);
