@@ -435,3 +435,11 @@ def test_elast_solve(parity):
         if rep.iterations != orep["iterations"]:
             xo, orep = om.solve(b, rtol=0.0, max_its=rep.iterations)
         assert rel(x, xo) < TOL_SOLUTION
+
+
+def test_telescope_timing_table_schema():
+    """Table-1 timing: T_setup from the plan build, T_apply = gather +
+    scatter of the telescoped level on the device; both positive, bytes = 2 x 8 x level size."""
+    w, s = make((33, 33, 33), 3, n_ranks=8, telescope=[T.TelescopeStage(2, 8)])
+    t_setup, t_apply, by = s.telescope_timing(0, reps=5)
+    assert t_setup > 0 and t_apply > 0 and by == 2 * 8 * 33 ** 3
