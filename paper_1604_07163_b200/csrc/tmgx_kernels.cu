@@ -605,7 +605,10 @@ template <bool VAR, bool PRE, int NR, bool DOTS = false>
 #ifndef TMGX_TB_MINB2
 #define TMGX_TB_MINB2 4
 #endif
-__global__ void __launch_bounds__(kTBNT, NR >= 4 ? 2 : (NR == 2 ? TMGX_TB_MINB2 : 4))
+#ifndef TMGX_TB_MINB_PRE
+#define TMGX_TB_MINB_PRE 2
+#endif
+__global__ void __launch_bounds__(kTBNT, NR >= 4 ? 2 : (NR == 2 ? (PRE ? TMGX_TB_MINB_PRE : TMGX_TB_MINB2) : 4))
     k_cheb2_tb(const __grid_constant__ TBMaps maps, BoxGeo g, OpParams op, double* __restrict__ xout, double s_theta,
                double c1, double c2, double* __restrict__ dpart, long long dstride) {
   // DOTS (finest post-smooth of the CG preconditioner): block partials of b.x' and x'.x', i.e.
