@@ -443,3 +443,17 @@ def test_telescope_timing_table_schema():
     w, s = make((33, 33, 33), 3, n_ranks=8, telescope=[T.TelescopeStage(2, 8)])
     t_setup, t_apply, by = s.telescope_timing(0, reps=5)
     assert t_setup > 0 and t_apply > 0 and by == 2 * 8 * 33 ** 3
+
+
+@pytest.mark.parametrize("parity", [True, False])
+def test_fused_residual_restrict_optin(parity, monkeypatch):
+    """The opt-in fused residual + restriction kernel (TMGX_FUSE_RR=1, measured slower and off
+    by default) keeps the restriction's arithmetic: bitwise in the parity build."""
+    monkeypatch.setenv("TMGX_FUSE_RR", "1")
+    np3, nl = (33, 65, 33), 3
+    om = oracle_mg(np3, nl, O.VARCOEF7)
+    w, s = make(np3, nl, T.VARCOEF7_HARMONIC, parity=parity, bounds=oracle_bounds(om, nl))
+    rng = np.random.default_rng(9)
+    n = om.level_size(nl - 1)
+    b, x = rng.standard_normal(n), rng.standard_normal(n)
+    check(s.residual_restrict(nl - 1, b, x), om.restrict(nl - 1, b - om.apply(nl - 1, x)), parity)
