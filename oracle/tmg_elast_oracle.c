@@ -17,7 +17,8 @@
  *     R = P^T per component (finite-element scaling: no 2^-3);
  *   - LU on the coarsest level (5^3 x 3 = 375 unknowns at the BASELINE config).
  * Row arithmetic order (shared with the GPU kernels): incident elements ez, ey, ex in {-1, 0}
- * ascending, element vertices l' = 0..7 (x fastest), components beta then alpha.
+ * ascending; per element the K_ref row block times the element's x (vertices l' = 0..7,
+ * x fastest, components beta then alpha) is accumulated first and then added scaled by E_e h.
  */
 #include <math.h>
 #include <stdlib.h>
@@ -114,24 +115,21 @@ static void el_apply(const orc_el_mg *mg, const el_level *L, const double *x, do
               if (ei < 0 || ej < 0 || ek < 0 || ei >= nx - 1 || ej >= ny - 1 || ek >= nz - 1) continue;
               const double eh = L->E[ei + (nx - 1) * (ej + (ny - 1) * ek)] * L->h;
               const int l = (int)(-ex) + 2 * (int)(-ey) + 4 * (int)(-ez);
+              /* element contribution K_ref row block times the element's x, then scaled by E h */
+              double ea[3] = {0.0, 0.0, 0.0};
               for (int lp = 0; lp < 8; ++lp) {
                 const int64_t vi = ei + (lp & 1), vj = ej + ((lp >> 1) & 1), vk = ek + (lp >> 2);
                 const int64_t w = vi + nx * (vj + ny * vk);
                 if (cl) {
                   if (lp != l) continue;
-                  for (int a = 0; a < 3; ++a) {
-                    const double c = eh * mg->K[(3 * l + a) * 24 + 3 * l + a];
-                    acc[a] += c * x[3 * w + a];
-                  }
+                  for (int a = 0; a < 3; ++a) ea[a] += mg->K[(3 * l + a) * 24 + 3 * l + a] * x[3 * w + a];
                   continue;
                 }
                 if (clamped(L, vi)) continue;
                 for (int b = 0; b < 3; ++b)
-                  for (int a = 0; a < 3; ++a) {
-                    const double c = eh * mg->K[(3 * l + a) * 24 + 3 * lp + b];
-                    acc[a] += c * x[3 * w + b];
-                  }
+                  for (int a = 0; a < 3; ++a) ea[a] += mg->K[(3 * l + a) * 24 + 3 * lp + b] * x[3 * w + b];
               }
+              for (int a = 0; a < 3; ++a) acc[a] += eh * ea[a];
             }
         y[3 * v + 0] = acc[0];
         y[3 * v + 1] = acc[1];

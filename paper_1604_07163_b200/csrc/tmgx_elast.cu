@@ -15,7 +15,8 @@
 // a 3-dof vector is three consecutive component planes of that layout (component c at
 // p + c * total), elements (ei, ej, ek) live at the vertex slot of their lower corner. The
 // operator is matrix-free and vertex-centric: a thread gathers its row from the 8 incident
-// elements (576 fused multiply-adds with K_ref in constant memory); everything else reuses the
+// elements (576 fused multiply-adds with K_ref in constant memory, one E h scaling per
+// element); everything else reuses the
 // scalar path's per-component kernels (restriction, prolongation, LU) or is pointwise.
 #include <cuda_runtime.h>
 
@@ -63,27 +64,32 @@ __global__ void __launch_bounds__(128) k_el_apply(BoxGeo g, const double* __rest
         if (ei < 0 || ej < 0 || ek < 0 || ei >= nx - 1 || ej >= ny - 1 || ek >= nz - 1) continue;
         const double eh = __ldg(E + vx(g, ei, ej, ek)) * h;
         const int l = -ex + 2 * (-ey) + 4 * (-ez);
+        // element contribution: K_ref row block times the element's x, then scaled by E h
+        double ea0 = 0.0, ea1 = 0.0, ea2 = 0.0;
         if (cl) {
           const long long w = vx(g, i, j, k);
-          acc0 += (eh * c_K[(3 * l + 0) * 24 + 3 * l + 0]) * __ldg(x + w);
-          acc1 += (eh * c_K[(3 * l + 1) * 24 + 3 * l + 1]) * __ldg(x + T + w);
-          acc2 += (eh * c_K[(3 * l + 2) * 24 + 3 * l + 2]) * __ldg(x + 2 * T + w);
-          continue;
-        }
+          ea0 += c_K[(3 * l + 0) * 24 + 3 * l + 0] * __ldg(x + w);
+          ea1 += c_K[(3 * l + 1) * 24 + 3 * l + 1] * __ldg(x + T + w);
+          ea2 += c_K[(3 * l + 2) * 24 + 3 * l + 2] * __ldg(x + 2 * T + w);
+        } else {
 #pragma unroll
-        for (int lp = 0; lp < 8; ++lp) {
-          const int vi = ei + (lp & 1), vj = ej + ((lp >> 1) & 1), vk = ek + (lp >> 2);
-          if (g.gx + vi == 0) continue;  // coupling to a clamped dof dropped
-          const long long w = vx(g, vi, vj, vk);
-          const double x0 = __ldg(x + w), x1 = __ldg(x + T + w), x2 = __ldg(x + 2 * T + w);
-          const double xb[3] = {x0, x1, x2};
+          for (int lp = 0; lp < 8; ++lp) {
+            const int vi = ei + (lp & 1), vj = ej + ((lp >> 1) & 1), vk = ek + (lp >> 2);
+            if (g.gx + vi == 0) continue;  // coupling to a clamped dof dropped
+            const long long w = vx(g, vi, vj, vk);
+            const double x0 = __ldg(x + w), x1 = __ldg(x + T + w), x2 = __ldg(x + 2 * T + w);
+            const double xb[3] = {x0, x1, x2};
 #pragma unroll
-          for (int bb = 0; bb < 3; ++bb) {
-            acc0 += (eh * c_K[(3 * l + 0) * 24 + 3 * lp + bb]) * xb[bb];
-            acc1 += (eh * c_K[(3 * l + 1) * 24 + 3 * lp + bb]) * xb[bb];
-            acc2 += (eh * c_K[(3 * l + 2) * 24 + 3 * lp + bb]) * xb[bb];
+            for (int bb = 0; bb < 3; ++bb) {
+              ea0 += c_K[(3 * l + 0) * 24 + 3 * lp + bb] * xb[bb];
+              ea1 += c_K[(3 * l + 1) * 24 + 3 * lp + bb] * xb[bb];
+              ea2 += c_K[(3 * l + 2) * 24 + 3 * lp + bb] * xb[bb];
+            }
           }
         }
+        acc0 += eh * ea0;
+        acc1 += eh * ea1;
+        acc2 += eh * ea2;
       }
   const long long v = vx(g, i, j, k);
   if (MODE == 0) {
