@@ -78,7 +78,11 @@ static BoxGeo make_geo(const tmg::GridHeader& h, int m) {
   g.Nx = (int)h.npoints[0];
   g.Ny = (int)h.npoints[1];
   g.Nz = (int)h.npoints[2];
-  g.zc = choose_zc(g.ex, g.ey, g.ez);
+  static const long long min_blocks = [] {  // TMGX_MIN_BLOCKS: tuning experiments
+    const char* e = std::getenv("TMGX_MIN_BLOCKS");
+    return e ? std::atoll(e) : (long long)kMinBlocks;
+  }();
+  g.zc = choose_zc(g.ex, g.ey, g.ez, min_blocks);
   g.px =((kXO + g.ex + 1) + 3) / 4 * 4;
   g.pxy = g.px * (g.ey + 2);
   g.base = kXO + g.px + g.pxy;

@@ -30,10 +30,10 @@ struct BoxGeo {
 // z-chunk so that a level launches >= kMinBlocks blocks: large boxes stream 16 planes per
 // block (register queue reuse), coarse boxes trade reuse for parallelism (latency-bound).
 constexpr int kMinBlocks = 8 * 148;
-inline int choose_zc(int ex, int ey, int ez) {
+inline int choose_zc(int ex, int ey, int ez, long long min_blocks = kMinBlocks) {
   const int bxy = ((ex + 2 * kBX - 1) / (2 * kBX)) * ((ey + kBY - 1) / kBY);  // pair tiles
   for (int zc = kZC; zc > 1; zc >>= 1)
-    if ((long long)bxy * ((ez + zc - 1) / zc) >= kMinBlocks) return zc;
+    if ((long long)bxy * ((ez + zc - 1) / zc) >= min_blocks) return zc;
   return 1;
 }
 
