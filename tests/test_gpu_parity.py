@@ -457,3 +457,25 @@ def test_fused_residual_restrict_optin(parity, monkeypatch):
     n = om.level_size(nl - 1)
     b, x = rng.standard_normal(n), rng.standard_normal(n)
     check(s.residual_restrict(nl - 1, b, x), om.restrict(nl - 1, b - om.apply(nl - 1, x)), parity)
+
+
+@pytest.mark.parametrize("cfg", ["cfg2", "cfg5"])
+def test_full_size_linearity_exact(cfg):
+    """BASELINE sizes, size-independent property: scaling the right-hand side by 2 scales every
+    intermediate of MG-CG exactly (powers of two commute with rounding), so the solve of 2b takes
+    the same iterations and returns exactly 2x (257^3 Poisson; 129^3 x 3 elasticity)."""
+    import bench as B
+
+    np3, nl, m, kind, _, rtol = B.CONFIGS[cfg]
+    cfgk = T.KrylovConfig("cg", rtol=rtol, initial_guess_nonzero=False)
+    w = T.World(1)
+    if kind == 2:
+        s = T.ElastSolver(w, np3, nl, smooth_its=m)
+        b = s.rhs()
+    else:
+        s = T.SolverNode(w, T.Problem(np3, kind), T.MGConfig(nl, m, T.EST_LANCZOS))
+        b = s.rhs(B.SEED_F)
+    x1, r1 = s.solve(b, cfg=cfgk)
+    x2, r2 = s.solve(2.0 * b, cfg=cfgk)
+    assert r1.converged() and r1.iterations == r2.iterations
+    assert np.array_equal(x2, 2.0 * x1)
