@@ -479,3 +479,25 @@ def test_full_size_linearity_exact(cfg):
     x2, r2 = s.solve(2.0 * b, cfg=cfgk)
     assert r1.converged() and r1.iterations == r2.iterations
     assert np.array_equal(x2, 2.0 * x1)
+
+
+def test_vcycle_partition_independent_large():
+    """129^3 (cfg5's grid, 6 levels): the 8-box, doubly telescoped V-cycle equals the 1-box one bit
+    for bit (parity build, shared Chebyshev bounds) — the decomposition-invariance property at a
+    size the CPU oracle cannot reach quickly."""
+    np3, nl = (129, 129, 129), 6
+    w1, s1 = make(np3, nl, parity=True)
+    bounds = np.zeros(2 * nl)
+    for l in range(1, nl):
+        bounds[2 * l], bounds[2 * l + 1] = s1.bounds(l)
+    w1, s1 = make(np3, nl, parity=True, bounds=bounds)
+    b_nat = O.rhs(np3, 42)
+    y1 = s1.pc_apply(b_nat)
+    w8, s8 = make(np3, nl, parity=True, n_ranks=8, bounds=bounds,
+                  telescope=[T.TelescopeStage(3, 4), T.TelescopeStage(1, 2)])
+    h, _ = s8.level_info(nl - 1)
+    perm = T.rank_block_to_natural(h)
+    y8 = s8.pc_apply(b_nat[perm])
+    y8n = np.empty_like(y8)
+    y8n[perm] = y8
+    assert np.array_equal(y8n, y1)
