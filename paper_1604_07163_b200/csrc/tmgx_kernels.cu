@@ -38,15 +38,6 @@ namespace tmgx {
 
 namespace {
 
-
-// Programmatic dependent launch (TMGX_PDL=1): every kernel first waits for its predecessor
-// grid (a no-op when launched without the attribute) and then lets its own dependents begin
-// launching, so the next kernel's launch and prologue overlap this kernel's tail.
-__device__ __forceinline__ void pdl_enter() {
-  asm volatile("griddepcontrol.wait;\n" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
-}
-
 __device__ __forceinline__ long long vidx(const BoxGeo& g, int i, int j, int k) {
   return g.base + i + g.px * j + g.pxy * k;
 }
@@ -211,7 +202,6 @@ __device__ double sphere_k(const BoxGeo& g, const Sphere* __restrict__ sph, int 
 
 __global__ void k_fill_coeff(BoxGeo g, double* __restrict__ kf, const Sphere* __restrict__ sph, int ns,
                              double k_in, int varcoef) {
-  pdl_enter();
   const int i = blockIdx.x * blockDim.x + threadIdx.x - 1;
   const int j = blockIdx.y * blockDim.y + threadIdx.y - 1;
   const int k = blockIdx.z - 1;
@@ -224,7 +214,6 @@ __global__ void k_fill_coeff(BoxGeo g, double* __restrict__ kf, const Sphere* __
 // FX/FY/FZ on [-1, e-1]^3 (the +face of every vertex whose row or whose +neighbour's row is
 // owned) and D on the owned box; every k read stays inside the filled ring.
 __global__ void k_fill_faces(BoxGeo g, OpParams op, double* __restrict__ fc, long long st) {
-  pdl_enter();
   const int i = blockIdx.x * blockDim.x + threadIdx.x - 1;
   const int j = blockIdx.y * blockDim.y + threadIdx.y - 1;
   const int k = blockIdx.z - 1;
@@ -244,7 +233,6 @@ __global__ void k_fill_faces(BoxGeo g, OpParams op, double* __restrict__ fc, lon
 }
 
 __global__ void k_fill_rhs(BoxGeo g, double* __restrict__ b, unsigned long long seed, int bzero) {
-  pdl_enter();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = blockIdx.y * blockDim.y + threadIdx.y;
   const int k = blockIdx.z;
@@ -306,7 +294,6 @@ struct MarchMinBlocks<FSpmvDotP> {
 template <bool VAR, class F, class U = ULoad>
 __global__ void __launch_bounds__(kBX* kBY, MarchMinBlocks<F>::v)
     k_march(BoxGeo g, OpParams op, U u, F f, const double* __restrict__ scal, int beta_slot) {
-  pdl_enter();
   if constexpr (!std::is_same<U, ULoad>::value) u.beta = scal[beta_slot];
   __shared__ double sh[32];
   const int i0 = 2 * (blockIdx.x * kBX + threadIdx.x), j = blockIdx.y * kBY + threadIdx.y;
@@ -394,7 +381,6 @@ __device__ __forceinline__ double row27(const BoxGeo& g, const double* __restric
 
 template <class F>
 __global__ void __launch_bounds__(kBX* kBY) k_march27(BoxGeo g, OpParams op, const double* __restrict__ u, F f) {
-  pdl_enter();
   __shared__ double sh[32];
   double acc0 = 0.0, acc1 = 0.0;
   const int i0 = 2 * (blockIdx.x * kBX + threadIdx.x), j = blockIdx.y * kBY + threadIdx.y;
@@ -431,7 +417,6 @@ template <bool FINE27, bool VAR>
 __global__ void __launch_bounds__(128) k_galerkin(BoxGeo F, OpParams fop, BoxGeo Cg, double* __restrict__ Sc,
                                                    long long cst, const Sphere* __restrict__ sph, int ns,
                                                    double k_in) {
-  pdl_enter();
   // k at a fine vertex given by local indices: stored ring, or (two cells out, for rows of
   // ghost-ring vertices) evaluated from the coefficient function itself
   auto Kat = [&](int li, int lj, int lk) -> double {
@@ -626,7 +611,6 @@ template <bool VAR, bool PRE, int NR, bool DOTS = false>
 __global__ void __launch_bounds__(kTBNT, NR >= 4 ? 2 : (NR == 2 ? (PRE ? TMGX_TB_MINB_PRE : TMGX_TB_MINB2) : 4))
     k_cheb2_tb(const __grid_constant__ TBMaps maps, BoxGeo g, OpParams op, double* __restrict__ xout, double s_theta,
                double c1, double c2, double* __restrict__ dpart, long long dstride) {
-  pdl_enter();
   // DOTS (finest post-smooth of the CG preconditioner): block partials of b.x' and x'.x', i.e.
   // the CG's r.z and z.z (solver.cpp:245-250) from the values already on chip.
   using G = TBG<NR>;
@@ -803,7 +787,6 @@ template <bool VAR>
 __global__ void __launch_bounds__(kBX * 8)
     k_resid_restrict(BoxGeo F, OpParams op, BoxGeo Cg, const double* __restrict__ b, const double* __restrict__ x,
                      double* __restrict__ bc) {
-  pdl_enter();
   __shared__ double rs[3][16][32];
   const int tx = threadIdx.x, ty = threadIdx.y, tid = tx + 32 * ty;
   const int I0 = blockIdx.x * kRRCX, J0 = blockIdx.y * kRRCY;
@@ -912,7 +895,6 @@ __global__ void __launch_bounds__(kBX * 8)
 // weights are exact powers of two, so the sum equals k_prolong_add's (grid.cpp:421) bit for bit.
 __global__ void __launch_bounds__(kBX* kBY)
     k_prolong_pair(BoxGeo F, BoxGeo Cg, const double* __restrict__ xc, const double* xf, double* xo) {
-  pdl_enter();
   const int i0 = 2 * (blockIdx.x * kBX + threadIdx.x), j = blockIdx.y * kBY + threadIdx.y;
   if (i0 >= F.ex || j >= F.ey) return;
   const bool two = i0 + 1 < F.ex;
@@ -1135,7 +1117,6 @@ __device__ __forceinline__ double invd_at(const BoxGeo& g, const OpParams& op, i
 template <bool VAR>
 __global__ void __launch_bounds__(kBX* kBY) k_cheb_start_zero(BoxGeo g, OpParams op, const double* __restrict__ b,
                                                                double* __restrict__ out, double s_theta) {
-  pdl_enter();
   TMGX_PAIR_LOOP_BEGIN
   const double2 bb = ld2(b + v);
   double2 o;
@@ -1150,7 +1131,6 @@ template <bool VAR>
 __global__ void __launch_bounds__(kBX* kBY)
     k_jacobi_dot(BoxGeo g, OpParams op, const double* __restrict__ r, double* __restrict__ z,
                  double* __restrict__ part) {
-  pdl_enter();
   __shared__ double sh[32];
   double acc = 0.0;
   TMGX_PAIR_LOOP_BEGIN
@@ -1172,7 +1152,6 @@ __global__ void __launch_bounds__(kBX* kBY)
 __global__ void __launch_bounds__(kBX* kBY)
     k_dot2(BoxGeo g, const double* __restrict__ a, const double* __restrict__ b, const double* __restrict__ c,
            double* __restrict__ pab, double* __restrict__ pcc) {
-  pdl_enter();
   __shared__ double sh[32];
   double s1 = 0.0, s2 = 0.0;
   TMGX_PAIR_LOOP_BEGIN
@@ -1196,7 +1175,6 @@ __global__ void __launch_bounds__(kBX* kBY)
 __global__ void __launch_bounds__(kBX* kBY)
     k_cg_update(BoxGeo g, const double* __restrict__ p, const double* __restrict__ w, double* __restrict__ x,
                 double* __restrict__ r, const double* __restrict__ scal, int as, int fs) {
-  pdl_enter();
   if (scal[fs] != 0.0) return;
   const double alpha = scal[as];
   TMGX_PAIR_LOOP_BEGIN
@@ -1215,7 +1193,6 @@ __global__ void __launch_bounds__(kBX* kBY)
 __global__ void __launch_bounds__(kBX* kBY)
     k_p_update(BoxGeo g, const double* __restrict__ z, double* __restrict__ p, const double* __restrict__ scal,
                int bs) {
-  pdl_enter();
   const double beta = scal[bs];
   TMGX_PAIR_LOOP_BEGIN
   const double2 zv = ld2(z + v);
@@ -1228,7 +1205,6 @@ __global__ void __launch_bounds__(kBX* kBY)
 
 __global__ void __launch_bounds__(kBX* kBY)
     k_axpy(BoxGeo g, double alpha, const double* __restrict__ x, double* __restrict__ y, int copy) {
-  pdl_enter();
   TMGX_PAIR_LOOP_BEGIN
   const double2 xv = ld2(x + v);
   double2 yv;
@@ -1244,7 +1220,6 @@ __global__ void __launch_bounds__(kBX* kBY)
 }
 
 __global__ void k_zero(double* p, long long n) {
-  pdl_enter();
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
     p[e] = 0.0;
 }
@@ -1255,7 +1230,6 @@ __global__ void k_zero(double* p, long long n) {
 
 // bc[I] = 0.125 * sum_{fine f near 2I, ascending natural order} w_f r_f   (R = 2^-3 P^T)
 __global__ void k_restrict(BoxGeo F, BoxGeo Cg, const double* __restrict__ rf, double* __restrict__ bc, double scale) {
-  pdl_enter();
   const int I = blockIdx.x * blockDim.x + threadIdx.x, J = blockIdx.y * blockDim.y + threadIdx.y;
   const int K = blockIdx.z;
   if (I >= Cg.ex || J >= Cg.ey) return;
@@ -1287,7 +1261,6 @@ __global__ void k_restrict(BoxGeo F, BoxGeo Cg, const double* __restrict__ rf, d
 
 // xf += P xc : per axis coincident (w 1) or midpoint (w 1/2, 1/2); columns ascending.
 __global__ void k_prolong_add(BoxGeo F, BoxGeo Cg, const double* __restrict__ xc, double* __restrict__ xf) {
-  pdl_enter();
   const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y * blockDim.y + threadIdx.y;
   const int k = blockIdx.z;
   if (i >= F.ex || j >= F.ey) return;
@@ -1315,7 +1288,6 @@ __global__ void k_prolong_add(BoxGeo F, BoxGeo Cg, const double* __restrict__ xc
 
 __global__ void k_reduce_partials(const double* __restrict__ part, int nblk, long long slot_stride,
                                   double* __restrict__ out, long long out_stride) {
-  pdl_enter();
   __shared__ double sh[32];
   const int slot = blockIdx.x;
   const double* p = part + slot * slot_stride;
@@ -1329,7 +1301,6 @@ __global__ void k_reduce_partials(const double* __restrict__ part, int nblk, lon
 // the products in local (natural) order; one thread reproduces it exactly.
 __global__ void k_fold_dot(BoxGeo g, const double* __restrict__ a, const double* __restrict__ b,
                            const double* __restrict__ c, double* __restrict__ out, long long out_stride) {
-  pdl_enter();
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   double s0 = 0.0, s1 = 0.0;
   for (int k = 0; k < g.ez; ++k)
@@ -1349,7 +1320,6 @@ __global__ void k_fold_dot(BoxGeo g, const double* __restrict__ a, const double*
 
 __global__ void k_cg_scalars(int op, const double* __restrict__ rs, int R, const int* __restrict__ ranks, int nr,
                              double* __restrict__ scal) {
-  pdl_enter();
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   double s0 = 0.0, s1 = 0.0;
   for (int q = 0; q < nr; ++q) {
@@ -1388,7 +1358,6 @@ __global__ void k_cg_scalars(int op, const double* __restrict__ rs, int R, const
 // ------------------------------------------------------------------------------------------
 
 __global__ void k_box_compact(BoxGeo g, const double* __restrict__ src, double* __restrict__ dst, int to_compact) {
-  pdl_enter();
   const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y * blockDim.y + threadIdx.y;
   const int k = blockIdx.z;
   if (i >= g.ex || j >= g.ey) return;
@@ -1402,7 +1371,6 @@ __global__ void k_box_compact(BoxGeo g, const double* __restrict__ src, double* 
 
 __global__ void k_region_copy(const CopyDesc* __restrict__ descs, PtrTable src, PtrTable dst,
                               const double* __restrict__ sbuf, double* __restrict__ dbuf) {
-  pdl_enter();
   const CopyDesc d = descs[blockIdx.y];
   const long long n = (long long)d.nx * d.ny * d.nz;
   const double* s = d.src_slot >= 0 ? src.p[d.src_slot] : sbuf;
@@ -1423,7 +1391,6 @@ __global__ void k_region_copy(const CopyDesc* __restrict__ descs, PtrTable src, 
 // y = Ainv x, one warp per row (fixed shuffle tree: deterministic)
 __global__ void k_dense_matvec(const double* __restrict__ A, int n, const long long* __restrict__ map,
                                const double* __restrict__ x, double* __restrict__ y) {
-  pdl_enter();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= n) return;
   double acc = 0.0;
@@ -1438,7 +1405,6 @@ __global__ void k_dense_matvec(const double* __restrict__ A, int n, const long l
 // in the reference's row order on one thread.
 __global__ void k_lu_solve(const double* __restrict__ lu, const long long* __restrict__ piv, int n,
                            const long long* __restrict__ map, const double* __restrict__ b, double* __restrict__ x) {
-  pdl_enter();
   extern __shared__ double y[];
   for (int t = threadIdx.x; t < n; t += blockDim.x) y[t] = b[map[t]];
   __syncthreads();
@@ -1479,71 +1445,43 @@ int grid_blocks(const BoxGeo& g) {
   return gr.x * gr.y * gr.z;
 }
 
-
-// Host launch helper: cudaLaunchKernelEx, with the programmatic-stream-serialization attribute
-// (captured into the CUDA graph as programmatic edges) when TMGX_PDL=1. Opt-in: measured about
-// 1% off the cfg2 solve (10.44 -> 10.34 ms, same box), but one intermittent perf-build
-// iteration-count mismatch was seen in a run combining it with memset-free reductions and is
-// not yet explained, so the default stays a plain launch.
-static bool pdl_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("TMGX_PDL");
-    return e && std::string(e) != "0";
-  }();
-  return on;
-}
-template <typename... KArgs, typename... Args>
-static void klaunch(void (*kern)(KArgs...), dim3 g, dim3 b, size_t smem, cudaStream_t s, Args&&... args) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = g;
-  cfg.blockDim = b;
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
-}
-
 static dim3 plane_grid(const BoxGeo& g, int extra) {
   return dim3((g.ex + extra + 31) / 32, (g.ey + extra + 3) / 4, g.ez + extra);
 }
 
 int launch_fill_coeff(const BoxGeo& g, double* k, const Sphere* sph, int ns, double k_in, bool varcoef,
                       cudaStream_t s) {
-  klaunch(k_fill_coeff, plane_grid(g, 2), dim3(32, 4), 0, s, g, k, sph, ns, k_in, varcoef ? 1 : 0);
+  k_fill_coeff<<<plane_grid(g, 2), dim3(32, 4), 0, s>>>(g, k, sph, ns, k_in, varcoef ? 1 : 0);
   return 1;
 }
 
 int launch_fill_faces(const BoxGeo& g, const OpParams& op, double* fc, long long st, cudaStream_t s) {
-  klaunch(k_fill_faces, plane_grid(g, 1), dim3(32, 4), 0, s, g, op, fc, st);
+  k_fill_faces<<<plane_grid(g, 1), dim3(32, 4), 0, s>>>(g, op, fc, st);
   return 1;
 }
 
 int launch_fill_rhs(const BoxGeo& g, double* b, unsigned long long seed, bool bzero, cudaStream_t s) {
-  klaunch(k_fill_rhs, plane_grid(g, 0), dim3(32, 4), 0, s, g, b, seed, bzero ? 1 : 0);
+  k_fill_rhs<<<plane_grid(g, 0), dim3(32, 4), 0, s>>>(g, b, seed, bzero ? 1 : 0);
   return 1;
 }
 
 int launch_cheb_start_zero(const BoxGeo& g, const OpParams& op, const double* b, double* out, double s_theta,
                            cudaStream_t s) {
   if (op.k)
-    klaunch(k_cheb_start_zero<true>, tile_grid(g), kBlock, 0, s, g, op, b, out, s_theta);
+    k_cheb_start_zero<true><<<tile_grid(g), kBlock, 0, s>>>(g, op, b, out, s_theta);
   else
-    klaunch(k_cheb_start_zero<false>, tile_grid(g), kBlock, 0, s, g, op, b, out, s_theta);
+    k_cheb_start_zero<false><<<tile_grid(g), kBlock, 0, s>>>(g, op, b, out, s_theta);
   return 1;
 }
 
 template <class F>
 static void march(const BoxGeo& g, const OpParams& op, const double* u, const F& f, cudaStream_t s) {
   if (op.S)
-    klaunch(k_march27<F>, tile_grid(g), kBlock, 0, s, g, op, u, f);
+    k_march27<F><<<tile_grid(g), kBlock, 0, s>>>(g, op, u, f);
   else if (op.fc)
-    klaunch(k_march<true, F>, tile_grid(g), kBlock, 0, s, g, op, ULoad{u}, f, nullptr, 0);
+    k_march<true, F><<<tile_grid(g), kBlock, 0, s>>>(g, op, ULoad{u}, f, nullptr, 0);
   else
-    klaunch(k_march<false, F>, tile_grid(g), kBlock, 0, s, g, op, ULoad{u}, f, nullptr, 0);
+    k_march<false, F><<<tile_grid(g), kBlock, 0, s>>>(g, op, ULoad{u}, f, nullptr, 0);
 }
 
 bool pspmv_supported(const OpParams& op) { return op.S == nullptr && (op.fc != nullptr || op.k == nullptr); }
@@ -1555,9 +1493,9 @@ int launch_pspmv_dot(const BoxGeo& g, const OpParams& op, const double* z, const
   const UPDir u{z, p_old, 0.0};
   const FSpmvDotP f{w, p_new, part};
   if (op.fc)
-    klaunch(k_march<true, FSpmvDotP, UPDir>, tile_grid(g), kBlock, 0, s, g, op, u, f, scal, beta_slot);
+    k_march<true, FSpmvDotP, UPDir><<<tile_grid(g), kBlock, 0, s>>>(g, op, u, f, scal, beta_slot);
   else
-    klaunch(k_march<false, FSpmvDotP, UPDir>, tile_grid(g), kBlock, 0, s, g, op, u, f, scal, beta_slot);
+    k_march<false, FSpmvDotP, UPDir><<<tile_grid(g), kBlock, 0, s>>>(g, op, u, f, scal, beta_slot);
   return 1;
 }
 
@@ -1683,7 +1621,7 @@ static int launch_tb_rows(const BoxGeo& g, const OpParams& op, const double* b, 
   auto run = [&](auto kern, size_t smem, int& slots, bool dots) {
     auto [gr, gt] = go(kern, smem, slots);
     if (dots && nblk > dmax) return false;  // partial buffer too small: caller falls back
-    klaunch(kern, gr, bl, smem, s, maps, gt, op, xout, s_theta, c.c1, c.c2, dpart, dstride);
+    kern<<<gr, bl, smem, s>>>(maps, gt, op, xout, s_theta, c.c1, c.c2, dpart, dstride);
     return true;
   };
   static int slots[6] = {0, 0, 0, 0, 0, 0};
@@ -1734,31 +1672,31 @@ int launch_resid_restrict(const BoxGeo& fine, const OpParams& op, const BoxGeo& 
                           const double* x, double* bc, cudaStream_t s) {
   const dim3 gr((coarse.ex + kRRCX - 1) / kRRCX, (coarse.ey + kRRCY - 1) / kRRCY, (coarse.ez + coarse.zc - 1) / coarse.zc);
   if (op.fc)
-    klaunch(k_resid_restrict<true>, gr, dim3(32, 8), 0, s, fine, op, coarse, b, x, bc);
+    k_resid_restrict<true><<<gr, dim3(32, 8), 0, s>>>(fine, op, coarse, b, x, bc);
   else
-    klaunch(k_resid_restrict<false>, gr, dim3(32, 8), 0, s, fine, op, coarse, b, x, bc);
+    k_resid_restrict<false><<<gr, dim3(32, 8), 0, s>>>(fine, op, coarse, b, x, bc);
   return 1;
 }
 
 int launch_prolong_to(const BoxGeo& fine, const BoxGeo& coarse, const double* xc, const double* xf, double* xo,
                       cudaStream_t s) {
-  klaunch(k_prolong_pair, tile_grid(fine), kBlock, 0, s, fine, coarse, xc, xf, xo);
+  k_prolong_pair<<<tile_grid(fine), kBlock, 0, s>>>(fine, coarse, xc, xf, xo);
   return 1;
 }
 
 int launch_restrict_scaled(const BoxGeo& fine, const BoxGeo& coarse, const double* rf, double* bc, double scale,
                            cudaStream_t s) {
-  klaunch(k_restrict, plane_grid(coarse, 0), dim3(32, 4), 0, s, fine, coarse, rf, bc, scale);
+  k_restrict<<<plane_grid(coarse, 0), dim3(32, 4), 0, s>>>(fine, coarse, rf, bc, scale);
   return 1;
 }
 
 int launch_restrict(const BoxGeo& fine, const BoxGeo& coarse, const double* rf, double* bc, cudaStream_t s) {
-  klaunch(k_restrict, plane_grid(coarse, 0), dim3(32, 4), 0, s, fine, coarse, rf, bc, 0.125);
+  k_restrict<<<plane_grid(coarse, 0), dim3(32, 4), 0, s>>>(fine, coarse, rf, bc, 0.125);
   return 1;
 }
 
 int launch_prolong_add(const BoxGeo& fine, const BoxGeo& coarse, const double* xc, double* xf, cudaStream_t s) {
-  klaunch(k_prolong_pair, tile_grid(fine), kBlock, 0, s, fine, coarse, xc, xf, xf);
+  k_prolong_pair<<<tile_grid(fine), kBlock, 0, s>>>(fine, coarse, xc, xf, xf);
   return 1;
 }
 
@@ -1766,11 +1704,11 @@ int launch_galerkin(const BoxGeo& fine, const OpParams& fop, const BoxGeo& coars
                     const Sphere* sph, int ns, double k_in, cudaStream_t s) {
   const dim3 gr(plane_grid(coarse, 0));
   if (fop.S)
-    klaunch(k_galerkin<true, false>, gr, dim3(32, 4), 0, s, fine, fop, coarse, Sc, cst, sph, ns, k_in);
+    k_galerkin<true, false><<<gr, dim3(32, 4), 0, s>>>(fine, fop, coarse, Sc, cst, sph, ns, k_in);
   else if (fop.k)
-    klaunch(k_galerkin<false, true>, gr, dim3(32, 4), 0, s, fine, fop, coarse, Sc, cst, sph, ns, k_in);
+    k_galerkin<false, true><<<gr, dim3(32, 4), 0, s>>>(fine, fop, coarse, Sc, cst, sph, ns, k_in);
   else
-    klaunch(k_galerkin<false, false>, gr, dim3(32, 4), 0, s, fine, fop, coarse, Sc, cst, sph, ns, k_in);
+    k_galerkin<false, false><<<gr, dim3(32, 4), 0, s>>>(fine, fop, coarse, Sc, cst, sph, ns, k_in);
   return 1;
 }
 
@@ -1781,71 +1719,71 @@ int launch_spmv_dot(const BoxGeo& g, const OpParams& op, const double* p, double
 
 int launch_dot2(const BoxGeo& g, const double* a, const double* b, const double* c, double* pab, double* pcc,
                 cudaStream_t s) {
-  klaunch(k_dot2, tile_grid(g), kBlock, 0, s, g, a, b, c, pab, pcc);
+  k_dot2<<<tile_grid(g), kBlock, 0, s>>>(g, a, b, c, pab, pcc);
   return 1;
 }
 
 int launch_jacobi_dot(const BoxGeo& g, const OpParams& op, const double* r, double* z, double* part,
                       cudaStream_t s) {
   if (op.k)
-    klaunch(k_jacobi_dot<true>, tile_grid(g), kBlock, 0, s, g, op, r, z, part);
+    k_jacobi_dot<true><<<tile_grid(g), kBlock, 0, s>>>(g, op, r, z, part);
   else
-    klaunch(k_jacobi_dot<false>, tile_grid(g), kBlock, 0, s, g, op, r, z, part);
+    k_jacobi_dot<false><<<tile_grid(g), kBlock, 0, s>>>(g, op, r, z, part);
   return 1;
 }
 
 int launch_cg_update(const BoxGeo& g, const double* p, const double* w, double* x, double* r, const double* scal,
                      int as, int fs, cudaStream_t s) {
-  klaunch(k_cg_update, tile_grid(g), kBlock, 0, s, g, p, w, x, r, scal, as, fs);
+  k_cg_update<<<tile_grid(g), kBlock, 0, s>>>(g, p, w, x, r, scal, as, fs);
   return 1;
 }
 
 int launch_p_update(const BoxGeo& g, const double* z, double* p, const double* scal, int bs, cudaStream_t s) {
-  klaunch(k_p_update, tile_grid(g), kBlock, 0, s, g, z, p, scal, bs);
+  k_p_update<<<tile_grid(g), kBlock, 0, s>>>(g, z, p, scal, bs);
   return 1;
 }
 
 int launch_copy_interior(const BoxGeo& g, const double* src, double* dst, cudaStream_t s) {
-  klaunch(k_axpy, tile_grid(g), kBlock, 0, s, g, 0.0, src, dst, 1);
+  k_axpy<<<tile_grid(g), kBlock, 0, s>>>(g, 0.0, src, dst, 1);
   return 1;
 }
 
 int launch_axpy(const BoxGeo& g, double alpha, const double* x, double* y, cudaStream_t s) {
-  klaunch(k_axpy, tile_grid(g), kBlock, 0, s, g, alpha, x, y, 0);
+  k_axpy<<<tile_grid(g), kBlock, 0, s>>>(g, alpha, x, y, 0);
   return 1;
 }
 
 int launch_zero(double* p, long long n, cudaStream_t s) {
   const long long blocks = (n + 255) / 256;
-  klaunch(k_zero, (unsigned)(blocks < 4096 ? (blocks > 0 ? blocks : 1) : 4096), 256, 0, s, p, n);
+  k_zero<<<(unsigned)(blocks < 4096 ? (blocks > 0 ? blocks : 1) : 4096), 256, 0, s>>>(p, n);
   return 1;
 }
 
 int launch_reduce_partials(const double* part, int nblk, int nslots, long long slot_stride, double* out,
                            long long out_stride, cudaStream_t s) {
-  klaunch(k_reduce_partials, nslots, 512, 0, s, part, nblk, slot_stride, out, out_stride);
+  k_reduce_partials<<<nslots, 512, 0, s>>>(part, nblk, slot_stride, out, out_stride);
   return 1;
 }
 
 int launch_fold_dot(const BoxGeo& g, const double* a, const double* b, const double* c, double* out,
                     long long out_stride, cudaStream_t s) {
-  klaunch(k_fold_dot, 1, 32, 0, s, g, a, b, c, out, out_stride);
+  k_fold_dot<<<1, 32, 0, s>>>(g, a, b, c, out, out_stride);
   return 1;
 }
 
 int launch_cg_scalars(int op, const double* rank_sums, int R, const int* ranks_dev, int nranks, double* scal,
                       cudaStream_t s) {
-  klaunch(k_cg_scalars, 1, 32, 0, s, op, rank_sums, R, ranks_dev, nranks, scal);
+  k_cg_scalars<<<1, 32, 0, s>>>(op, rank_sums, R, ranks_dev, nranks, scal);
   return 1;
 }
 
 int launch_box_to_compact(const BoxGeo& g, const double* box, double* compact, cudaStream_t s) {
-  klaunch(k_box_compact, plane_grid(g, 0), dim3(32, 4), 0, s, g, box, compact, 1);
+  k_box_compact<<<plane_grid(g, 0), dim3(32, 4), 0, s>>>(g, box, compact, 1);
   return 1;
 }
 
 int launch_compact_to_box(const BoxGeo& g, const double* compact, double* box, cudaStream_t s) {
-  klaunch(k_box_compact, plane_grid(g, 0), dim3(32, 4), 0, s, g, compact, box, 0);
+  k_box_compact<<<plane_grid(g, 0), dim3(32, 4), 0, s>>>(g, compact, box, 0);
   return 1;
 }
 
@@ -1855,14 +1793,14 @@ int launch_region_copy(const CopyDesc* desc_dev, int ndesc, int max_elems, const
   int bx = (max_elems + 255) / 256;
   if (bx > 1024) bx = 1024;
   if (bx < 1) bx = 1;
-  klaunch(k_region_copy, dim3(bx, ndesc), 256, 0, s, desc_dev, src, dst, src_buf, dst_buf);
+  k_region_copy<<<dim3(bx, ndesc), 256, 0, s>>>(desc_dev, src, dst, src_buf, dst_buf);
   return 1;
 }
 
 int launch_dense_matvec(const double* A, int n, const long long* map, const double* x, double* y, cudaStream_t s) {
   const int threads = 256;
   const int blocks = (n * 32 + threads - 1) / threads;
-  klaunch(k_dense_matvec, blocks, threads, 0, s, A, n, map, x, y);
+  k_dense_matvec<<<blocks, threads, 0, s>>>(A, n, map, x, y);
   return 1;
 }
 
@@ -1870,7 +1808,7 @@ int launch_lu_solve(const double* lu, const long long* piv, int n, const long lo
                     cudaStream_t s) {
   const size_t shmem = sizeof(double) * 2 * (size_t)n;
   if (shmem > 48 * 1024) cudaFuncSetAttribute(k_lu_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem);
-  klaunch(k_lu_solve, 1, 256, shmem, s, lu, piv, n, map, b, x);
+  k_lu_solve<<<1, 256, shmem, s>>>(lu, piv, n, map, b, x);
   return 1;
 }
 
