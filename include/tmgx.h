@@ -161,7 +161,11 @@ int tmgx_fill_rhs(tmgx_solver s, uint64_t seed, double *b_local);
 /* krylov_solve (solver.cpp:420-480) with the MG preconditioner. b/x are this process's
  * slice of the rank-block ordering (DistVector local order, grid.cpp:61-82), host or
  * device memory as flagged. history: room for max_its+1 norms, or NULL. Returns 0, or 2
- * on divergence (report filled either way). */
+ * on divergence (report filled either way).
+ * Stream contract: the library works on its own non-blocking stream. Device-resident b / x are
+ * read only after all work previously submitted to the legacy default stream (e.g. torch's
+ * default stream) has completed; work on any other caller stream must be synchronised by the
+ * caller first. The call returns after x is written (host-synchronous). */
 int tmgx_solve(tmgx_solver s, const double *b, double *x, int on_device, const tmgx_ksp_cfg *cfg,
                double *history, tmgx_report *rep);
 /* Same, with the right-hand side generated on the device from `seed` (inputs resident). */

@@ -300,11 +300,16 @@ int main(int argc, char** argv) {
     char buf[512];
     std::snprintf(buf, sizeof buf,
                   "{\"iterations\": %d, \"reason\": \"%s\", \"xnorm\": %.17g, \"final_ratio\": %.17g, "
-                  "\"t_setup_s\": %.6f, \"t_solve_s\": %.6f, \"n\": %lld, \"cheb_hi_fine\": %.17g}",
+                  "\"t_setup_s\": %.6f, \"t_solve_s\": %.6f, \"n\": %lld, \"cheb_hi_fine\": %.17g, \"history\": [",
                   rep.iterations, to_string(rep.reason).c_str(), norm2(x),
                   rep.residual_history.back() / rep.residual_history.front(), t_setup, t_solve / std::max(1, steps),
                   (long long)(N * N * N), mg->bound_hi(nlevels - 1));
-    return std::string(buf);
+    std::string out(buf);
+    for (std::size_t q = 0; q < rep.residual_history.size(); ++q) {
+      std::snprintf(buf, sizeof buf, "%s%.17g", q ? ", " : "", rep.residual_history[q]);
+      out += buf;
+    }
+    return out + "]}";
   });
   std::printf("%s\n", res[0].c_str());
   return 0;

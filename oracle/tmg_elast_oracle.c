@@ -102,6 +102,8 @@ static int clamped(const el_level *L, int64_t i) { (void)L; return i == 0; }
 /* y = A x on level L (rows in natural vertex order, 3 interleaved dofs) */
 static void el_apply(const orc_el_mg *mg, const el_level *L, const double *x, double *y) {
   const int64_t nx = L->n[0], ny = L->n[1], nz = L->n[2];
+
+  #pragma omp parallel for schedule(static)
   for (int64_t k = 0; k < nz; ++k)
     for (int64_t j = 0; j < ny; ++j)
       for (int64_t i = 0; i < nx; ++i) {

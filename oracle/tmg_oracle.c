@@ -357,6 +357,7 @@ static void level_build(const orc_mg_cfg *cfg, orc_level *L) {
     L->ih2[a] = 1.0 / (h * h);
   }
   L->k = malloc(sizeof(double) * L->nv);
+  #pragma omp parallel for schedule(static)
   for (int64_t k = 0; k < nz; ++k)
     for (int64_t j = 0; j < ny; ++j)
       for (int64_t i = 0; i < nx; ++i) {
@@ -376,6 +377,7 @@ static void level_build(const orc_mg_cfg *cfg, orc_level *L) {
   L->diag = malloc(sizeof(double) * L->nv);
   L->inv_diag = malloc(sizeof(double) * L->nv);
   const int64_t sx = 1, sy = nx, sz = nx * ny;
+  #pragma omp parallel for schedule(static)
   for (int64_t k = 0; k < nz; ++k)
     for (int64_t j = 0; j < ny; ++j)
       for (int64_t i = 0; i < nx; ++i) {
@@ -408,6 +410,7 @@ static void level_apply(const orc_level *L, const double *x, double *y) {
   const int64_t nx = L->n[0], ny = L->n[1], nz = L->n[2];
   const int64_t sy = nx, sz = nx * ny;
   if (L->S) { /* 27-point Galerkin row, columns ascending (dz, dy, dx lexicographic) */
+    #pragma omp parallel for schedule(static)
     for (int64_t k = 0; k < nz; ++k)
       for (int64_t j = 0; j < ny; ++j)
         for (int64_t i = 0; i < nx; ++i) {
@@ -422,6 +425,7 @@ static void level_apply(const orc_level *L, const double *x, double *y) {
         }
     return;
   }
+  #pragma omp parallel for schedule(static)
   for (int64_t k = 0; k < nz; ++k)
     for (int64_t j = 0; j < ny; ++j)
       for (int64_t i = 0; i < nx; ++i) {
@@ -466,6 +470,7 @@ static double pw1(int64_t d) { return d == 0 ? 1.0 : ((d == 1 || d == -1) ? 0.5 
 static void galerkin_build(const orc_level *F, orc_level *C) {
   const int64_t cn = C->nv;
   C->S = calloc((size_t)(27 * cn), sizeof(double));
+  #pragma omp parallel for schedule(static)
   for (int64_t K = 0; K < C->n[2]; ++K)
     for (int64_t J = 0; J < C->n[1]; ++J)
       for (int64_t I = 0; I < C->n[0]; ++I) {
@@ -523,6 +528,7 @@ double orc_dot(int64_t n, const double *x, const double *y) {
 }
 
 static void jacobi(const orc_level *L, const double *x, double *y) {
+  #pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < L->nv; ++i) y[i] = x[i] * L->inv_diag[i];
 }
 
@@ -577,7 +583,9 @@ int orc_estimate_generic(int64_t n, op_fn A, op_fn M, const void *ctx, const dou
       break;
     }
     const double alpha = rz / pw;
+    #pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < n; ++i) x[i] += alpha * p[i];
+    #pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < n; ++i) r[i] += -alpha * w[i];
     M(ctx, r, z);
     const double rz_new = orc_dot(n, r, z);
@@ -587,6 +595,7 @@ int orc_estimate_generic(int64_t n, op_fn A, op_fn M, const void *ctx, const dou
     betas[nb++] = beta;
     rz = rz_new;
     if (mode == ORC_EST_LANCZOS)
+      #pragma omp parallel for schedule(static)
       for (int64_t i = 0; i < n; ++i) p[i] = z[i] + beta * p[i];
   }
   free(r); free(z); free(p); free(w); free(x);
@@ -614,6 +623,7 @@ static void lvl_A(const void *ctx, const double *x, double *y) { level_apply((co
 static void lvl_M(const void *ctx, const double *x, double *y) { jacobi((const orc_level *)ctx, x, y); }
 
 void orc_fill_random(int64_t n, uint64_t seed, double *x) {
+  #pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < n; ++i) x[i] = 2.0 * orc_hashed_uniform(seed, (uint64_t)i) - 1.0;
 }
 
@@ -664,18 +674,23 @@ static void smooth(const orc_level *L, int m, const double *b, double *x) {
   const double sigma = theta / delta;
   double rho = 1.0 / sigma;
   level_apply(L, x, r);
+  #pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < n; ++i) r[i] = b[i] - r[i];
   jacobi(L, r, z);
   const double s = 1.0 / theta;
+  #pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < n; ++i) d[i] = z[i] * s;
   for (int it = 0; it < m; ++it) {
+    #pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < n; ++i) x[i] += 1.0 * d[i];
     if (it + 1 == m) break;
     level_apply(L, d, ad);
+    #pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < n; ++i) r[i] += -1.0 * ad[i];
     jacobi(L, r, z);
     const double rho_new = 1.0 / (2.0 * sigma - rho);
     const double c1 = rho_new * rho, c2 = 2.0 * rho_new / delta;
+    #pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < n; ++i) d[i] = c1 * d[i] + c2 * z[i];
     rho = rho_new;
   }
@@ -684,6 +699,7 @@ static void smooth(const orc_level *L, int m, const double *b, double *x) {
 
 /* R = 2^-3 P^T, P from grid.cpp:373-428; transpose columns ascending (1 rank). */
 static void restrict_(const orc_level *F, const orc_level *C, const double *rf, double *bc) {
+  #pragma omp parallel for schedule(static)
   for (int64_t K = 0; K < C->n[2]; ++K)
     for (int64_t J = 0; J < C->n[1]; ++J)
       for (int64_t I = 0; I < C->n[0]; ++I) {
@@ -708,6 +724,7 @@ static void restrict_(const orc_level *F, const orc_level *C, const double *rf, 
 
 /* y = P xc (grid.cpp:396-425 weights, columns ascending) then axpy(1, y, xf) */
 static void prolong_add(const orc_level *F, const orc_level *C, const double *xc, double *xf) {
+  #pragma omp parallel for schedule(static)
   for (int64_t k = 0; k < F->n[2]; ++k)
     for (int64_t j = 0; j < F->n[1]; ++j)
       for (int64_t i = 0; i < F->n[0]; ++i) {
@@ -807,6 +824,7 @@ void orc_vcycle(const orc_mg *mg, int level, const double *b, double *x) {
   smooth(L, mg->cfg.smooth_its, b, x);
   double *r = malloc(sizeof(double) * L->nv);
   level_apply(L, x, r);
+  #pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < L->nv; ++i) r[i] = b[i] - r[i];
   double *bc = malloc(sizeof(double) * C->nv), *xc = malloc(sizeof(double) * C->nv);
   restrict_(L, C, r, bc);
@@ -864,6 +882,7 @@ void orc_mg_coeff(const orc_mg *mg, int level, double *k_out) {
 }
 
 void orc_rhs(const int64_t np[3], uint64_t seed, double *b) {
+  #pragma omp parallel for schedule(static)
   for (int64_t k = 0; k < np[2]; ++k)
     for (int64_t j = 0; j < np[1]; ++j)
       for (int64_t i = 0; i < np[0]; ++i) {
@@ -895,6 +914,7 @@ int orc_mgcg_solve(const orc_mg *mg, const double *b, double *x, double rtol, do
   double *p = malloc(sizeof(double) * n), *w = malloc(sizeof(double) * n);
   memset(rep, 0, sizeof *rep);
   level_apply(L, x, r);
+  #pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < n; ++i) r[i] = b[i] - r[i];
   orc_vcycle(mg, top, r, z);
   double nrm = sqrt(orc_dot(n, z, z));
@@ -914,7 +934,9 @@ int orc_mgcg_solve(const orc_mg *mg, const double *b, double *x, double rtol, do
     const double pw = orc_dot(n, p, w);
     if (pw <= 0.0 || !isfinite(pw)) { rep->reason = 4; goto done; }
     const double alpha = rz / pw;
+    #pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < n; ++i) x[i] += alpha * p[i];
+    #pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < n; ++i) r[i] += -alpha * w[i];
     orc_vcycle(mg, top, r, z);
     const double rz_new = orc_dot(n, r, z);
@@ -926,6 +948,7 @@ int orc_mgcg_solve(const orc_mg *mg, const double *b, double *x, double rtol, do
     if (rz == 0.0 || !isfinite(rz_new)) { rep->reason = 4; goto done; }
     const double beta = rz_new / rz;
     rz = rz_new;
+    #pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < n; ++i) p[i] = z[i] + beta * p[i];
   }
   rep->reason = 2;

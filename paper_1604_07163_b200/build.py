@@ -56,6 +56,10 @@ def build(parity=False, verbose=False, force=False):
     if parity:
         flags += ["-fmad=false", "-DTMGX_PARITY"]
     flags += os.environ.get("TMGX_NVCC_EXTRA", "").split()  # tuning experiments (e.g. -DTMGX_TB_PF=6)
+    # objects built with other flags (e.g. a TMGX_NVCC_EXTRA experiment) are never reused
+    stamp = os.path.join(objdir, "flags.txt")
+    if not os.path.exists(stamp) or open(stamp).read() != " ".join(flags):
+        force = True
     cmds, objs = [], []
     for src in SOURCES:
         s = os.path.join(CSRC, src)
@@ -73,6 +77,8 @@ def build(parity=False, verbose=False, force=False):
 
     with ThreadPoolExecutor(max_workers=4) as ex:
         logs = list(ex.map(run, cmds))
+    with open(stamp, "w") as f:
+        f.write(" ".join(flags))
     if verbose:
         for lg in logs:
             sys.stdout.write(lg)

@@ -344,9 +344,7 @@ int tmgx_solver_from_options(tmgx_world w, const tmgx_problem* prob, tmgx_option
     const auto r = tmg::resolve_solver_tree(o->db, prefix ? prefix : "", default_ksp ? default_ksp : "gmres");
     tmgx_mg_cfg mg;
     resolved_to_c(r, &mg, ksp);
-    const int rc = tmgx_solver_create(w, prob, &mg, out);
-    if (rc) throw tmg::ConfigError(g_err);
-    return 0;
+    return tmgx_solver_create(w, prob, &mg, out);  // its status code (config / CUDA / internal) and message
   });
 }
 

@@ -349,12 +349,14 @@ void ElastSolver::download(int l, const double* dev, double* host) {
 ElastSolver::ElastSolver(World& W_, const int64_t np[3], int nlevels, int m_, int est_mode, uint64_t seed_e, double nu)
     : W(W_), m(m_) {
   CK(cudaSetDevice(W.device));
+  arena.set_stream(W.stream);
   if (W.R != 1 || W.P != 1)
     throw tmg::ConfigError("elasticity path: one box on one GPU (box split + telescope not implemented)");
   if (nlevels < 1 || m < 1) throw tmg::ConfigError("elasticity: nlevels and smooth_its must be >= 1");
   double K[576];
   q1_kref(nu, K);
-  CK(cudaMemcpyToSymbol(c_K, K, sizeof K));
+  CK(cudaMemcpyToSymbolAsync(c_K, K, sizeof K, 0, cudaMemcpyHostToDevice, W.stream));
+  CK(cudaStreamSynchronize(W.stream));
   // level ladder (coarsest first)
   std::vector<std::array<int64_t, 3>> dims(nlevels);
   std::array<int64_t, 3> n = {np[0], np[1], np[2]};
@@ -412,7 +414,7 @@ ElastSolver::ElastSolver(World& W_, const int64_t np[3], int nlevels, int m_, in
         for (int i = 0; i < mx; ++i)
           Epad[(size_t)(g.base + i + g.px * j + g.pxy * k)] = Eh[(size_t)i + (size_t)mx * (j + (size_t)my * k)];
     lv.E = arena.alloc(g.total);
-    CK(cudaMemcpy(lv.E, Epad.data(), sizeof(double) * g.total, cudaMemcpyHostToDevice));
+    arena.upload(lv.E, Epad.data(), sizeof(double) * g.total);
     lv.binv = arena.alloc(9 * g.total);
     k_el_binv<<<vgrid(g), 128, 0, W.stream>>>(g, lv.E, lv.h, lv.binv);
     for (double** f : {&lv.b, &lv.x, &lv.r, &lv.z, &lv.d, &lv.ad}) *f = arena.alloc(3 * g.total);
@@ -551,6 +553,13 @@ int ElastSolver::solve(const double* b, double* x, double rtol, double atol, int
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
+  {  // stream contract (tmgx.h): order after the caller's legacy-default-stream work on b / x
+    cudaEvent_t ev;
+    CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    CK(cudaEventRecord(ev, cudaStreamLegacy));
+    CK(cudaStreamWaitEvent(W.stream, ev, 0));
+    CK(cudaEventDestroy(ev));
+  }
   CK(cudaEventRecord(e0, W.stream));
   upload(top, b, cw);  // b -> cw
   if (x && x0_nonzero)

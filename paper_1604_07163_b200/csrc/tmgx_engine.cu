@@ -121,10 +121,17 @@ DeviceArena::~DeviceArena() {
 double* DeviceArena::alloc(long long n) {
   void* p = nullptr;
   if (n < 1) n = 1;
+  if (!stream_) throw tmg::Error("device arena: no stream bound");
   CK(cudaMalloc(&p, (size_t)n * sizeof(double)));
-  CK(cudaMemset(p, 0, (size_t)n * sizeof(double)));
   ptrs_.push_back(p);
+  CK(cudaMemsetAsync(p, 0, (size_t)n * sizeof(double), stream_));
   return static_cast<double*>(p);
+}
+
+void DeviceArena::upload(void* dst, const void* src, size_t bytes) {
+  if (!bytes) return;
+  CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream_));
+  CK(cudaStreamSynchronize(stream_));
 }
 
 Field make_field(DeviceArena& A, const Dist& D) {
@@ -248,7 +255,7 @@ RegionPlan upload_plan(DeviceArena& A, const PlanHost& h) {
     n = (int)v.size();
     if (!n) return;
     dst = A.alloc_t<CopyDesc>(n);
-    CK(cudaMemcpy(dst, v.data(), sizeof(CopyDesc) * v.size(), cudaMemcpyHostToDevice));
+    A.upload(dst, v.data(), sizeof(CopyDesc) * v.size());
   };
   up(h.loc, plan.d_local, plan.n_local);
   up(h.pack, plan.d_pack, plan.n_pack);
@@ -365,6 +372,7 @@ static OpParams make_op(const tmg::GridHeader& h) {
 
 Solver::Solver(World& W_, const ProblemDesc& P, const MGDesc& M) : W(W_), prob(P), mgd(M) {
   CK(cudaSetDevice(W.device));
+  arena.set_stream(W.stream);
   if (const char* e = std::getenv("TMGX_GRAPHS")) use_graphs = std::string(e) != "0";
   if (const char* e = std::getenv("TMGX_TB")) tb_enabled = std::string(e) != "0";
   if (const char* e = std::getenv("TMGX_FUSE_CG")) fuse_cg = std::string(e) != "0";
@@ -384,7 +392,7 @@ Solver::Solver(World& W_, const ProblemDesc& P, const MGDesc& M) : W(W_), prob(P
       spheres.push_back(sp);
     }
     spheres_dev = arena.alloc_t<Sphere>((long long)spheres.size());
-    CK(cudaMemcpy(spheres_dev, spheres.data(), sizeof(Sphere) * spheres.size(), cudaMemcpyHostToDevice));
+    arena.upload(spheres_dev, spheres.data(), sizeof(Sphere) * spheres.size());
   }
   build_nodes();
 }
@@ -528,7 +536,7 @@ void Solver::build_nodes() {
   {
     const Dist& D0 = *nodes[0].dist;
     ranks_dev = arena.alloc_t<int>(D0.h.n_ranks());
-    CK(cudaMemcpy(ranks_dev, D0.wr.data(), sizeof(int) * D0.wr.size(), cudaMemcpyHostToDevice));
+    arena.upload(ranks_dev, D0.wr.data(), sizeof(int) * D0.wr.size());
   }
   if (mgd.galerkin) build_galerkin();
   setup_coarse(nodes.back());
@@ -615,12 +623,12 @@ void dense_lu_setup(DeviceArena& arena, std::vector<double> a, int n, const std:
     }
   }
   *map_dev = arena.alloc_t<long long>(n);
-  CK(cudaMemcpy(*map_dev, map.data(), sizeof(long long) * n, cudaMemcpyHostToDevice));
+  arena.upload(*map_dev, map.data(), sizeof(long long) * n);
   *A_dev = arena.alloc((long long)n * n);
   if (parity_build()) {
     *piv_dev = arena.alloc_t<long long>(n);
-    CK(cudaMemcpy(*piv_dev, piv.data(), sizeof(long long) * n, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(*A_dev, a.data(), sizeof(double) * (size_t)n * n, cudaMemcpyHostToDevice));
+    arena.upload(*piv_dev, piv.data(), sizeof(long long) * n);
+    arena.upload(*A_dev, a.data(), sizeof(double) * (size_t)n * n);
   } else {
     // Performance build: explicit inverse from the same factors (columns = DenseLU::solve(e_c)),
     // applied as one warp-per-row matvec instead of a 2n-step dependent substitution chain.
@@ -640,7 +648,7 @@ void dense_lu_setup(DeviceArena& arena, std::vector<double> a, int n, const std:
       }
       for (int r = 0; r < n; ++r) inv[(size_t)r * n + c] = x[(size_t)r];
     }
-    CK(cudaMemcpy(*A_dev, inv.data(), sizeof(double) * (size_t)n * n, cudaMemcpyHostToDevice));
+    arena.upload(*A_dev, inv.data(), sizeof(double) * (size_t)n * n);
   }
 }
 
@@ -655,7 +663,8 @@ void Solver::setup_coarse(Node& nd) {
   std::vector<double> a((size_t)n * n, 0.0);
   if (!nd.S.p.empty()) {  // 27-point Galerkin rows from the device
     std::vector<double> S((size_t)27 * g.total);
-    CK(cudaMemcpy(S.data(), nd.S.p[0], sizeof(double) * S.size(), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpyAsync(S.data(), nd.S.p[0], sizeof(double) * S.size(), cudaMemcpyDeviceToHost, W.stream));
+    CK(cudaStreamSynchronize(W.stream));
     for (int k = 0; k < nz; ++k)
       for (int j = 0; j < ny; ++j)
         for (int i = 0; i < nx; ++i) {
@@ -1108,7 +1117,17 @@ void Solver::run_iteration(int par) {
   W.cnt.launches += iter_launches;
 }
 
+// Device inputs (tmgx.h stream contract): the library's stream waits for all work submitted so far
+// to the legacy default stream (torch's default stream), so a caller that filled b / x there
+// needs no extra synchronisation. Work on other caller streams must be synchronised by the caller.
+void Solver::order_after_caller() {
+  if (!caller_ev) CK(cudaEventCreateWithFlags(&caller_ev, cudaEventDisableTiming));
+  CK(cudaEventRecord(caller_ev, cudaStreamLegacy));
+  CK(cudaStreamWaitEvent(W.stream, caller_ev, 0));
+}
+
 Solver::~Solver() {
+  if (caller_ev) cudaEventDestroy(caller_ev);
   for (auto& e : iter_exec)
     if (e) cudaGraphExecDestroy(e);
   if (host_scal) cudaFreeHost(host_scal);
@@ -1124,6 +1143,7 @@ int Solver::solve(const double* b, double* x, bool on_device, int method, double
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
+  if (on_device) order_after_caller();
   CK(cudaEventRecord(e0, W.stream));
   *its = 0;
   *reason = 2;  // max_its

@@ -75,17 +75,25 @@ struct Field {
   PtrTable table() const;
 };
 
+// Device allocations of one solver. Every buffer is zeroed, and every host upload is issued, in
+// stream order on the owner's stream (cudaStreamNonBlocking streams do not order against the
+// legacy default stream, so a plain cudaMemset/cudaMemcpy could land after the setup kernels that
+// follow it on that stream).
 class DeviceArena {
  public:
   ~DeviceArena();
+  void set_stream(cudaStream_t s) { stream_ = s; }
   double* alloc(long long n);
   template <class T>
   T* alloc_t(long long n) {
     return reinterpret_cast<T*>(alloc((n * (long long)sizeof(T) + 7) / 8));
   }
+  // H2D copy on the arena's stream; returns when the copy is complete (src may be a temporary)
+  void upload(void* dst, const void* src, size_t bytes);
 
  private:
   std::vector<void*> ptrs_;
+  cudaStream_t stream_ = nullptr;
 };
 
 Field make_field(DeviceArena& A, const Dist& D);
@@ -233,6 +241,8 @@ class Solver {
   void upload(int i, const Field& f, const double* src, bool on_device);
   void download(int i, const Field& f, double* dst, bool on_device);
 
+  cudaEvent_t caller_ev = nullptr;
+  void order_after_caller();
   int solve(const double* b, double* x, bool on_device, int method, double rtol, double atol, int max_its,
             double* hist, int* reason, int* its, double* norm0, double* normf, double* t_ms, bool seeded,
             unsigned long long seed, bool x0_nonzero = true);

@@ -1298,24 +1298,43 @@ __global__ void k_reduce_partials(const double* __restrict__ part, int nblk, lon
 }
 
 // Parity build: dist_vector.cpp:33-38 + comm.cpp:338-351 on one rank is a serial left fold of
-// the products in local (natural) order; one thread reproduces it exactly.
-__global__ void k_fold_dot(BoxGeo g, const double* __restrict__ a, const double* __restrict__ b,
-                           const double* __restrict__ c, double* __restrict__ out, long long out_stride) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+// the products in local (natural) order. The block forms the products of a chunk in parallel
+// (each product rounds exactly as in the serial loop) and thread 0 folds them in order.
+constexpr int kFoldChunk = 4096;
+__global__ void __launch_bounds__(1024) k_fold_dot(BoxGeo g, const double* __restrict__ a, const double* __restrict__ b,
+                                                   const double* __restrict__ c, double* __restrict__ out,
+                                                   long long out_stride) {
+  __shared__ double pa[kFoldChunk];
+  __shared__ double pc[kFoldChunk];
+  const long long n = (long long)g.ex * g.ey * g.ez;
   double s0 = 0.0, s1 = 0.0;
-  for (int k = 0; k < g.ez; ++k)
-    for (int j = 0; j < g.ey; ++j)
-      for (int i = 0; i < g.ex; ++i) {
-        const long long v = vidx(g, i, j, k);
-        const double p = a[v] * b[v];
-        s0 += p;
-        if (c) {
-          const double q = c[v] * c[v];
-          s1 += q;
+  for (long long e0 = 0; e0 < n; e0 += kFoldChunk) {
+    const int cnt = (int)min((long long)kFoldChunk, n - e0);
+    for (int t = threadIdx.x; t < cnt; t += blockDim.x) {
+      const long long e = e0 + t;
+      const int i = (int)(e % g.ex);
+      const long long q = e / g.ex;
+      const int j = (int)(q % g.ey), k = (int)(q / g.ey);
+      const long long v = vidx(g, i, j, k);
+      pa[t] = a[v] * b[v];
+      if (c) pc[t] = c[v] * c[v];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (c)
+        for (int t = 0; t < cnt; ++t) {
+          s0 += pa[t];
+          s1 += pc[t];
         }
-      }
-  out[0] = s0;
-  if (c) out[out_stride] = s1;
+      else
+        for (int t = 0; t < cnt; ++t) s0 += pa[t];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    out[0] = s0;
+    if (c) out[out_stride] = s1;
+  }
 }
 
 __global__ void k_cg_scalars(int op, const double* __restrict__ rs, int R, const int* __restrict__ ranks, int nr,
@@ -1767,7 +1786,7 @@ int launch_reduce_partials(const double* part, int nblk, int nslots, long long s
 
 int launch_fold_dot(const BoxGeo& g, const double* a, const double* b, const double* c, double* out,
                     long long out_stride, cudaStream_t s) {
-  k_fold_dot<<<1, 32, 0, s>>>(g, a, b, c, out, out_stride);
+  k_fold_dot<<<1, 1024, 0, s>>>(g, a, b, c, out, out_stride);
   return 1;
 }
 

@@ -1,0 +1,82 @@
+"""Run-to-run determinism of the sm_100a path (performance build).
+
+Every reduction is a fixed tree (block partials -> per-box sums -> rank-ordered sum), every launch
+geometry is a pure function of the grid, and all setup work (buffer zeroing, uploads, coefficient
+planes, Galerkin rows, Chebyshev estimates) is ordered on the library's stream. Repeated solves
+in one process, a freshly set-up solver, and a solve in a second process must therefore agree bit
+for bit: x, the residual history and the iteration count.
+"""
+import hashlib
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from paper_1604_07163_b200 import tmgx as T
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+CASES = {
+    "cfg1": ((65, 65, 65), 5, 2, T.POISSON7, False),
+    "varcoef": ((65, 65, 33), 5, 2, T.VARCOEF7_HARMONIC, False),
+    "varcoef_m3": ((33, 33, 33), 4, 3, T.VARCOEF7_HARMONIC, False),
+    "galerkin129": ((129, 129, 129), 6, 3, T.VARCOEF7_HARMONIC, True),
+}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def gpu():
+    try:
+        import torch
+
+        if not torch.cuda.is_available():
+            pytest.skip("no CUDA device")
+    except ImportError:
+        pytest.skip("torch missing")
+
+
+def _solve(name, solver=None):
+    np3, nl, m, kind, gal = CASES[name]
+    if solver is None:
+        w = T.World(1)
+        solver = (w, T.SolverNode(w, T.Problem(np3, kind), T.MGConfig(nl, m, T.EST_LANCZOS, galerkin=gal)))
+    s = solver[1]
+    b = s.rhs(1234)
+    x, rep = s.solve(b, cfg=T.KrylovConfig("cg", rtol=1e-8, initial_guess_nonzero=False))
+    assert rep.converged()
+    return solver, x, rep
+
+
+def _digest(x, rep):
+    h = hashlib.sha256(np.ascontiguousarray(x).tobytes())
+    h.update(np.ascontiguousarray(rep.residual_history).tobytes())
+    return f"{rep.iterations}:{h.hexdigest()}"
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_repeat_solves_bitwise(name):
+    solver, x0, r0 = _solve(name)
+    for _ in range(4):
+        _, x, r = _solve(name, solver)
+        assert r.iterations == r0.iterations
+        assert np.array_equal(r.residual_history, r0.residual_history)
+        assert np.array_equal(x, x0)
+    # a second, freshly set up solver (setup ordering: zeroed buffers, coefficient planes,
+    # Galerkin rows, estimates) gives the same bits
+    _, x1, r1 = _solve(name)
+    assert _digest(x1, r1) == _digest(x0, r0)
+
+
+def test_cross_process_bitwise():
+    names = ["cfg1", "varcoef"]
+    code = ("import json,sys; sys.path[:0] = [%r, %r]; import test_gpu_determinism as D; "
+            "print(json.dumps({n: D._digest(*D._solve(n)[1:]) for n in %r}))" % (ROOT, os.path.join(ROOT, "tests"), names))
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=ROOT, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    other = json.loads(out.stdout.strip().splitlines()[-1])
+    for n in names:
+        assert other[n] == _digest(*_solve(n)[1:]), n
