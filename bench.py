@@ -272,12 +272,12 @@ def main():
         return
     est = T.EST_LANCZOS if args.est == "lanczos" else T.EST_REFERENCE
 
-    nccl_id = None
-    if world > 1:
-        obj = [T.nccl_unique_id() if rank == 0 else None]
+    job = None
+    if world > 1:  # node-local rendezvous name for the peer-memory transport
+        obj = [T.job_token() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
-    w = T.World(n_ranks=world, nproc=world, proc=rank, device=local, nccl_id=nccl_id)
+        job = obj[0]
+    w = T.World(n_ranks=world, nproc=world, proc=rank, device=local, job=job)
     tele = [T.TelescopeStage(tele_level, world)] if (world > 1 and tele_level is not None) else []
     t0 = time.perf_counter()
     galerkin = GALERKIN.get(args.config, False) if args.galerkin is None else args.galerkin == "on"

@@ -7,13 +7,15 @@
  * binding a reference maintainer would add.
  *
  * Process model: spawn_world (comm.hpp:176-207) ran R rank threads in one process.
- * Here R reference ranks (grid boxes) are spread over P processes, one GPU each
- * (P == R: one box per GPU, NCCL over NVLink) or P == 1 (all R boxes on one GPU,
- * used to exercise decompositions on a single device). Every call below that the
- * reference made collectively is collective over the P processes.
+ * Here R reference ranks (grid boxes) are spread over P processes of one node, one GPU
+ * each in production (P == R: one box per GPU; several processes may also share a GPU).
+ * Processes exchange data by storing into each other's CUDA-IPC-mapped mailboxes (peer
+ * memory over NVLink / NVSwitch) and synchronise through stream-ordered host barriers on
+ * a shared-memory segment named by the job token. P == 1 runs all R boxes on one GPU.
+ * Every call below that the reference made collectively is collective over the P processes.
  *
  * Status codes: 0 ok, 1 configuration error (tmg::ConfigError),
- * 2 diverged (SolveReport reason), 3 CUDA/NCCL error, 4 internal/usage error (tmg::Error).
+ * 2 diverged (SolveReport reason), 3 CUDA / transport error, 4 internal/usage error (tmg::Error).
  * tmgx_last_error() returns the message of the last failure on the calling thread.
  */
 #ifndef TMGX_H
@@ -34,7 +36,7 @@ extern "C" {
 
 #define TMGX_MAX_AXIS_PARTS 64
 #define TMGX_MAX_TELESCOPE 4
-#define TMGX_NCCL_ID_BYTES 128
+#define TMGX_JOB_TOKEN_BYTES 33
 
 /* GridHeader (grid.hpp:41-79): rank-independent grid description. */
 typedef struct {
@@ -78,18 +80,21 @@ int tmgx_permutation(const tmgx_header *old_h, const tmgx_header *new_h, int64_t
 typedef struct tmgx_world_s *tmgx_world;
 typedef struct tmgx_solver_s *tmgx_solver;
 
-/* Writes an NCCL unique id (call on process 0, broadcast the bytes to the others). */
-int tmgx_nccl_unique_id(void *out_id /* TMGX_NCCL_ID_BYTES */);
-/* n_ranks reference ranks over nproc processes; process `proc` owns ranks
- * [proc*n_ranks/nproc, (proc+1)*n_ranks/nproc). nccl_id ignored when nproc == 1. */
-int tmgx_world_create(int n_ranks, int nproc, int proc, int device, const void *nccl_id, tmgx_world *out);
+/* Writes a fresh random job token (32 hex chars + NUL; call on one process and hand the string
+ * to the others, e.g. through the launcher's environment or an MPI/torch broadcast). */
+int tmgx_job_token(char *out /* TMGX_JOB_TOKEN_BYTES */);
+/* spawn_world (comm.hpp:176-207): n_ranks reference ranks over nproc processes of one node;
+ * process `proc` owns ranks [proc*n_ranks/nproc, (proc+1)*n_ranks/nproc) and drives CUDA
+ * device `device`. job: the node-local rendezvous name shared by the nproc processes (ignored
+ * when nproc == 1). Collective over the processes. */
+int tmgx_world_create(int n_ranks, int nproc, int proc, int device, const char *job, tmgx_world *out);
 int tmgx_world_destroy(tmgx_world w);
 /* First and one-past-last reference rank owned by this process. */
 int tmgx_world_local_ranks(tmgx_world w, int *first, int *end);
 
 enum { TMGX_POISSON7 = 0, TMGX_VARCOEF7_HARMONIC = 1 };
 enum { TMGX_EST_REFERENCE = 0, TMGX_EST_LANCZOS = 1 };
-enum { TMGX_KSP_CG = 2, TMGX_KSP_PREONLY = 5 }; /* KrylovMethod (solver.hpp:637) */
+enum { TMGX_KSP_CG = 2, TMGX_KSP_PREONLY = 5 }; /* KrylovMethod (solver.hpp:19) */
 enum { TMGX_RTOL = 0, TMGX_ATOL = 1, TMGX_MAX_ITS = 2, TMGX_FIXED_ITS_DONE = 3, TMGX_REASON_DIVERGED = 4 };
 
 /* assemble_problem (reference problems.cpp is missing): 7-point FD operator
@@ -263,6 +268,16 @@ int tmgx_telescope_timing(tmgx_solver s, int stage, int reps, double *t_setup_s,
  * multi-process consistency tests (every send must match the peer's receive). */
 int tmgx_plan_summary(int n_ranks, int nproc, int proc, const tmgx_problem *prob, const tmgx_mg_cfg *mg,
                       int64_t *records, int max_records, int *n_records);
+
+/* Host-only (no GPU): the node-local process group the multi-process World synchronises with
+ * (shared-memory barrier + allgather). Process `proc` of `nproc` joins `job`, allgathers its
+ * index, then runs `rounds` barriers, each followed by a check of a shared round counter.
+ * out[0] = sum of the gathered indices, out[1] = rounds completed consistently. Used by the CPU
+ * multi-process transport tests. */
+int tmgx_node_selftest(const char *job, int nproc, int proc, int rounds, int64_t out[2]);
+/* Timing of one cross-box exchange (halo of `level`, `reps` times; collective): mean device
+ * microseconds per exchange (pack + publishing barrier + unpack) and bytes moved per process. */
+int tmgx_exchange_timing(tmgx_solver s, int level, int reps, double *us_per_exchange, int64_t *bytes_per_exchange);
 
 /* Kernel micro-timing for the roofline (bench.py): launches kernel `which` on `level` `iters`
  * times back to back on the library stream between CUDA events. Outputs the mean device time

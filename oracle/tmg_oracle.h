@@ -97,7 +97,7 @@ int orc_estimate(const orc_mg *mg, int level, int mode, double *lo, double *hi);
 double orc_dot(int64_t n, const double *x, const double *y);          /* dist_vector.cpp:33-38 */
 
 typedef struct {
-  int reason;        /* 0 rtol 1 atol 2 max_its 3 fixed 4 diverged (solver.hpp:642) */
+  int reason;        /* 0 rtol 1 atol 2 max_its 3 fixed 4 diverged (solver.hpp:24) */
   int iterations;
   double norm0;
   double norm_final;

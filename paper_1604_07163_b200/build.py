@@ -16,21 +16,9 @@ from concurrent.futures import ThreadPoolExecutor
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = ["tmg_grid.cpp", "tmg_options.cpp", "tmgx_kernels.cu", "tmgx_engine.cu", "tmgx_elast.cu", "tmgx_capi.cu"]
+SOURCES = ["tmg_grid.cpp", "tmg_options.cpp", "tmgx_node.cpp", "tmgx_kernels.cu", "tmgx_engine.cu", "tmgx_elast.cu",
+           "tmgx_capi.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-
-
-def nccl_dirs():
-    try:
-        import nvidia.nccl as nn  # torch-bundled NCCL (same one torch.distributed loads)
-
-        base = list(nn.__path__)[0]
-        inc, lib = os.path.join(base, "include"), os.path.join(base, "lib")
-        if os.path.exists(os.path.join(inc, "nccl.h")):
-            return inc, lib
-    except Exception:
-        pass
-    return "/usr/include", "/usr/lib/x86_64-linux-gnu"
 
 
 def lib_path(parity=False):
@@ -45,14 +33,13 @@ def _stale(target, deps):
 
 
 def build(parity=False, verbose=False, force=False):
-    inc, lib = nccl_dirs()
     tag = "parity" if parity else "perf"
     objdir = os.path.join(HERE, "build", tag)
     os.makedirs(objdir, exist_ok=True)
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".hpp", ".cuh", ".h"))]
     headers.append(os.path.join(ROOT, "include", "tmgx.h"))
     flags = ARCH + ["-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC,-ffp-contract=off",
-                    "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc, "-Xptxas", "-v"]
+                    "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-Xptxas", "-v"]
     if parity:
         flags += ["-fmad=false", "-DTMGX_PARITY"]
     flags += os.environ.get("TMGX_NVCC_EXTRA", "").split()  # tuning experiments (e.g. -DTMGX_TB_PF=6)
@@ -84,8 +71,7 @@ def build(parity=False, verbose=False, force=False):
             sys.stdout.write(lg)
     out = lib_path(parity)
     if force or cmds or _stale(out, objs):
-        run(["nvcc"] + ARCH + ["-shared", "-o", out] + objs +
-            ["-L", lib, "-l:libnccl.so.2", "-Xlinker", "-rpath," + lib, "-cudart", "static"])
+        run(["nvcc"] + ARCH + ["-shared", "-o", out] + objs + ["-lrt", "-cudart", "static"])
     return out
 
 

@@ -1,5 +1,6 @@
 // extern "C" boundary (include/tmgx.h) over the C++ host layer. Exceptions become status codes:
 // tmg::ConfigError -> 1, tmg::CudaError -> 3, any other failure -> 4.
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -223,20 +224,25 @@ int tmgx_permutation(const tmgx_header* oh, const tmgx_header* nh, int64_t rb, i
   });
 }
 
-int tmgx_nccl_unique_id(void* out) {
+int tmgx_job_token(char* out) {
   return guard([&] {
-    ncclUniqueId id;
-    tmgx::nccl_check(ncclGetUniqueId(&id), "ncclGetUniqueId");
-    std::memcpy(out, &id, sizeof(id));
+    unsigned char r[16];
+    FILE* f = std::fopen("/dev/urandom", "rb");
+    if (!f || std::fread(r, 1, sizeof r, f) != sizeof r) {
+      if (f) std::fclose(f);
+      throw tmg::Error("job token: /dev/urandom unavailable");
+    }
+    std::fclose(f);
+    for (int i = 0; i < 16; ++i) std::snprintf(out + 2 * i, 3, "%02x", r[i]);
     return 0;
   });
 }
 
-int tmgx_world_create(int n_ranks, int nproc, int proc, int device, const void* nccl_id, tmgx_world* out) {
+int tmgx_world_create(int n_ranks, int nproc, int proc, int device, const char* job, tmgx_world* out) {
   return guard([&] {
     auto w = new tmgx_world_s;
     try {
-      w->w = std::make_unique<tmgx::World>(n_ranks, nproc, proc, device, nccl_id);
+      w->w = std::make_unique<tmgx::World>(n_ranks, nproc, proc, device, job);
     } catch (...) {
       delete w;
       throw;
@@ -745,6 +751,55 @@ int tmgx_plan_summary(int n_ranks, int nproc, int proc, const tmgx_problem* p, c
       }
     }
     *n_records = n;
+    return 0;
+  });
+}
+
+int tmgx_node_selftest(const char* job, int nproc, int proc, int rounds, int64_t out[2]) {
+  return guard([&] {
+    tmgx::NodeGroup g(job, nproc, proc);
+    const std::string mine(reinterpret_cast<const char*>(&proc), sizeof proc);
+    long long sum = 0;
+    for (const std::string& v : g.allgather(mine)) {
+      int q;
+      std::memcpy(&q, v.data(), sizeof q);
+      sum += q;
+    }
+    // every round: all processes see the same round number on the board before anyone moves on
+    long long ok = 0;
+    for (int r = 0; r < rounds; ++r) {
+      const std::string tag(reinterpret_cast<const char*>(&r), sizeof r);
+      bool same = true;
+      for (const std::string& v : g.allgather(tag)) same = same && v == tag;
+      ok += same ? 1 : 0;
+      g.barrier();
+    }
+    out[0] = sum;
+    out[1] = ok;
+    return 0;
+  });
+}
+
+int tmgx_exchange_timing(tmgx_solver s, int level, int reps, double* us, int64_t* bytes) {
+  return guard([&] {
+    auto& S = *s->s;
+    const int i = check_level(s, level);
+    tmgx::Node& nd = S.nodes[i];
+    if (reps < 1) throw tmg::ConfigError("reps must be >= 1");
+    S.halo(i, nd.x);  // warm-up
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, S.W.stream);
+    for (int r = 0; r < reps; ++r) S.halo(i, nd.x);
+    cudaEventRecord(e1, S.W.stream);
+    S.sync();
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *us = 1e3 * ms / reps;
+    *bytes = 8 * nd.halo.send_total;
     return 0;
   });
 }

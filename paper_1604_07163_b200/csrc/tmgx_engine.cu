@@ -12,9 +12,6 @@ namespace tmgx {
 void cuda_check(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw tmg::CudaError(std::string(what) + ": " + cudaGetErrorString(e));
 }
-void nccl_check(ncclResult_t e, const char* what) {
-  if (e != ncclSuccess) throw tmg::CudaError(std::string(what) + ": " + ncclGetErrorString(e));
-}
 #define CK(x) cuda_check((x), #x)
 
 // ------------------------------------------------------------------------------------------
@@ -28,20 +25,27 @@ Owners::Owners(int R_, int P_, int me_) : R(R_), P(P_), me(me_) {
   end = (int)((long long)(me + 1) * R / P);
 }
 
-World::World(int R_, int P_, int me_, int device_, const void* nccl_id) : Owners(R_, P_, me_), device(device_) {
+World::World(int R_, int P_, int me_, int device_, const char* job) : Owners(R_, P_, me_), device(device_) {
   CK(cudaSetDevice(device));
   CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
   if (P > 1) {
-    if (!nccl_id) throw tmg::ConfigError("world: nproc > 1 needs an NCCL unique id");
-    ncclUniqueId id;
-    std::memcpy(&id, nccl_id, sizeof(id));
-    nccl_check(ncclCommInitRank(&nccl, P, id, me), "ncclCommInitRank");
+    if (!job || !*job) throw tmg::ConfigError("world: nproc > 1 needs a job token (the node-local rendezvous name)");
+    grp = std::make_unique<NodeGroup>(job, P, me);
   }
 }
 
 World::~World() {
-  if (nccl) ncclCommDestroy(nccl);
+  grp.reset();
   if (stream) cudaStreamDestroy(stream);
+}
+
+void World::stream_barrier() {
+  grp->enqueue_barrier(stream);
+  ++nbar;
+}
+
+void World::check() const {
+  if (grp && grp->failed()) throw tmg::CudaError("world: a stream barrier timed out or a peer process aborted");
 }
 
 int Owners::owner(int wr) const {
@@ -229,6 +233,7 @@ PlanHost plan_host(const Owners& W, const Dist& S, const Dist& T, RegionFn regio
         d.dst_pxy = (long long)d.nx * d.ny;
         soff[ot] += n;
         plan.pack.push_back(d);
+        plan.pack_peer.push_back(ot);
         plan.max_pack = std::max<long long>(plan.max_pack, n);
         auto& cs = plan.send_sum[sidx[ot]];
         cs = cs * 31 + region_sum(reg, T.h);
@@ -258,15 +263,17 @@ RegionPlan upload_plan(DeviceArena& A, const PlanHost& h) {
     A.upload(dst, v.data(), sizeof(CopyDesc) * v.size());
   };
   up(h.loc, plan.d_local, plan.n_local);
-  up(h.pack, plan.d_pack, plan.n_pack);
+  up(h.pack, plan.d_pack, plan.n_pack);  // rewired to peer mailboxes by Solver::wire_transport
   up(h.unpack, plan.d_unpack, plan.n_unpack);
   plan.max_local = h.max_local;
   plan.max_pack = h.max_pack;
   plan.max_unpack = h.max_unpack;
   plan.sends = h.sends;
   plan.recvs = h.recvs;
-  if (h.send_total) plan.sendbuf = A.alloc(h.send_total);
-  if (h.recv_total) plan.recvbuf = A.alloc(h.recv_total);
+  plan.send_total = h.send_total;
+  plan.recv_total = h.recv_total;
+  plan.pack_h = h.pack;
+  plan.pack_peer = h.pack_peer;
   return plan;
 }
 
@@ -295,22 +302,23 @@ PlanHost transfer_plan_host(const Owners& W, const Dist& S, const Dist& T) {
   });
 }
 
-void run_plan(World& W, const RegionPlan& plan, const Field& src, const Field& dst, bool telescope) {
+// One use of a plan. Cross-process regions: pack straight into the peers' mailboxes, one stream
+// barrier publishes them, unpack from this process's mailbox. A plan reused with no barrier since
+// its previous use first waits for the peers to have unpacked that use (write-after-read).
+void run_plan(World& W, RegionPlan& plan, const Field& src, const Field& dst, bool telescope) {
   const PtrTable ts = src.table(), td = dst.table();
-  if (plan.n_pack) W.cnt.launches += launch_region_copy(plan.d_pack, plan.n_pack, plan.max_pack, ts, td, nullptr,
-                                                        plan.sendbuf, W.stream);
-  if (!plan.sends.empty() || !plan.recvs.empty()) {
-    nccl_check(ncclGroupStart(), "ncclGroupStart");
-    for (const auto& p : plan.sends) {
-      nccl_check(ncclSend(plan.sendbuf + p.off, (size_t)p.count, ncclDouble, p.proc, W.nccl, W.stream), "ncclSend");
-      (telescope ? W.cnt.tele_bytes : W.cnt.halo_bytes) += p.count * 8;
-    }
-    for (const auto& p : plan.recvs)
-      nccl_check(ncclRecv(plan.recvbuf + p.off, (size_t)p.count, ncclDouble, p.proc, W.nccl, W.stream), "ncclRecv");
-    nccl_check(ncclGroupEnd(), "ncclGroupEnd");
+  const bool xp = plan.xproc && W.P > 1;
+  if (xp && plan.last_bar == W.nbar) W.stream_barrier();
+  if (plan.n_pack) {
+    W.cnt.launches += launch_region_copy(plan.d_pack, plan.n_pack, plan.max_pack, ts, td, nullptr, nullptr, W.stream);
+    (telescope ? W.cnt.tele_bytes : W.cnt.halo_bytes) += plan.send_total * 8;
   }
   if (plan.n_local)
     W.cnt.launches += launch_region_copy(plan.d_local, plan.n_local, plan.max_local, ts, td, nullptr, nullptr, W.stream);
+  if (xp) {
+    W.stream_barrier();
+    plan.last_bar = W.nbar;
+  }
   if (plan.n_unpack)
     W.cnt.launches += launch_region_copy(plan.d_unpack, plan.n_unpack, plan.max_unpack, ts, td, plan.recvbuf, nullptr,
                                          W.stream);
@@ -524,12 +532,19 @@ void Solver::build_nodes() {
       const auto t0 = std::chrono::steady_clock::now();
       nodes[i].gather = upload_plan(arena, transfer_plan_host(W, *nodes[i].dist, *nodes[i + 1].dist));
       nodes[i].scatter = upload_plan(arena, transfer_plan_host(W, *nodes[i + 1].dist, *nodes[i].dist));
-      CK(cudaStreamSynchronize(W.stream));
+      sync();
       nodes[i].t_setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     }
   part = arena.alloc((long long)nloc_max * 2 * nblk_max);
   for (int q = 0; q < nloc_max; ++q) part_off.push_back((long long)q * 2 * nblk_max);
-  rank_sums = arena.alloc(2LL * W.R);
+  for (Node& nd : nodes) {  // creation order, identical on every process
+    plans.push_back(&nd.halo);
+    if (nd.kind == TELESCOPE) {
+      plans.push_back(&nd.gather);
+      plans.push_back(&nd.scatter);
+    }
+  }
+  wire_transport();  // allocates rank_sums (+ the IPC mailbox when P > 1)
   scal = arena.alloc(S_NSLOTS);
   CK(cudaMallocHost(&host_scal, sizeof(double) * (S_NSLOTS + 2 * W.R + 8)));
   staging = arena.alloc(staging_n);
@@ -540,7 +555,7 @@ void Solver::build_nodes() {
   }
   if (mgd.galerkin) build_galerkin();
   setup_coarse(nodes.back());
-  CK(cudaStreamSynchronize(W.stream));
+  sync();
 
   // Chebyshev intervals: given, or estimated (SolverNode::create, solver.cpp:591-592)
   for (size_t i = 0; i < nodes.size(); ++i) {
@@ -553,7 +568,100 @@ void Solver::build_nodes() {
       estimate((int)i, mgd.est_mode);
     }
   }
-  CK(cudaStreamSynchronize(W.stream));
+  sync();
+}
+
+// Cross-process wiring (P > 1): one mailbox allocation per process holds the rank_sums slots
+// and every plan's receive area; its CUDA IPC handle and the per-plan segment offsets are
+// allgathered once, after which each pack descriptor points straight at its segment in the
+// receiving process's mailbox. Single process: rank_sums only, no mailbox.
+namespace {
+struct Pub {
+  cudaIpcMemHandle_t handle;
+  int nplans;
+};
+void put(std::string& s, const void* p, size_t n) { s.append(static_cast<const char*>(p), n); }
+template <class T>
+T take(const std::string& s, size_t& at) {
+  T v;
+  std::memcpy(&v, s.data() + at, sizeof(T));
+  at += sizeof(T);
+  return v;
+}
+}  // namespace
+
+void Solver::wire_transport() {
+  if (W.P == 1) {
+    rank_sums = arena.alloc(2LL * W.R);
+    return;
+  }
+  long long off = 2LL * W.R;
+  for (RegionPlan* p : plans) {
+    p->mb_off = off;
+    off += p->recv_total;
+  }
+  mailbox = arena.alloc(off);
+  sync();
+  rank_sums = mailbox;
+  for (RegionPlan* p : plans) p->recvbuf = p->recv_total ? mailbox + p->mb_off : nullptr;
+  // publication: handle, then per plan {send_total, nrecvs, (src proc, segment offset)...}
+  std::string mine;
+  Pub pub{};
+  CK(cudaIpcGetMemHandle(&pub.handle, mailbox));
+  pub.nplans = (int)plans.size();
+  put(mine, &pub, sizeof pub);
+  for (RegionPlan* p : plans) {
+    const long long st = p->send_total;
+    const int nr = (int)p->recvs.size();
+    put(mine, &st, sizeof st);
+    put(mine, &nr, sizeof nr);
+    for (const auto& r : p->recvs) {
+      const long long seg = p->mb_off + r.off;
+      put(mine, &r.proc, sizeof r.proc);
+      put(mine, &seg, sizeof seg);
+    }
+  }
+  const std::vector<std::string> all = W.grp->allgather(mine);
+  peer_mail.assign((size_t)W.P, nullptr);
+  // seg[q][k][src] = offset of src's segment in q's mailbox for plan k
+  std::vector<std::vector<std::vector<long long>>> seg((size_t)W.P);
+  std::vector<char> xproc(plans.size(), 0);
+  for (int q = 0; q < W.P; ++q) {
+    size_t at = 0;
+    const Pub pq = take<Pub>(all[(size_t)q], at);
+    if (pq.nplans != (int)plans.size()) throw tmg::Error("transport: processes built different plan lists");
+    seg[(size_t)q].assign(plans.size(), std::vector<long long>((size_t)W.P, -1));
+    for (size_t k = 0; k < plans.size(); ++k) {
+      const long long st = take<long long>(all[(size_t)q], at);
+      const int nr = take<int>(all[(size_t)q], at);
+      if (st > 0) xproc[k] = 1;
+      for (int j = 0; j < nr; ++j) {
+        const int src = take<int>(all[(size_t)q], at);
+        seg[(size_t)q][k][(size_t)src] = take<long long>(all[(size_t)q], at);
+      }
+    }
+    if (q != W.me) {
+      void* ptr = nullptr;
+      CK(cudaIpcOpenMemHandle(&ptr, pq.handle, cudaIpcMemLazyEnablePeerAccess));
+      peer_mail[(size_t)q] = static_cast<double*>(ptr);
+    }
+  }
+  for (size_t k = 0; k < plans.size(); ++k) {
+    RegionPlan& p = *plans[k];
+    p.xproc = xproc[k] != 0;
+    if (!p.n_pack) continue;
+    std::vector<long long> start((size_t)W.P, 0);
+    for (const auto& sd : p.sends) start[(size_t)sd.proc] = sd.off;
+    for (size_t d = 0; d < p.pack_h.size(); ++d) {
+      const int q = p.pack_peer[d];
+      const long long sg = seg[(size_t)q][k][(size_t)W.me];
+      if (sg < 0) throw tmg::Error("transport: receiver has no segment for this sender");
+      p.pack_h[d].dst_abs = peer_mail[(size_t)q] + sg;
+      p.pack_h[d].dst_off -= start[(size_t)q];
+    }
+    arena.upload(p.d_pack, p.pack_h.data(), sizeof(CopyDesc) * p.pack_h.size());
+  }
+  W.grp->barrier();
 }
 
 // Galerkin coarse operators (mg_setup with galerkin; ptap dist_matrix.cpp:462-468):
@@ -587,7 +695,7 @@ void Solver::build_galerkin() {
       nd.op[q].S_stride = D.geo[q].total;
     }
   }
-  CK(cudaStreamSynchronize(W.stream));
+  sync();
 }
 
 // LUPC (precond.cpp:220-229): dense LU of the coarse operator, factored on the host with
@@ -664,7 +772,7 @@ void Solver::setup_coarse(Node& nd) {
   if (!nd.S.p.empty()) {  // 27-point Galerkin rows from the device
     std::vector<double> S((size_t)27 * g.total);
     CK(cudaMemcpyAsync(S.data(), nd.S.p[0], sizeof(double) * S.size(), cudaMemcpyDeviceToHost, W.stream));
-    CK(cudaStreamSynchronize(W.stream));
+    sync();
     for (int k = 0; k < nz; ++k)
       for (int j = 0; j < ny; ++j)
         for (int i = 0; i < nx; ++i) {
@@ -876,12 +984,31 @@ bool Solver::use_tb(int i) const {
          nd.op[0].S == nullptr && cheb2_tb_supported(nd.dist->geo[0]) && nd.dist->geo[0].ex >= tb_min_extent;
 }
 
+// Cross-process scalar reduction: every process stores its rank slots into every peer's
+// rank_sums, then one stream barrier; each process then sums the slots in rank order itself
+// (identical on all processes, and identical to the single-process sum).
 void Solver::device_allreduce_ranksums(int nslots) {
-  if (W.P > 1) {
-    nccl_check(ncclAllReduce(rank_sums, rank_sums, (size_t)nslots * W.R, ncclDouble, ncclSum, W.nccl, W.stream),
-               "ncclAllReduce");
-    W.cnt.allreduces++;
-  }
+  if (W.P == 1) return;
+  if (rs_last_bar == W.nbar) W.stream_barrier();  // peers done reading the previous values
+  PtrTable peers{};
+  int np = 0;
+  for (int q = 0; q < W.P; ++q)
+    if (q != W.me) peers.p[np++] = peer_mail[(size_t)q];
+  W.cnt.launches += launch_push_ranksums(rank_sums, W.R, nslots, W.first, W.end, peers, np, W.stream);
+  W.stream_barrier();
+  rs_last_bar = W.nbar;
+  W.cnt.allreduces++;
+}
+
+// Single process: clear the slots (only the listed ranks' slots are ever summed). With peers
+// storing into this buffer concurrently, clearing would race; every summed slot is rewritten.
+void Solver::sync() {
+  CK(cudaStreamSynchronize(W.stream));
+  W.check();
+}
+
+void Solver::zero_ranksums() {
+  if (W.P == 1) CK(cudaMemsetAsync(rank_sums, 0, sizeof(double) * 2 * W.R, W.stream));
 }
 
 // Deterministic collective sums for node i's distribution: per-box block partials are reduced
@@ -901,11 +1028,11 @@ void Solver::reduce_local(const Dist& D, int nslots, const Field* a, const Field
 
 std::array<double, 2> Solver::collect2(int i, int nslots, const Field* a, const Field* b) {
   const Dist& D = *nodes[i].dist;
-  CK(cudaMemsetAsync(rank_sums, 0, sizeof(double) * 2 * W.R, W.stream));
+  zero_ranksums();
   reduce_local(D, nslots, a, b, nullptr);
   device_allreduce_ranksums(nslots);
   CK(cudaMemcpyAsync(host_scal, rank_sums, sizeof(double) * 2 * W.R, cudaMemcpyDeviceToHost, W.stream));
-  CK(cudaStreamSynchronize(W.stream));
+  sync();
   std::array<double, 2> s{0.0, 0.0};
   for (int m = 0; m < D.h.n_ranks(); ++m) {
     s[0] += host_scal[D.wr[m]];
@@ -984,7 +1111,7 @@ void Solver::estimate(int i, int mode) {
       *hb = beta;
       CK(cudaMemcpyAsync(scal + S_TMP0, hb, sizeof(double), cudaMemcpyHostToDevice, W.stream));
       for (size_t q = 0; q < nb; ++q) W.cnt.launches += launch_p_update(D.geo[q], z.p[q], p.p[q], scal, S_TMP0, W.stream);
-      CK(cudaStreamSynchronize(W.stream));
+      sync();
     }
   }
   if (broke || alphas.empty()) {
@@ -1021,7 +1148,7 @@ void Solver::upload(int i, const Field& f, const double* src, bool on_device) {
       s = staging;
     }
     W.cnt.launches += launch_compact_to_box(g, s, f.p[q], W.stream);
-    if (!on_device) CK(cudaStreamSynchronize(W.stream));
+    if (!on_device) sync();
     off += n;
   }
 }
@@ -1037,7 +1164,7 @@ void Solver::download(int i, const Field& f, double* dst, bool on_device) {
     } else {
       W.cnt.launches += launch_box_to_compact(g, f.p[q], staging, W.stream);
       CK(cudaMemcpyAsync(dst + off, staging, sizeof(double) * n, cudaMemcpyDeviceToHost, W.stream));
-      CK(cudaStreamSynchronize(W.stream));
+      sync();
     }
     off += n;
   }
@@ -1049,7 +1176,7 @@ void Solver::download(int i, const Field& f, double* dst, bool on_device) {
 // stopping test ||z_k|| <= max(rtol ||z_0||, atol) (solver.cpp:71-77).
 void Solver::cg_dots(int op) {
   const Dist& D = *nodes[0].dist;
-  CK(cudaMemsetAsync(rank_sums, 0, sizeof(double) * 2 * W.R, W.stream));
+  zero_ranksums();
   const int fused = parity_build() ? 0 : dots_nblk;  // r.z, z.z partials from the finest post-smooth
   if (!parity_build() && !fused)
     for (size_t q = 0; q < D.local.size(); ++q)
@@ -1073,7 +1200,7 @@ void Solver::cg_iteration(int par) {
   const size_t nb = D.local.size();
   const bool fused = fused_cg();
   Field& pn = (fused && par == 0) ? cp2 : cp;  // direction written this iteration
-  CK(cudaMemsetAsync(rank_sums, 0, sizeof(double) * 2 * W.R, W.stream));
+  zero_ranksums();
   if (fused) {
     const Field& po = par == 0 ? cp : cp2;
     W.cnt.launches += launch_pspmv_dot(D.geo[0], top.op[0], cz.p[0], po.p[0], pn.p[0], cw.p[0], part + part_off[0],
@@ -1103,7 +1230,7 @@ void Solver::run_iteration(int par) {
     return;
   }
   if (!iter_exec[par]) {
-    const long long l0 = W.cnt.launches;
+    const long long l0 = W.cnt.launches, b0 = W.nbar;
     cudaGraph_t g;
     CK(cudaStreamBeginCapture(W.stream, cudaStreamCaptureModeThreadLocal));
     cg_iteration(par);
@@ -1111,10 +1238,23 @@ void Solver::run_iteration(int par) {
     CK(cudaGraphInstantiate(&iter_exec[par], g, 0));
     CK(cudaGraphDestroy(g));
     iter_launches = W.cnt.launches - l0;
+    iter_bars = W.nbar - b0;  // stream barriers (host nodes) in one iteration
     W.cnt.launches = l0;
+    W.nbar = b0;
+    graph_base = b0;
   }
+  // Host barrier bookkeeping of a replay: the plans used in the graph last published at
+  // (previous start + their offset inside the iteration); move them to this replay's start.
+  const long long shift = W.nbar - graph_base;
+  if (shift) {
+    for (RegionPlan* p : plans)
+      if (p->last_bar > graph_base) p->last_bar += shift;
+    if (rs_last_bar > graph_base) rs_last_bar += shift;
+  }
+  graph_base = W.nbar;
   CK(cudaGraphLaunch(iter_exec[par], W.stream));
   W.cnt.launches += iter_launches;
+  W.nbar += iter_bars;
 }
 
 // Device inputs (tmgx.h stream contract): the library's stream waits for all work submitted so far
@@ -1127,6 +1267,15 @@ void Solver::order_after_caller() {
 }
 
 Solver::~Solver() {
+  if (W.grp) {  // collective teardown: no peer may still store into our mailbox
+    cudaStreamSynchronize(W.stream);
+    try {
+      W.grp->barrier(30.0);
+    } catch (...) {
+    }
+    for (double* p : peer_mail)
+      if (p) cudaIpcCloseMemHandle(p);
+  }
   if (caller_ev) cudaEventDestroy(caller_ev);
   for (auto& e : iter_exec)
     if (e) cudaGraphExecDestroy(e);
@@ -1172,7 +1321,7 @@ int Solver::solve(const double* b, double* x, bool on_device, int method, double
     vcycle(0);
     cg_dots(CG_INIT);  // also sets beta = 0 so that the first p = z + 0 p = z
     CK(cudaMemcpyAsync(host_scal, scal, sizeof(double) * S_NSLOTS, cudaMemcpyDeviceToHost, W.stream));
-    CK(cudaStreamSynchronize(W.stream));
+    sync();
     const double nrm0 = host_scal[S_NRM];
     *norm0 = nrm0;
     *normf = nrm0;
@@ -1187,7 +1336,7 @@ int Solver::solve(const double* b, double* x, bool on_device, int method, double
       }
       for (int it = 1; it <= max_its; ++it) {
         run_iteration((it - 1) & 1);
-        CK(cudaStreamSynchronize(W.stream));
+        sync();
         if (host_scal[S_FLAG_PW] != 0.0) {  // solver.cpp:237-241 (x, r not updated)
           *reason = 4;
           rc = 2;
@@ -1212,6 +1361,7 @@ int Solver::solve(const double* b, double* x, bool on_device, int method, double
   }
   CK(cudaEventRecord(e1, W.stream));
   CK(cudaEventSynchronize(e1));
+  W.check();
   float ms = 0.f;
   cudaEventElapsedTime(&ms, e0, e1);
   *t_ms = ms;

@@ -13,7 +13,6 @@
 #pragma once
 
 #include <cuda_runtime.h>
-#include <nccl.h>
 
 #include <array>
 #include <memory>
@@ -23,11 +22,11 @@
 
 #include "tmg_grid.hpp"
 #include "tmgx_kernels.cuh"
+#include "tmgx_node.hpp"
 
 namespace tmgx {
 
 void cuda_check(cudaError_t e, const char* what);
-void nccl_check(ncclResult_t e, const char* what);
 
 struct Counters {
   long long launches = 0;
@@ -47,14 +46,19 @@ struct Owners {
   bool local(int world_rank) const { return owner(world_rank) == me; }
 };
 
+// R reference ranks over P processes (one GPU each in production; any number sharing a GPU in
+// tests). Processes synchronise only through stream-ordered host barriers (NodeGroup).
 struct World : Owners {
   int device = 0;
   cudaStream_t stream = nullptr;
-  ncclComm_t nccl = nullptr;
+  std::unique_ptr<NodeGroup> grp;  // P > 1
+  long long nbar = 0;              // stream barriers enqueued so far (identical on every process)
   Counters cnt;
 
-  World(int R, int P, int me, int device, const void* nccl_id);
+  World(int R, int P, int me, int device, const char* job);
   ~World();
+  void stream_barrier();  // every process's stream reaches this point before any proceeds
+  void check() const;     // throws if a stream barrier failed (timeout / peer abort)
 };
 
 // A GridHeader over a communicator whose comm rank m is reference rank wr[m].
@@ -103,6 +107,9 @@ void dense_lu_setup(DeviceArena& arena, std::vector<double> a, int n, const std:
                     double** A_dev, long long** piv_dev, long long** map_dev);
 
 // Region copies between two distributions (halo: same dist, box halo incl. corners).
+// Cross-process movement: the pack kernel stores each region straight into the receiving
+// process's mailbox (peer pointer from its CUDA IPC handle), a stream barrier publishes it, and
+// the receiver unpacks from its own mailbox. Same-process regions are one copy kernel.
 struct RegionPlan {
   CopyDesc* d_local = nullptr;
   int n_local = 0, max_local = 0;
@@ -115,8 +122,13 @@ struct RegionPlan {
     long long off, count;
   };
   std::vector<Peer> sends, recvs;
-  double* sendbuf = nullptr;
-  double* recvbuf = nullptr;
+  long long send_total = 0, recv_total = 0;
+  double* recvbuf = nullptr;      // this process's mailbox area of the plan
+  long long mb_off = 0;           // its offset in the mailbox
+  std::vector<CopyDesc> pack_h;   // host copies of the pack descriptors (rewired to peer pointers)
+  std::vector<int> pack_peer;     // destination process of each pack descriptor
+  bool xproc = false;             // some process pair exchanges data (global, same on all)
+  long long last_bar = -1;        // W.nbar right after the last use's publishing barrier
   bool empty() const { return n_local == 0 && sends.empty() && recvs.empty(); }
 };
 
@@ -127,6 +139,7 @@ struct PlanHost {
   std::vector<CopyDesc> loc, pack, unpack;
   std::vector<RegionPlan::Peer> sends, recvs;
   std::vector<unsigned long long> send_sum, recv_sum;  // aligned with sends / recvs
+  std::vector<int> pack_peer;                          // destination process of each pack descriptor
   long long local_count = 0;
   int max_local = 0, max_pack = 0, max_unpack = 0;
   long long send_total = 0, recv_total = 0;
@@ -134,7 +147,7 @@ struct PlanHost {
 PlanHost halo_plan_host(const Owners& W, const Dist& D);
 PlanHost transfer_plan_host(const Owners& W, const Dist& S, const Dist& T);
 RegionPlan upload_plan(DeviceArena& A, const PlanHost& h);
-void run_plan(World& W, const RegionPlan& plan, const Field& src, const Field& dst, bool telescope);
+void run_plan(World& W, RegionPlan& plan, const Field& src, const Field& dst, bool telescope);
 
 struct ProblemDesc {
   int kind = 0;  // 0 POISSON7, 1 VARCOEF7_HARMONIC
@@ -213,7 +226,12 @@ class Solver {
   double* part = nullptr;       // per local box partials [box][2][nblk]
   std::vector<long long> part_off;
   int nblk_max = 0;
-  double* rank_sums = nullptr;  // [2][R] (+ staging)
+  double* rank_sums = nullptr;  // [2][R]; P > 1: the head of this process's IPC mailbox
+  double* mailbox = nullptr;
+  std::vector<double*> peer_mail;  // peers' mailboxes (IPC-mapped), nullptr for this process
+  long long rs_last_bar = -1;
+  std::vector<RegionPlan*> plans;  // every plan in creation order (identical on all processes)
+  void wire_transport();
   double* scal = nullptr;       // S_NSLOTS
   double* host_scal = nullptr;  // pinned
   int* ranks_dev = nullptr;     // comm ranks -> world ranks of the top dist
@@ -236,6 +254,8 @@ class Solver {
   std::array<double, 2> collect2(int i, int nslots, const Field* a, const Field* b);
   void reduce_local(const Dist& D, int nslots, const Field* a, const Field* b, const Field* c, int nblk = 0);
   void device_allreduce_ranksums(int nslots);
+  void zero_ranksums();
+  void sync();  // drain the stream; throws if a cross-process barrier failed
 
   // compact (host or device) <-> field
   void upload(int i, const Field& f, const double* src, bool on_device);
@@ -260,6 +280,7 @@ class Solver {
   ChebStep cheb_first_step(const Node& nd) const;
   cudaGraphExec_t iter_exec[2] = {nullptr, nullptr};  // one captured CG iteration per p parity
   long long iter_launches = 0;
+  long long iter_bars = 0, graph_base = 0;
   void cg_dots(int op);
   void cg_iteration(int par);
   void run_iteration(int par);

@@ -1300,7 +1300,7 @@ __global__ void k_reduce_partials(const double* __restrict__ part, int nblk, lon
 // Parity build: dist_vector.cpp:33-38 + comm.cpp:338-351 on one rank is a serial left fold of
 // the products in local (natural) order. The block forms the products of a chunk in parallel
 // (each product rounds exactly as in the serial loop) and thread 0 folds them in order.
-constexpr int kFoldChunk = 4096;
+constexpr int kFoldChunk = 2048;
 __global__ void __launch_bounds__(1024) k_fold_dot(BoxGeo g, const double* __restrict__ a, const double* __restrict__ b,
                                                    const double* __restrict__ c, double* __restrict__ out,
                                                    long long out_stride) {
@@ -1391,16 +1391,28 @@ __global__ void k_box_compact(BoxGeo g, const double* __restrict__ src, double* 
 __global__ void k_region_copy(const CopyDesc* __restrict__ descs, PtrTable src, PtrTable dst,
                               const double* __restrict__ sbuf, double* __restrict__ dbuf) {
   const CopyDesc d = descs[blockIdx.y];
-  const long long n = (long long)d.nx * d.ny * d.nz;
   const double* s = d.src_slot >= 0 ? src.p[d.src_slot] : sbuf;
-  double* t = d.dst_slot >= 0 ? dst.p[d.dst_slot] : dbuf;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
-    const long long a = e % d.nx;
-    const long long q = e / d.nx;
-    const long long b = q % d.ny;
-    const long long c = q / d.ny;
-    t[d.dst_off + a + b * d.dst_px + c * d.dst_pxy] = s[d.src_off + a + b * d.src_px + c * d.src_pxy];
+  double* t = d.dst_abs ? d.dst_abs : (d.dst_slot >= 0 ? dst.p[d.dst_slot] : dbuf);
+  // one warp per region row (rows are x-contiguous in every layout); 32-bit row arithmetic
+  const int rows = d.ny * d.nz;
+  for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += gridDim.x * (blockDim.x >> 5)) {
+    const int b = r % d.ny, c = r / d.ny;
+    const double* sr = s + d.src_off + b * d.src_px + c * d.src_pxy;
+    double* tr = t + d.dst_off + b * d.dst_px + c * d.dst_pxy;
+    for (int a = threadIdx.x & 31; a < d.nx; a += 32) tr[a] = sr[a];
   }
+  if (d.dst_abs) __threadfence_system();  // peer stores visible before the publishing barrier
+}
+
+__global__ void k_push_ranksums(const double* __restrict__ rs, int R, int nslots, int first, int end, PtrTable peers,
+                                int npeers) {
+  const int nl = end - first;
+  for (int t = threadIdx.x; t < npeers * nslots * nl; t += blockDim.x) {
+    const int q = t / (nslots * nl), rem = t % (nslots * nl);
+    const int slot = rem / nl, r = first + rem % nl;
+    peers.p[q][slot * R + r] = rs[slot * R + r];
+  }
+  __threadfence_system();
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1813,6 +1825,13 @@ int launch_region_copy(const CopyDesc* desc_dev, int ndesc, int max_elems, const
   if (bx > 1024) bx = 1024;
   if (bx < 1) bx = 1;
   k_region_copy<<<dim3(bx, ndesc), 256, 0, s>>>(desc_dev, src, dst, src_buf, dst_buf);
+  return 1;
+}
+
+int launch_push_ranksums(const double* rs, int R, int nslots, int first, int end, const PtrTable& peers, int npeers,
+                         cudaStream_t s) {
+  if (npeers <= 0) return 0;
+  k_push_ranksums<<<1, 256, 0, s>>>(rs, R, nslots, first, end, peers, npeers);
   return 1;
 }
 

@@ -66,6 +66,7 @@ struct CopyDesc {
   long long src_off, dst_off; // element offset of the region origin (or buffer offset)
   int nx, ny, nz;
   long long src_px, src_pxy, dst_px, dst_pxy;  // pitches (packed: nx, nx*ny)
+  double* dst_abs;            // non-null: destination base (a peer process's mailbox segment)
 };
 
 struct PtrTable {
@@ -167,6 +168,11 @@ int launch_compact_to_box(const BoxGeo& g, const double* compact, double* box, c
 // Region copies (halo exchange, telescope gather/scatter, pack/unpack).
 int launch_region_copy(const CopyDesc* desc_dev, int ndesc, int max_elems, const PtrTable& src,
                        const PtrTable& dst, double* src_buf, double* dst_buf, cudaStream_t s);
+
+// Cross-process scalar reduction: store this process's rank slots [first, end) of `nslots`
+// slots (stride R) into every peer's rank_sums (peers.p[0..npeers)).
+int launch_push_ranksums(const double* rs, int R, int nslots, int first, int end, const PtrTable& peers, int npeers,
+                         cudaStream_t s);
 
 // Coarse direct solve: perf build y = Ainv x ; parity build: DenseLU::solve loop order.
 // `map[c]` = padded-box element offset of compact (natural) index c.

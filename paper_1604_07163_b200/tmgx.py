@@ -19,7 +19,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 MAX_AXIS_PARTS = 64
 MAX_TELESCOPE = 4
-NCCL_ID_BYTES = 128
+JOB_TOKEN_BYTES = 33
 
 POISSON7, VARCOEF7_HARMONIC = 0, 1
 EST_REFERENCE, EST_LANCZOS = 0, 1
@@ -37,7 +37,7 @@ class ConfigError(Error):
 
 
 class CudaError(Error):
-    """CUDA / NCCL failure (C-ABI status 3)"""
+    """CUDA / cross-process transport failure (C-ABI status 3)"""
 
 
 # ----------------------------------------------------------------- ctypes structs
@@ -80,12 +80,13 @@ class _Counters(C.Structure):
 EXPORTS = [
     "tmgx_choose_proc_grid", "tmgx_grid_header", "tmgx_coarsen_header", "tmgx_layout_offsets",
     "tmgx_global_to_natural", "tmgx_natural_to_global", "tmgx_split_strided", "tmgx_repartition_header",
-    "tmgx_prefusion_layout", "tmgx_permutation", "tmgx_nccl_unique_id", "tmgx_world_create",
+    "tmgx_prefusion_layout", "tmgx_permutation", "tmgx_job_token", "tmgx_world_create",
     "tmgx_world_destroy", "tmgx_world_local_ranks", "tmgx_solver_create", "tmgx_solver_destroy",
     "tmgx_solver_level_info", "tmgx_solver_bounds", "tmgx_fill_rhs", "tmgx_solve", "tmgx_solve_seeded",
     "tmgx_pc_apply", "tmgx_level_apply", "tmgx_level_smooth", "tmgx_level_residual_restrict",
     "tmgx_level_prolong_add", "tmgx_coarse_solve", "tmgx_telescope_gather", "tmgx_telescope_scatter",
     "tmgx_get_counters", "tmgx_parity_build", "tmgx_last_error", "tmgx_bench_kernel", "tmgx_plan_summary",
+    "tmgx_node_selftest", "tmgx_exchange_timing",
     "tmgx_options_create", "tmgx_options_destroy", "tmgx_options_parse", "tmgx_options_parse_file_text",
     "tmgx_options_set", "tmgx_options_get", "tmgx_options_serialize", "tmgx_options_unused",
     "tmgx_options_resolve", "tmgx_solver_from_options", "tmgx_telescope_timing",
@@ -124,8 +125,8 @@ def load(parity: bool = False):
         "tmgx_repartition_header": [C.c_int, C.c_int, P(C.c_int), H],
         "tmgx_prefusion_layout": [H, C.c_int, P(C.c_int), C.c_int, I64],
         "tmgx_permutation": [H, H, C.c_int64, C.c_int64, I64],
-        "tmgx_nccl_unique_id": [C.c_void_p],
-        "tmgx_world_create": [C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, P(C.c_void_p)],
+        "tmgx_job_token": [C.c_char_p],
+        "tmgx_world_create": [C.c_int, C.c_int, C.c_int, C.c_int, C.c_char_p, P(C.c_void_p)],
         "tmgx_world_destroy": [C.c_void_p],
         "tmgx_world_local_ranks": [C.c_void_p, P(C.c_int), P(C.c_int)],
         "tmgx_solver_create": [C.c_void_p, P(_Problem), P(_MG), P(C.c_void_p)],
@@ -146,6 +147,8 @@ def load(parity: bool = False):
         "tmgx_get_counters": [C.c_void_p, P(_Counters)],
         "tmgx_bench_kernel": [C.c_void_p, C.c_int, C.c_int, C.c_int, D, D],
         "tmgx_plan_summary": [C.c_int, C.c_int, C.c_int, P(_Problem), P(_MG), I64, C.c_int, P(C.c_int)],
+        "tmgx_node_selftest": [C.c_char_p, C.c_int, C.c_int, C.c_int, I64],
+        "tmgx_exchange_timing": [C.c_void_p, C.c_int, C.c_int, P(C.c_double), P(C.c_int64)],
         "tmgx_options_create": [P(C.c_void_p)],
         "tmgx_options_destroy": [C.c_void_p],
         "tmgx_options_parse": [C.c_void_p, C.c_int, P(C.c_char_p)],
@@ -489,22 +492,24 @@ def build_solver_tree(db: OptionsDatabase, world: "World", problem: "Problem", p
     return SolverNode(world, problem, r.mg), r.ksp
 
 
-def nccl_unique_id(parity=False):
+def job_token(parity=False):
+    """A fresh node-local rendezvous name for a multi-process World (make it on one process and
+    pass it to the others)."""
     L = load(parity)
-    buf = (C.c_ubyte * NCCL_ID_BYTES)()
-    _check(L, L.tmgx_nccl_unique_id(buf))
-    return bytes(buf)
+    buf = C.create_string_buffer(JOB_TOKEN_BYTES)
+    _check(L, L.tmgx_job_token(buf))
+    return buf.value.decode()
 
 
 class World:
     """spawn_world analog: n_ranks reference ranks over nproc processes (one GPU each)."""
 
-    def __init__(self, n_ranks=1, nproc=1, proc=0, device=0, nccl_id: Optional[bytes] = None, parity=False):
+    def __init__(self, n_ranks=1, nproc=1, proc=0, device=0, job: Optional[str] = None, parity=False):
         self.L = load(parity)
         self.parity = parity
         self.h = C.c_void_p()
-        idb = C.create_string_buffer(nccl_id, NCCL_ID_BYTES) if nccl_id else None
-        _check(self.L, self.L.tmgx_world_create(n_ranks, nproc, proc, device, idb, C.byref(self.h)))
+        jb = job.encode() if job else None
+        _check(self.L, self.L.tmgx_world_create(n_ranks, nproc, proc, device, jb, C.byref(self.h)))
         f, e = C.c_int(), C.c_int()
         self.L.tmgx_world_local_ranks(self.h, C.byref(f), C.byref(e))
         self.local_ranks = (f.value, e.value)
@@ -563,6 +568,15 @@ def plan_summary(n_ranks, nproc, proc, problem: Problem, mg: MGConfig, max_recor
     return [tuple(int(v) for v in out[6 * i: 6 * i + 6]) for i in range(n.value)]
 
 
+def node_selftest(job, nproc, proc, rounds=50):
+    """Host-only: join the node-local process group `job` and run its barrier / allgather
+    self-check (tmgx_node_selftest). Returns (sum of gathered indices, consistent rounds)."""
+    L = load()
+    out = np.zeros(2, dtype=np.int64)
+    _check(L, L.tmgx_node_selftest(job.encode(), nproc, proc, rounds, _i64(out)))
+    return int(out[0]), int(out[1])
+
+
 class SolverNode:
     """SolverNode (solver.hpp:72-93): CG + MG(Chebyshev-Jacobi, telescope, LU) on tmgx."""
 
@@ -595,6 +609,12 @@ class SolverNode:
         ts, ta, by = C.c_double(), C.c_double(), C.c_int64()
         _check(self.L, self.L.tmgx_telescope_timing(self.h, stage, reps, C.byref(ts), C.byref(ta), C.byref(by)))
         return ts.value, ta.value, by.value
+
+    def exchange_timing(self, level, reps=50):
+        """(us per halo exchange of `level`, bytes this process sends per exchange); collective."""
+        us, by = C.c_double(), C.c_int64()
+        _check(self.L, self.L.tmgx_exchange_timing(self.h, level, reps, C.byref(us), C.byref(by)))
+        return us.value, by.value
 
     def level_info(self, level):
         h = Header()

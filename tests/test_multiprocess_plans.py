@@ -1,6 +1,6 @@
 """CPU, multi-process (gloo, world_size 2 and 4): the one-box-per-GPU path's host logic.
 
-Every process builds the halo and telescope plans it would execute with NCCL send/recv
+Every process builds the halo and telescope plans it would execute over the peer-mailbox transport
 (tmgx_plan_summary, no GPU needed). The processes exchange their plans over gloo and check:
   * every send p->q matches q's receive from p (same vertex count and the same checksum of
     the global vertex indices, i.e. the same regions in the same order);
