@@ -113,55 +113,90 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples), "power_w_max": max(pw) if pw else None}
 
 
-def cpu_reference_sample(steps=1, warmup=0, np3=(129, 129, 129), nlevels=6, m=2):
-    """The reference algorithm on the host: oracle/_ref (compiled reference translation units
-    plus the SPEC-following V-cycle glue) when it was built, else the C restatement in oracle/.
-    Returns (dof_per_s, seconds_per_solve, kind, sample description)."""
+def workload_config(config, world, tele_level, galerkin, est):
+    """The `config` object of both arms' JSON lines (identical for the same --config / N)."""
+    np3, nlevels, m, kind, _, rtol = CONFIGS[config]
+    n_dof = np3[0] * np3[1] * np3[2]
+    tele = world > 1 and tele_level is not None
+    return {"workload": f"{config}: {np3[0]}x{np3[1]}x{np3[2]} {'var-coef' if kind else 'Poisson'} {nlevels}-level "
+                        f"MG V({m},{m}) Cheb-Jacobi CG rtol {rtol:g}, est={est}, "
+                        f"coarse={'galerkin' if galerkin else 'rediscretised'}",
+            "global_batch": 1, "seq_len": np3[0],
+            "parallelism": f"box{world}" + (f"+telescope(L{tele_level},r{world})" if tele else ""),
+            "l2": ("inputs larger than L2 (one fine vector = %.0f MB)" % (n_dof * 8 / 1e6) if n_dof * 8 > 126e6 else
+                   "L2-resident problem (one fine vector = %.1f MB): a latency benchmark" % (n_dof * 8 / 1e6))}
+
+
+def cpu_reference_sample(config="cfg2", steps=1, warmup=0, galerkin=False, budget_s=0.0):
+    """The reference algorithm on the host, on the SAME problem as the GPU arm (BASELINE config,
+    full size): oracle/_ref (the reference's own translation units + the SPEC-following V-cycle
+    glue) when it was built, else the C restatement in oracle/. One rank = one core (the
+    reference has no threaded kernels; its n-rank mode is a mutex-serialised simulated transport).
+    Setup (assembly, hierarchy, estimates) is excluded; `warmup` untimed solves first, then the
+    mean over `steps` complete solves. Returns (dof_per_s, seconds_per_solve, kind, description,
+    iterations)."""
+    np3, nlevels, m, kind_p, _, rtol = CONFIGS[config]
     ref_bin = os.path.join(ROOT, "oracle", "_ref", "tmg_ref_bench")
     n = np3[0] * np3[1] * np3[2]
-    if os.path.exists(ref_bin):
-        out = subprocess.run([ref_bin, str(np3[0]), str(nlevels), str(m), str(steps), str(warmup), str(SEED_F)],
+    if os.path.exists(ref_bin) and np3[0] == np3[1] == np3[2]:
+        out = subprocess.run([ref_bin, str(np3[0]), str(nlevels), str(m), str(steps), str(warmup), str(SEED_F),
+                              "lanczos", "1" if galerkin else "0", str(kind_p), "-", str(budget_s)],
                              capture_output=True, text=True, check=True).stdout
         rec = json.loads(out.strip().splitlines()[-1])
-        t = rec["t_solve_s"]
-        kind = "reference"
-        its = rec["iterations"]
+        t, its, kind = rec["t_solve_s"], rec["iterations"], "reference"
+        setup, steps = rec["t_setup_s"], rec.get("steps_timed", steps)
     else:
+        os.environ.setdefault("OMP_NUM_THREADS", "1")  # the port's element loops are OpenMP
         from oracle import oracle as O
 
-        mg = O.MG(np3, nlevels, smooth_its=m, est_mode=O.EST_LANCZOS)
+        t0 = time.perf_counter()
+        mg = O.MG(np3, nlevels, kind=kind_p, smooth_its=m, est_mode=O.EST_LANCZOS, seed_k=SEED_K,
+                  galerkin=galerkin)
         b = O.rhs(np3, SEED_F)
+        setup = time.perf_counter() - t0
+        tw = 0.0
         for _ in range(warmup):
-            mg.solve(b, rtol=1e-8)
+            t0 = time.perf_counter()
+            mg.solve(b, rtol=rtol)
+            tw = time.perf_counter() - t0
+        if budget_s > 0 and tw > 0:
+            steps = max(1, min(steps, int(budget_s // tw)))
         ts = []
         for _ in range(steps):
             t0 = time.perf_counter()
-            _, rep = mg.solve(b, rtol=1e-8)
+            _, rep = mg.solve(b, rtol=rtol)
             ts.append(time.perf_counter() - t0)
-        t = sum(ts) / len(ts)
-        kind = "port"
-        its = rep["iterations"]
+        t, its, kind = sum(ts) / len(ts), rep["iterations"], "port"
     impl = ("reference translation units + SPEC glue (oracle/_ref/tmg_ref_bench)" if kind == "reference"
             else "oracle C restatement (oracle/liboracle.so)")
-    desc = (f"{np3[0]}x{np3[1]}x{np3[2]} Poisson, {nlevels}-level MG V({m},{m}) Cheb-Jacobi CG rtol 1e-8, "
-            f"{its} its, 1 core, solve only (setup excluded), {impl}")
-    return n / t, t, kind, desc
+    desc = (f"same problem as the GPU arm: {np3[0]}x{np3[1]}x{np3[2]}, {nlevels}-level MG V({m},{m}) CG rtol "
+            f"{rtol:g}, {its} its; {steps} timed complete solve(s) after {warmup} untimed, setup ({setup:.1f} s) "
+            f"excluded; 1 rank on 1 core; {impl}")
+    return n / t, t, kind, desc, its, steps
 
 
 def run_reference(args, rank, world):
-    cfg = CONFIGS[args.config]
+    """--impl reference: the reference's own CPU implementation of the path on this host, on the
+    GPU arm's config (same problem, same size). One complete 257^3 solve takes ~50 s on one
+    core, so K steps are capped by a time budget (TMGX_REF_BUDGET_S, default 150 s of timed
+    solves after one untimed solve); `steps` reports the solves actually timed."""
+    np3, nlevels, m, kind, tele_level, rtol = CONFIGS[args.config]
     if rank != 0:
         return
-    W = max(args.warmup, 0)
-    K = max(args.steps, 1)
-    rate, t, kind, desc = cpu_reference_sample(steps=K, warmup=min(W, 1))
+    galerkin = GALERKIN.get(args.config, False) if args.galerkin is None else args.galerkin == "on"
+    budget = float(os.environ.get("TMGX_REF_BUDGET_S", "150"))
+    W = 1 if args.warmup > 0 else 0  # the reference protocol: time the second of identical solves
+    rate, t, kind_s, desc, its, K = cpu_reference_sample(args.config, steps=max(args.steps, 1), warmup=W,
+                                                         galerkin=galerkin, budget_s=budget if W else 0.0)
     line = {
         "impl": "reference", "metric": "MG-CG DOF/s (time-to-solution)", "value": rate, "unit": "DOF/s",
-        "n_gpus": args.gpus, "steps": K, "warmup": W, "ms_per_step": t * 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded RHS)",
-        "config": {"workload": f"{args.config} sample on host cores", "global_batch": 1,
-                   "seq_len": cfg[0][0], "parallelism": "cpu"},
-        "cpu_baseline": {"value": rate, "unit": "DOF/s", "cores": 1, "kind": kind, "sample": desc},
+        "n_gpus": args.gpus, "steps": K, "warmup": W, "steps_requested": args.steps,
+        "warmup_requested": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded RHS, natural-index hash; BASELINE configs are synthetic)",
+        "config": workload_config(args.config, world, tele_level, galerkin, args.est),
+        "solve": {"iterations": its},
+        "cpu_baseline": {"value": rate, "unit": "DOF/s", "cores": 1, "kind": kind_s, "sample": desc},
         "e2e": {"value": rate, "unit": "DOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -368,7 +403,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        rate, t_cpu, ckind, desc = cpu_reference_sample(steps=1, warmup=0)
+        rate, t_cpu, ckind, desc, _, _ = cpu_reference_sample(args.config, steps=1, warmup=0, galerkin=galerkin)
         cpu = {"value": rate, "unit": "DOF/s", "cores": 1, "kind": ckind, "sample": desc}
 
     if rank == 0:
@@ -377,15 +412,9 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_dev / args.steps * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded RHS, natural-index hash; BASELINE configs are synthetic)",
-            "config": {"workload": f"{args.config}: {np3[0]}x{np3[1]}x{np3[2]} "
-                                   f"{'var-coef' if kind else 'Poisson'} {nlevels}-level MG V({m},{m}) "
-                                   f"Cheb-Jacobi CG rtol {rtol:g}, est={args.est}, "
-                                   f"coarse={'galerkin' if galerkin else 'rediscretised'}",
-                       "global_batch": 1, "seq_len": np3[0],
-                       "parallelism": f"box{world}" + (f"+telescope(L{tele_level},r{world})" if tele else ""),
-                       "l2": "inputs larger than L2 (one fine vector = %.0f MB)" % (n_dof * 8 / 1e6),
-                       "iterations": its[-1] if its else None, "t_setup_s": t_setup,
-                       "wall_ms_per_step": t_wall / args.steps * 1e3},
+            "config": workload_config(args.config, world, tele_level, galerkin, args.est),
+            "solve": {"iterations": its[-1] if its else None, "t_setup_s": t_setup,
+                      "wall_ms_per_step": t_wall / args.steps * 1e3},
             "e2e": {"value": e2e, "unit": "DOF/s", "h2d_bytes_per_step": 8 * n_dof,
                     "d2h_bytes_per_step": 8 * n_dof},
             "gpu_launches": launches,

@@ -12,7 +12,7 @@
 // coarsen, create_interpolation, spawn_world (1 rank = 1 core, the baseline protocol).
 //
 // usage: tmg_ref_bench N nlevels m steps warmup seed [est=lanczos|reference] [galerkin=0|1]
-//                      [kind=0|1] [dump_x_path]
+//                      [kind=0|1] [dump_x_path|-] [budget_s]
 // prints one JSON line {iterations, xnorm, final_ratio, t_setup_s, t_solve_s, ...}
 #include <chrono>
 #include <cmath>
@@ -255,7 +255,10 @@ int main(int argc, char** argv) {
   const bool galerkin = argc > 8 && std::atoi(argv[8]) != 0;
   Problem pr;
   pr.kind = argc > 9 ? std::atoi(argv[9]) : 0;
-  const std::string dump = argc > 10 ? argv[10] : "";
+  const std::string dump = argc > 10 && std::string(argv[10]) != "-" ? argv[10] : "";
+  // optional time budget (s) for the timed solves: after the warm-up, at most budget / t_warmup
+  // solves (at least one) are timed
+  const double budget = argc > 11 ? std::atof(argv[11]) : 0.0;
   for (int s = 0; s < 32; ++s)
     pr.spheres.push_back({hashed_uniform(pr.seed_k, 4ull * s + 0), hashed_uniform(pr.seed_k, 4ull * s + 1),
                           hashed_uniform(pr.seed_k, 4ull * s + 2),
@@ -281,12 +284,17 @@ int main(int argc, char** argv) {
         }
     DistVector x(comm, g.layout());
     SolveReport rep;
+    double t_warm = 0.0;
     for (int w = 0; w < warmup; ++w) {
       set_all(x, 0.0);
+      const double t1 = now();
       rep = outer.solve(b, x);
+      t_warm = now() - t1;
     }
+    int n_timed = steps;
+    if (budget > 0.0 && t_warm > 0.0) n_timed = std::max(1, std::min(steps, (int)(budget / t_warm)));
     double t_solve = 0.0;
-    for (int s = 0; s < steps; ++s) {
+    for (int s = 0; s < n_timed; ++s) {
       set_all(x, 0.0);
       const double t1 = now();
       rep = outer.solve(b, x);
@@ -302,9 +310,11 @@ int main(int argc, char** argv) {
                   "{\"iterations\": %d, \"reason\": \"%s\", \"xnorm\": %.17g, \"final_ratio\": %.17g, "
                   "\"t_setup_s\": %.6f, \"t_solve_s\": %.6f, \"n\": %lld, \"cheb_hi_fine\": %.17g, \"history\": [",
                   rep.iterations, to_string(rep.reason).c_str(), norm2(x),
-                  rep.residual_history.back() / rep.residual_history.front(), t_setup, t_solve / std::max(1, steps),
+                  rep.residual_history.back() / rep.residual_history.front(), t_setup, t_solve / std::max(1, n_timed),
                   (long long)(N * N * N), mg->bound_hi(nlevels - 1));
     std::string out(buf);
+    out.resize(out.size() - std::string(", \"history\": [").size());
+    out += std::string(", \"steps_timed\": ") + std::to_string(n_timed) + ", \"history\": [";
     for (std::size_t q = 0; q < rep.residual_history.size(); ++q) {
       std::snprintf(buf, sizeof buf, "%s%.17g", q ? ", " : "", rep.residual_history[q]);
       out += buf;
