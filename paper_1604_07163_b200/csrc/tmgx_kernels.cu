@@ -774,6 +774,269 @@ __global__ void __launch_bounds__(kTBNT, NR >= 4 ? 2 : (NR == 2 ? (PRE ? TMGX_TB
   }
 }
 
+// ------------------------------------------------------------------------------------------
+// Temporally blocked m = 2 Chebyshev, constant coefficients, issue-lean (round 2). Same tiles,
+// TMA staging, plane schedule and arithmetic as k_cheb2_tb (hence bitwise identical results),
+// restructured to cut the instructions issued per output point (k_cheb2_tb was issue bound at
+// ~190 thread-instructions per point, IPC 3.1, 47% of the copy peak):
+//  * boundary topology as exact-zero coefficients. A Dirichlet row's off-diagonals and every
+//    coupling to a Dirichlet neighbour are multiplied by 0 instead of skipped: the partial sum
+//    of a row is never -0 (it starts at +0 and x + (-x) rounds to +0), so acc + (+-0) == acc bit
+//    for bit, contracted to DFMA or not. Out-of-grid ring points get invd = 0, so d0 = 0 there.
+//    The coefficients of a lane's rows depend on y and z only through "interior or not"; a warp
+//    whose rows are all y-interior (warp-uniform test) on a z-interior plane (block-uniform)
+//    takes them from per-lane registers, so the interior runs with no per-point masks. The few
+//    warps and planes that touch a y/z boundary build them per point (same row function).
+//  * the plane loop is unrolled by three (queue period), so the z register queues never move;
+//  * pass-2 rows are guarded per thread (only lanes 0/31 and the tile's first/last row idle).
+// ------------------------------------------------------------------------------------------
+struct RowC {
+  double azm, aym, axm, axp, ayp, azp, invd;
+};
+
+// Row coefficients of global vertex (gi, gj, gk) with the topology folded in (see above).
+__device__ __forceinline__ RowC rowc_point(const BoxGeo& g, const OpParams& op, int gi, int gj, int gk) {
+  const bool in = gi >= 0 && gi < g.Nx && gj >= 0 && gj < g.Ny && gk >= 0 && gk < g.Nz;
+  const bool bnd = gi <= 0 || gj <= 0 || gk <= 0 || gi >= g.Nx - 1 || gj >= g.Ny - 1 || gk >= g.Nz - 1;
+  RowC c;
+  c.azm = (!bnd && gk >= 2) ? -op.ih2z : 0.0;
+  c.aym = (!bnd && gj >= 2) ? -op.ih2y : 0.0;
+  c.axm = (!bnd && gi >= 2) ? -op.ih2x : 0.0;
+  c.axp = (!bnd && gi <= g.Nx - 3) ? -op.ih2x : 0.0;
+  c.ayp = (!bnd && gj <= g.Ny - 3) ? -op.ih2y : 0.0;
+  c.azp = (!bnd && gk <= g.Nz - 3) ? -op.ih2z : 0.0;
+  c.invd = in ? op.cinvd : 0.0;
+  return c;
+}
+
+// The reference row loop (columns ascending: -z,-y,-x,c,+x,+y,+z) with every term present. The
+// performance build may sum it as a tree (TMGX_ROW_TREE: dependency depth 4 instead of 7).
+#ifndef TMGX_ROW_TREE
+#define TMGX_ROW_TREE 0
+#endif
+__device__ __forceinline__ double row7(const RowC& c, double dg, double uzm, double uym, double uxm, double uc,
+                                       double uxp, double uyp, double uzp) {
+#if TMGX_ROW_TREE && !defined(TMGX_PARITY)
+  const double a = c.azm * uzm + c.aym * uym, b = c.axm * uxm + dg * uc, e = c.axp * uxp + c.ayp * uyp;
+  return (a + b) + (e + c.azp * uzp);
+#endif
+  double acc = 0.0;
+  acc += c.azm * uzm;
+  acc += c.aym * uym;
+  acc += c.axm * uxm;
+  acc += dg * uc;
+  acc += c.axp * uxp;
+  acc += c.ayp * uyp;
+  acc += c.azp * uzp;
+  return acc;
+}
+
+#ifndef TMGX_TBF_MINB
+#define TMGX_TBF_MINB 3
+#endif
+template <bool PRE, int NR>
+struct alignas(128) TBFSmem {
+  using G = TBG<NR>;
+  static constexpr int NS = PRE ? kTBPF + 1 : kTBPF + 2;  // POST keeps x of the pass-1 plane
+  alignas(128) unsigned char b[NS][tb_al128(G::BB)];
+  alignas(128) unsigned char x[PRE ? 1 : NS][tb_al128(G::XB)];
+  double d[2][G::RY + 2][kTBX];  // d0 planes; rows 0 and RY+1 stay zero (pass-2 reads of idle rows)
+  unsigned long long bar[NS];
+};
+
+template <bool PRE, bool DOTS, int NR>
+__global__ void __launch_bounds__(kTBNT, NR >= 4 ? 2 : TMGX_TBF_MINB)
+    k_cheb2_fast(const __grid_constant__ TBMaps maps, BoxGeo g, OpParams op, double* __restrict__ xout,
+                 double s_theta, double c1, double c2, double* __restrict__ dpart, long long dstride) {
+  using G = TBG<NR>;
+  using SM = TBFSmem<PRE, NR>;
+  constexpr int NS = SM::NS;
+  extern __shared__ __align__(1024) unsigned char tb_smem_raw[];
+  SM& S = *reinterpret_cast<SM*>(tb_smem_raw);
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = tx + kTBX * ty;
+  const int ox = blockIdx.x * G::OX, oy = blockIdx.y * G::OY;
+  const int k0 = blockIdx.z * g.zc, k1 = min(k0 + g.zc, g.ez);
+  const int jr0 = ty * NR;  // first ring row of this thread
+  const int i = ox - 1 + tx, j0 = oy - 1 + jr0;
+  const int gi = g.gx + i, gj0 = g.gy + j0;
+  const bool out_x = tx >= 1 && tx <= kTBX - 2 && i < g.ex;
+  bool out_r[NR];
+#pragma unroll
+  for (int r = 0; r < NR; ++r) out_r[r] = out_x && jr0 + r >= 1 && jr0 + r <= G::RY - 2 && j0 + r < g.ey;
+  const bool wfast = gj0 >= 2 && gj0 + NR - 1 <= g.Ny - 3;  // warp-uniform: every row y-interior
+  // this lane's coefficients on y/z-interior rows (-y/+y and -z/+z coincide there); opaque to the
+  // optimiser so they stay in registers instead of being re-derived per plane with selects
+  const RowC L0 = rowc_point(g, op, gi, 2, 2);
+  double Lay = L0.aym, Laz = L0.azm, Laxm = L0.axm, Laxp = L0.axp, Linvd = L0.invd;
+  asm volatile("" : "+d"(Lay), "+d"(Laz), "+d"(Laxm), "+d"(Laxp), "+d"(Linvd));
+  const double dg = op.cdiag;
+
+  constexpr int LAG1 = PRE ? 0 : 1;
+  const int T0 = k0 - 1 - LAG1, T1 = k1 + LAG1;
+  const unsigned sb = smem_u32(&S.b[0][0]), sx = smem_u32(&S.x[0][0]), sbar = smem_u32(&S.bar[0]);
+  auto issue = [&](int t, int sl) {  // elected thread only
+    if (t > T1) return;
+    const unsigned bar = sbar + 8 * sl;
+    mbar_expect_tx(&S.bar[sl], PRE ? G::BB : G::BB + G::XB);
+    tma_load3(sb + sl * tb_al128(G::BB), &maps.b, kXO + ox - 2, oy, t - LAG1 + 1, bar);
+    if (!PRE) tma_load3(sx + sl * tb_al128(G::XB), &maps.x, kXO + ox - 2, oy - 1, t + 1, bar);
+  };
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) mbar_init(&S.bar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    for (int s = 0; s < kTBPF; ++s) issue(T0 + s, s);
+  }
+  if (tid < 4 * kTBX) S.d[tid >> 6][(tid >> 5) & 1 ? G::RY + 1 : 0][tx] = 0.0;
+  __syncthreads();
+
+  // z queues indexed by plane mod 3 (static after the unroll): d0(p), r0(p) (POST) / b(p) (PRE)
+  // -> dq[p%3], rq[p%3], phase-relative. x(p1) and x(p1+1) are read from their staging slots; x(p1-1)
+  // (pass 1's -z operand and pass 2's x) is the previous step's x(p1), kept in xm.
+  double xm[NR], dq[3][NR], rq[3][NR];
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    xm[r] = 0.0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) dq[a][r] = rq[a][r] = 0.0;
+  }
+  int sl = 0, isl = kTBPF, psl = NS - 1;
+  unsigned ph = 0;
+  double* outp = xout + g.base + i + g.px * (long long)j0 + g.pxy * (long long)(T0 - LAG1 - 1);
+  double dot_bz = 0.0, dot_zz = 0.0;
+  const int ob = jr0 * kTBSX + tx + 1;  // this thread's first ring row in a b / x-staging plane
+
+  // One step's work: pass 1 on plane p1 and pass 2 on plane p2 = p1 - 1, written as one basic block
+  // (all shared-memory loads, then both passes' row chains, then the stores) so that the NR
+  // independent rows of both passes interleave; the prologue/epilogue steps compute garbage on
+  // planes outside the chunk and only predicate their stores (every such value is finite, and
+  // nothing downstream reads it: a pass-2 plane only uses d0 planes pass 1 ran on).
+  auto body = [&](auto phase, auto fast, int p1, bool run1, bool run2) {
+    constexpr int PH = decltype(phase)::value;
+    constexpr bool FAST = decltype(fast)::value;
+    constexpr int P1 = PRE ? PH : (PH + 2) % 3;           // queue slot of plane p1
+    constexpr int P2 = (P1 + 2) % 3, P2m = (P1 + 1) % 3;  // p2 = p1 - 1, p2 - 1
+    const int p2 = p1 - 1;
+    auto coef = [&](int r, int p) -> RowC {
+      if (FAST) return RowC{Laz, Lay, Laxm, Laxp, Lay, Laz, Linvd};
+      return rowc_point(g, op, gi, gj0 + r, g.gz + p);
+    };
+    const double* bsm = reinterpret_cast<const double*>(S.b[sl]) + ob;
+    const double* X = reinterpret_cast<const double*>(S.x[psl]) + ob + kTBSX;  // x(p1), staged rows +1
+    const double* XP = reinterpret_cast<const double*>(S.x[sl]) + ob + kTBSX;  // x(p1 + 1)
+    const double* D = &S.d[p2 & 1][jr0 + 1][tx];                              // d0(p2)
+    const double* bp = reinterpret_cast<const double*>(S.b[psl]) + ob;        // b(p2) (POST)
+    double* Dw = &S.d[p1 & 1][jr0 + 1][tx];
+    // loads
+    double bb[NR], xc[NR], xw[NR], xe[NR], xp[NR], dw[NR], de[NR], bo[NR];
+    double xs0 = 0.0, xnN = 0.0;
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      bb[r] = bsm[r * kTBSX];
+      if (!PRE) {
+        xc[r] = X[r * kTBSX];
+        xw[r] = X[r * kTBSX - 1];
+        xe[r] = X[r * kTBSX + 1];
+        xp[r] = XP[r * kTBSX];
+      }
+      dw[r] = D[r * kTBX - 1];
+      de[r] = D[r * kTBX + 1];
+      if (DOTS) bo[r] = bp[r * kTBSX];
+    }
+    if (!PRE) {
+      xs0 = X[-kTBSX];
+      xnN = X[NR * kTBSX];
+    }
+    const double ds0 = D[-kTBX], dnN = D[NR * kTBX];
+    // pass 1: d0 = D^-1 (b - A x) / theta   (PRE: D^-1 b / theta)
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const RowC c = coef(r, p1);
+      double d0, rr;
+      if (PRE) {
+        d0 = (bb[r] * c.invd) * s_theta;
+        rr = bb[r];
+      } else {
+        const double xs_ = r == 0 ? xs0 : xc[r > 0 ? r - 1 : 0];
+        const double xn = r == NR - 1 ? xnN : xc[r < NR - 1 ? r + 1 : 0];
+        const double ax = row7(c, dg, xm[r], xs_, xw[r], xc[r], xe[r], xn, xp[r]);
+        rr = bb[r] - ax;
+        d0 = (rr * c.invd) * s_theta;
+      }
+      dq[P1][r] = d0;
+      rq[P1][r] = rr;
+    }
+    // pass 2 (output points): x' = (x + d0) + (c1 d0 + c2 D^-1 (r0 - A d0))
+    double xo[NR];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const RowC c = coef(r, p2);
+      const double d0 = dq[P2][r];
+      const double x1 = PRE ? d0 : xm[r] + d0;
+      const double ds = r == 0 ? ds0 : dq[P2][r > 0 ? r - 1 : 0];
+      const double dn_ = r == NR - 1 ? dnN : dq[P2][r < NR - 1 ? r + 1 : 0];
+      const double ad = row7(c, dg, dq[P2m][r], ds, dw[r], d0, de[r], dn_, dq[P1][r]);
+      const double r1 = rq[P2][r] - ad;
+      const double z = r1 * c.invd;
+      const double dn = c1 * d0 + c2 * z;
+      xo[r] = x1 + dn;
+    }
+    // stores
+#pragma unroll
+    for (int r = 0; r < NR; ++r) Dw[r * kTBX] = dq[P1][r];
+    if (run2) {
+#pragma unroll
+      for (int r = 0; r < NR; ++r)
+        if (out_r[r]) {
+          outp[g.px * r] = xo[r];
+          if (DOTS) {
+            dot_bz += bo[r] * xo[r];
+            dot_zz += xo[r] * xo[r];
+          }
+        }
+    }
+    (void)run1;
+#pragma unroll
+    for (int r = 0; r < NR; ++r) xm[r] = PRE ? 0.0 : xc[r];  // x(p1) is the next step's x(p1 - 1)
+  };
+  auto zin = [&](int p) { return g.gz + p >= 2 && g.gz + p <= g.Nz - 3; };
+  auto step = [&](auto phase, int t) {
+    const int p1 = t - LAG1;
+    mbar_wait(sbar + 8 * sl, ph);
+    __syncthreads();  // group t visible; slot of group t-2 and the d buffer of step t-2 are free
+    if (tid == 0) {
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      issue(t + kTBPF, isl);
+    }
+    const bool run1 = p1 >= k0 - 1, run2 = p1 - 1 >= k0 && p1 - 1 < k1;
+    if (wfast && zin(p1) && zin(p1 - 1))
+      body(phase, std::true_type{}, p1, run1, run2);
+    else
+      body(phase, std::false_type{}, p1, run1, run2);
+    psl = sl;
+    if (++sl == NS) sl = 0, ph ^= 1u;
+    if (++isl == NS) isl = 0;
+    outp += g.pxy;
+  };
+  for (int t = T0;;) {
+    if (t > T1) break;
+    step(std::integral_constant<int, 0>{}, t++);
+    if (t > T1) break;
+    step(std::integral_constant<int, 1>{}, t++);
+    if (t > T1) break;
+    step(std::integral_constant<int, 2>{}, t++);
+  }
+  if (DOTS) {
+    __syncthreads();
+    double* sh = &S.d[0][0][0];
+    const double s0 = block_sum(dot_bz, sh);
+    const double s1 = block_sum(dot_zz, sh);
+    if (tid == 0) {
+      dpart[blk_linear()] = s0;
+      dpart[dstride + blk_linear()] = s1;
+    }
+  }
+}
+
 // Residual fused with the restriction (single-box levels, 7-point rows):
 //   r = b - A x  (k_march FApply<1> arithmetic)   b_c = 2^-3 P^T r  (k_restrict order)
 // A block owns a 15 x 7 coarse tile and marches coarse planes; its 32 x 8 threads compute the
@@ -1567,6 +1830,20 @@ static int tb_rows() {
   return nr;
 }
 bool cheb2_tb_supported(const BoxGeo& g) { return tb_fits<1>(g); }
+static int tbf_rows() {  // rows per thread of the issue-lean kernel (TMGX_TBF_NR = 4, default, or 2)
+  static const int nr = [] {
+    const char* e = std::getenv("TMGX_TBF_NR");
+    return e && std::atoi(e) == 2 ? 2 : 4;
+  }();
+  return nr;
+}
+static bool tb_fast() {  // TMGX_TB_FAST=0: the r02 blocked kernel for constant coefficients too
+  static const bool on = [] {
+    const char* e = std::getenv("TMGX_TB_FAST");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 // TMA descriptor of a padded box array (dims px x (ey+2) x (ez+2), fp64, zero fill outside),
 // cached per (array, box shape).
@@ -1655,10 +1932,17 @@ static int launch_tb_rows(const BoxGeo& g, const OpParams& op, const double* b, 
     kern<<<gr, bl, smem, s>>>(maps, gt, op, xout, s_theta, c.c1, c.c2, dpart, dstride);
     return true;
   };
-  static int slots[6] = {0, 0, 0, 0, 0, 0};
+  static int slots[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   const bool dots = dpart != nullptr && !pre;
   bool ok;
-  if (op.fc) {
+  if (NR == tbf_rows() && !op.fc && !op.k && !op.S && tb_fast()) {  // constant coefficients: issue-lean kernel
+    if (pre)
+      ok = run(k_cheb2_fast<true, false, NR>, sizeof(TBFSmem<true, NR>), slots[6], false);
+    else if (dots)
+      ok = run(k_cheb2_fast<false, true, NR>, sizeof(TBFSmem<false, NR>), slots[7], true);
+    else
+      ok = run(k_cheb2_fast<false, false, NR>, sizeof(TBFSmem<false, NR>), slots[8], false);
+  } else if (op.fc) {
     if (pre)
       ok = run(k_cheb2_tb<true, true, NR>, sizeof(TBSmem<NR, true>), slots[0], false);
     else if (dots)
@@ -1679,7 +1963,7 @@ static int launch_tb_rows(const BoxGeo& g, const OpParams& op, const double* b, 
 int launch_cheb2_tb(const BoxGeo& g, const OpParams& op, const double* b, const double* xin, double* xout,
                     double s_theta, ChebStep c, bool pre, cudaStream_t s, double* dpart, long long dstride, int dmax,
                     int* dblocks) {
-  const int nr = tb_rows();
+  const int nr = (!op.fc && !op.k && !op.S && tb_fast()) ? tbf_rows() : tb_rows();
   int nb;
   if (nr >= 4 && tb_fits<4>(g))
     nb = launch_tb_rows<4>(g, op, b, xin, xout, s_theta, c, pre, dpart, dstride, dmax, s);
