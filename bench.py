@@ -379,7 +379,7 @@ def main():
     # blocked smoother applies (m = 2, single-box level), else the fused Chebyshev pass.
     peak, peak_kind = read_peaks()
     tb = m == 2 and world == 1 and os.environ.get("TMGX_TB", "1") != "0" and not galerkin
-    dom_id, dom_key, dom_name = ((9, "tb_post", "k_cheb2_tb<post> (blocked V(2,2) post-smooth, fine level)") if tb
+    dom_id, dom_key, dom_name = ((9, "tb_post", "k_cheb2_fast<post> (blocked V(2,2) post-smooth, TMA-staged, fine level)") if tb
                                  else (1, "cheb_step_last", "k_cheb_step (last pass, fine level)"))
     ms, by = s.bench_kernel(dom_id, nlevels - 1, iters=20)
     ms_all = max_over_ranks(ms)

@@ -513,9 +513,9 @@ constexpr int kTBSX = kTBX + 2;  // staged width (ring + 1 each side; TMA x-star
 constexpr int kTBPF = TMGX_TB_PF;  // plane groups in flight
 __host__ __device__ constexpr int tb_al128(int b) { return (b + 127) / 128 * 128; }
 
-template <int NR>
+template <int NR, int TY = kTBY>
 struct TBG {
-  static constexpr int RY = kTBY * NR;              // ring rows
+  static constexpr int RY = TY * NR;                // ring rows
   static constexpr int OX = kTBX - 2, OY = RY - 2;  // output tile
   static constexpr int SY = RY + 2;                 // staged x rows
   static constexpr int BB = kTBSX * RY * 8, XB = kTBSX * SY * 8;  // box bytes
@@ -834,9 +834,9 @@ __device__ __forceinline__ double row7(const RowC& c, double dg, double uzm, dou
 #ifndef TMGX_TBF_MINB
 #define TMGX_TBF_MINB 3
 #endif
-template <bool PRE, int NR>
+template <bool PRE, int NR, int TY>
 struct alignas(128) TBFSmem {
-  using G = TBG<NR>;
+  using G = TBG<NR, TY>;
   static constexpr int NS = PRE ? kTBPF + 1 : kTBPF + 2;  // POST keeps x of the pass-1 plane
   alignas(128) unsigned char b[NS][tb_al128(G::BB)];
   alignas(128) unsigned char x[PRE ? 1 : NS][tb_al128(G::XB)];
@@ -844,12 +844,12 @@ struct alignas(128) TBFSmem {
   unsigned long long bar[NS];
 };
 
-template <bool PRE, bool DOTS, int NR>
-__global__ void __launch_bounds__(kTBNT, NR >= 4 ? 2 : TMGX_TBF_MINB)
+template <bool PRE, bool DOTS, int NR, int TY>
+__global__ void __launch_bounds__(kTBX* TY, NR >= 4 ? 16 / TY : TMGX_TBF_MINB)
     k_cheb2_fast(const __grid_constant__ TBMaps maps, BoxGeo g, OpParams op, double* __restrict__ xout,
                  double s_theta, double c1, double c2, double* __restrict__ dpart, long long dstride) {
-  using G = TBG<NR>;
-  using SM = TBFSmem<PRE, NR>;
+  using G = TBG<NR, TY>;
+  using SM = TBFSmem<PRE, NR, TY>;
   constexpr int NS = SM::NS;
   extern __shared__ __align__(1024) unsigned char tb_smem_raw[];
   SM& S = *reinterpret_cast<SM*>(tb_smem_raw);
@@ -886,7 +886,11 @@ __global__ void __launch_bounds__(kTBNT, NR >= 4 ? 2 : TMGX_TBF_MINB)
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     for (int s = 0; s < kTBPF; ++s) issue(T0 + s, s);
   }
-  if (tid < 4 * kTBX) S.d[tid >> 6][(tid >> 5) & 1 ? G::RY + 1 : 0][tx] = 0.0;
+  // zero the d0 planes: pad rows, and the rows of warps that never compute (outside the grid)
+  for (int e = tid; e < 2 * (G::RY + 2) * kTBX; e += kTBX * TY) (&S.d[0][0][0])[e] = 0.0;
+  // a warp whose rows all lie outside the grid skips the arithmetic (no in-grid row reads its
+  // d0: only Dirichlet rows border it, and their off-diagonal coefficients are zero)
+  const bool wskip = gj0 >= g.Ny || gj0 + NR - 1 < 0;
   __syncthreads();
 
   // z queues indexed by plane mod 3 (static after the unroll): d0(p), r0(p) (POST) / b(p) (PRE)
@@ -1010,8 +1014,240 @@ __global__ void __launch_bounds__(kTBNT, NR >= 4 ? 2 : TMGX_TBF_MINB)
     const bool run1 = p1 >= k0 - 1, run2 = p1 - 1 >= k0 && p1 - 1 < k1;
     if (wfast && zin(p1) && zin(p1 - 1))
       body(phase, std::true_type{}, p1, run1, run2);
-    else
+    else if (!wskip)
       body(phase, std::false_type{}, p1, run1, run2);
+    psl = sl;
+    if (++sl == NS) sl = 0, ph ^= 1u;
+    if (++isl == NS) isl = 0;
+    outp += g.pxy;
+  };
+  for (int t = T0;;) {
+    if (t > T1) break;
+    step(std::integral_constant<int, 0>{}, t++);
+    if (t > T1) break;
+    step(std::integral_constant<int, 1>{}, t++);
+    if (t > T1) break;
+    step(std::integral_constant<int, 2>{}, t++);
+  }
+  if (DOTS) {
+    __syncthreads();
+    double* sh = &S.d[0][0][0];
+    const double s0 = block_sum(dot_bz, sh);
+    const double s1 = block_sum(dot_zz, sh);
+    if (tid == 0) {
+      dpart[blk_linear()] = s0;
+      dpart[dstride + blk_linear()] = s1;
+    }
+  }
+}
+
+// Paired-column variant: a thread owns two adjacent columns x NR rows, so the staged x / b
+// planes, the d0 plane and the output are read and written as 16-byte pairs (half the shared
+// memory instructions of the one-column layout for the same points). A warp covers 32 columns x
+// 2 NR rows (16 lanes across x, 2 across y). The ring starts on an even column (output tile
+// [30 bx - 1, 30 bx + 28]; the first tile's column -1 is out of the grid and idle) so that every
+// pair is 16-byte aligned in the padded array, the TMA boxes and the d0 plane.
+template <bool PRE, int NR, int TY>
+struct alignas(128) TBPSmem {
+  static constexpr int RY = 2 * TY * NR;             // ring rows
+  static constexpr int BW = 32, XW = 36, DW = 36;    // staged widths: b = ring, x = ring +-2, d0 = ring +-2
+  static constexpr int BB = BW * RY * 8, XB = XW * (RY + 2) * 8;
+  static constexpr int NS = PRE ? kTBPF + 1 : kTBPF + 2;
+  alignas(128) unsigned char b[NS][tb_al128(BB)];
+  alignas(128) unsigned char x[PRE ? 1 : NS][tb_al128(XB)];
+  double d[2][RY + 2][DW];  // d0 planes; pad rows 0 / RY+1 and pad columns stay zero
+  unsigned long long bar[NS];
+};
+
+template <bool PRE, bool DOTS, int NR, int TY>
+__global__ void __launch_bounds__(kTBX* TY, 16 / TY)
+    k_cheb2_pair(const __grid_constant__ TBMaps maps, BoxGeo g, OpParams op, double* __restrict__ xout,
+                 double s_theta, double c1, double c2, double* __restrict__ dpart, long long dstride) {
+  using SM = TBPSmem<PRE, NR, TY>;
+  constexpr int NS = SM::NS, RY = SM::RY, BW = SM::BW, XW = SM::XW, DW = SM::DW;
+  constexpr int OX = 30, OY = RY - 2;
+  extern __shared__ __align__(1024) unsigned char tb_smem_raw[];
+  SM& S = *reinterpret_cast<SM*>(tb_smem_raw);
+  const int lane = threadIdx.x, wy = threadIdx.y, tid = lane + kTBX * wy;
+  const int lx = lane & 15, ly = lane >> 4;
+  const int rs = blockIdx.x * OX - 2, oy = blockIdx.y * OY;  // ring column 0 / output row 0 (local)
+  const int k0 = blockIdx.z * g.zc, k1 = min(k0 + g.zc, g.ez);
+  const int c0 = 2 * lx;               // ring columns c0, c0 + 1
+  const int jr0 = (2 * wy + ly) * NR;  // first ring row
+  const int i0 = rs + c0, j0 = oy - 1 + jr0;
+  const int gi0 = g.gx + i0, gj0 = g.gy + j0;
+  bool out_c[2], out_r[NR];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) out_c[q] = c0 + q >= 1 && c0 + q <= 30 && i0 + q >= 0 && i0 + q < g.ex;
+#pragma unroll
+  for (int r = 0; r < NR; ++r) out_r[r] = jr0 + r >= 1 && jr0 + r <= RY - 2 && j0 + r < g.ey;
+  // warp-uniform y test over the warp's 2 NR rows
+  const int wj0 = g.gy + oy - 1 + 2 * wy * NR;
+  const bool wfast = wj0 >= 2 && wj0 + 2 * NR - 1 <= g.Ny - 3;
+  const RowC La = rowc_point(g, op, gi0, 2, 2), Lb = rowc_point(g, op, gi0 + 1, 2, 2);
+  double ay0 = La.aym, az0 = La.azm, axm0 = La.axm, axp0 = La.axp, iv0 = La.invd;
+  double ay1 = Lb.aym, az1 = Lb.azm, axm1 = Lb.axm, axp1 = Lb.axp, iv1 = Lb.invd;
+  asm volatile("" : "+d"(ay0), "+d"(az0), "+d"(axm0), "+d"(axp0), "+d"(iv0));
+  asm volatile("" : "+d"(ay1), "+d"(az1), "+d"(axm1), "+d"(axp1), "+d"(iv1));
+  const double dg = op.cdiag;
+
+  constexpr int LAG1 = PRE ? 0 : 1;
+  const int T0 = k0 - 1 - LAG1, T1 = k1 + LAG1;
+  const unsigned sb = smem_u32(&S.b[0][0]), sx = smem_u32(&S.x[0][0]), sbar = smem_u32(&S.bar[0]);
+  auto issue = [&](int t, int sl) {  // elected thread only
+    if (t > T1) return;
+    const unsigned bar = sbar + 8 * sl;
+    mbar_expect_tx(&S.bar[sl], PRE ? SM::BB : SM::BB + SM::XB);
+    tma_load3(sb + sl * tb_al128(SM::BB), &maps.b, kXO + rs, oy, t - LAG1 + 1, bar);
+    if (!PRE) tma_load3(sx + sl * tb_al128(SM::XB), &maps.x, kXO + rs - 2, oy - 1, t + 1, bar);
+  };
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) mbar_init(&S.bar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    for (int s = 0; s < kTBPF; ++s) issue(T0 + s, s);
+  }
+  for (int e = tid; e < 2 * (RY + 2) * DW; e += kTBX * TY) (&S.d[0][0][0])[e] = 0.0;
+  __syncthreads();
+
+  // per point (row r, column q): queues of d0 / r0 (POST) or b (PRE) by plane mod 3; xm = x(p1-1)
+  double2 xm[NR], dq[3][NR], rq[3][NR];
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    xm[r] = double2{0.0, 0.0};
+#pragma unroll
+    for (int a = 0; a < 3; ++a) dq[a][r] = rq[a][r] = double2{0.0, 0.0};
+  }
+  int sl = 0, isl = kTBPF, psl = NS - 1;
+  unsigned ph = 0;
+  double* outp = xout + g.base + i0 + g.px * (long long)j0 + g.pxy * (long long)(T0 - LAG1 - 1);
+  double dot_bz = 0.0, dot_zz = 0.0;
+  const int obb = jr0 * BW + c0;             // b pair of this thread's first row
+  const int obx = (jr0 + 1) * XW + c0 + 2;   // x pair (staged rows +1, columns +2)
+  const int obd = (jr0 + 1) * DW + c0 + 2;   // d0 pair (pad row +1, pad columns +2)
+  auto ld2s = [](const double* p) { return *reinterpret_cast<const double2*>(p); };
+
+  auto body = [&](auto phase, auto fast, int p1, bool run2) {
+    constexpr int PH = decltype(phase)::value;
+    constexpr bool FAST = decltype(fast)::value;
+    constexpr int P1 = PRE ? PH : (PH + 2) % 3;
+    constexpr int P2 = (P1 + 2) % 3, P2m = (P1 + 1) % 3;
+    const int p2 = p1 - 1;
+    auto coef = [&](int q, int r, int p) -> RowC {
+      if (FAST) {
+        if (q == 0) return RowC{az0, ay0, axm0, axp0, ay0, az0, iv0};
+        return RowC{az1, ay1, axm1, axp1, ay1, az1, iv1};
+      }
+      return rowc_point(g, op, gi0 + q, gj0 + r, g.gz + p);
+    };
+    const double* B = reinterpret_cast<const double*>(S.b[sl]) + obb;
+    const double* X = reinterpret_cast<const double*>(S.x[psl]) + obx;   // x(p1)
+    const double* XP = reinterpret_cast<const double*>(S.x[sl]) + obx;   // x(p1 + 1)
+    const double* D = &S.d[p2 & 1][0][0] + obd;                          // d0(p2)
+    const double* BP = reinterpret_cast<const double*>(S.b[psl]) + obb;  // b(p2) (POST)
+    double* Dw = &S.d[p1 & 1][0][0] + obd;
+    double2 bb[NR], xc[NR], xp[NR], bo[NR];
+    double xw[NR], xe[NR], dw[NR], de[NR];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      bb[r] = ld2s(B + r * BW);
+      if (!PRE) {
+        xc[r] = ld2s(X + r * XW);
+        xw[r] = X[r * XW - 1];
+        xe[r] = X[r * XW + 2];
+        xp[r] = ld2s(XP + r * XW);
+      }
+      dw[r] = D[r * DW - 1];
+      de[r] = D[r * DW + 2];
+      if (DOTS) bo[r] = ld2s(BP + r * BW);
+    }
+    double2 xs0{0.0, 0.0}, xnN{0.0, 0.0};
+    if (!PRE) {
+      xs0 = ld2s(X - XW);
+      xnN = ld2s(X + NR * XW);
+    }
+    const double2 ds0 = ld2s(D - DW), dnN = ld2s(D + NR * DW);
+    // pass 1
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const RowC c = coef(q, r, p1);
+        const double b_ = get(bb[r], q);
+        double d0, rr;
+        if (PRE) {
+          d0 = (b_ * c.invd) * s_theta;
+          rr = b_;
+        } else {
+          const double uw = q ? xc[r].x : xw[r], ue = q ? xe[r] : xc[r].y;
+          const double us = r == 0 ? get(xs0, q) : get(xc[r > 0 ? r - 1 : 0], q);
+          const double un = r == NR - 1 ? get(xnN, q) : get(xc[r < NR - 1 ? r + 1 : 0], q);
+          const double ax = row7(c, dg, get(xm[r], q), us, uw, get(xc[r], q), ue, un, get(xp[r], q));
+          rr = b_ - ax;
+          d0 = (rr * c.invd) * s_theta;
+        }
+        set(dq[P1][r], q, d0);
+        set(rq[P1][r], q, rr);
+      }
+    }
+    // pass 2
+    double2 xo[NR];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const RowC c = coef(q, r, p2);
+        const double d0 = get(dq[P2][r], q);
+        const double x1 = PRE ? d0 : get(xm[r], q) + d0;
+        const double uw = q ? dq[P2][r].x : dw[r], ue = q ? de[r] : dq[P2][r].y;
+        const double us = r == 0 ? get(ds0, q) : get(dq[P2][r > 0 ? r - 1 : 0], q);
+        const double un = r == NR - 1 ? get(dnN, q) : get(dq[P2][r < NR - 1 ? r + 1 : 0], q);
+        const double ad = row7(c, dg, get(dq[P2m][r], q), us, uw, d0, ue, un, get(dq[P1][r], q));
+        const double r1 = get(rq[P2][r], q) - ad;
+        const double z = r1 * c.invd;
+        const double dn = c1 * d0 + c2 * z;
+        set(xo[r], q, x1 + dn);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < NR; ++r) *reinterpret_cast<double2*>(Dw + r * DW) = dq[P1][r];
+    if (run2) {
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        if (!out_r[r]) continue;
+        double* o = outp + g.px * r;
+        if (out_c[0] && out_c[1])
+          *reinterpret_cast<double2*>(o) = xo[r];
+        else if (out_c[0])
+          o[0] = xo[r].x;
+        else if (out_c[1])
+          o[1] = xo[r].y;
+        if (DOTS) {
+#pragma unroll
+          for (int q = 0; q < 2; ++q)
+            if (out_c[q]) {
+              dot_bz += get(bo[r], q) * get(xo[r], q);
+              dot_zz += get(xo[r], q) * get(xo[r], q);
+            }
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < NR; ++r) xm[r] = PRE ? double2{0.0, 0.0} : xc[r];
+  };
+  auto zin = [&](int p) { return g.gz + p >= 2 && g.gz + p <= g.Nz - 3; };
+  auto step = [&](auto phase, int t) {
+    const int p1 = t - LAG1;
+    mbar_wait(sbar + 8 * sl, ph);
+    __syncthreads();
+    if (tid == 0) {
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      issue(t + kTBPF, isl);
+    }
+    const bool run2 = p1 - 1 >= k0 && p1 - 1 < k1;
+    if (wfast && zin(p1) && zin(p1 - 1))
+      body(phase, std::true_type{}, p1, run2);
+    else
+      body(phase, std::false_type{}, p1, run2);
     psl = sl;
     if (++sl == NS) sl = 0, ph ^= 1u;
     if (++isl == NS) isl = 0;
@@ -1830,12 +2066,12 @@ static int tb_rows() {
   return nr;
 }
 bool cheb2_tb_supported(const BoxGeo& g) { return tb_fits<1>(g); }
-static int tbf_rows() {  // rows per thread of the issue-lean kernel (TMGX_TBF_NR = 4, default, or 2)
-  static const int nr = [] {
-    const char* e = std::getenv("TMGX_TBF_NR");
-    return e && std::atoi(e) == 2 ? 2 : 4;
+static int tbf_ty() {  // warps per block of the issue-lean kernel (TMGX_TBF_TY = 8, default, or 4)
+  static const int ty = [] {
+    const char* e = std::getenv("TMGX_TBF_TY");
+    return e ? (std::atoi(e) == 4 ? 4 : (std::atoi(e) == 2 ? 2 : 8)) : 8;  // 2: paired columns
   }();
-  return nr;
+  return ty;
 }
 static bool tb_fast() {  // TMGX_TB_FAST=0: the r02 blocked kernel for constant coefficients too
   static const bool on = [] {
@@ -1881,6 +2117,116 @@ static CUtensorMap tensor_map(const BoxGeo& g, const double* base_ptr, int bx, i
   return m;
 }
 
+// z planes per block: minimise waves x (planes + pipeline fill) over the split count (a pure
+// function of the geometry and the kernel's residency, so repeated launches agree on the block
+// count and hence on the fused dot-product partials).
+static int tb_zchunk(const BoxGeo& g, long long cols, int slots) {
+  static const int zc_env = [] {
+    const char* e = std::getenv("TMGX_TB_ZC");
+    return e ? std::max(1, std::atoi(e)) : 0;
+  }();
+  if (zc_env) return std::min(zc_env, g.ez);
+  int best = g.ez;
+  long long best_cost = -1;
+  for (int nzb = 1; nzb <= g.ez; ++nzb) {
+    const int zc = (g.ez + nzb - 1) / nzb;
+    const long long waves = (cols * nzb + slots - 1) / slots;
+    const long long cost = waves * (zc + 3);
+    if (best_cost < 0 || cost < best_cost) best_cost = cost, best = zc;
+  }
+  return best;
+}
+
+// The issue-lean constant-coefficient kernel: NR rows per thread, TY warps per block.
+template <int NR, int TY>
+static bool tbf_fits(const BoxGeo& g) {
+  return g.px >= kTBSX && g.ey + 2 >= TBG<NR, TY>::SY;
+}
+template <int NR, int TY>
+static int launch_tbf(const BoxGeo& g, const OpParams& op, const double* b, const double* xin, double* xout,
+                      double s_theta, ChebStep c, bool pre, double* dpart, long long dstride, int dmax,
+                      cudaStream_t s) {
+  using G = TBG<NR, TY>;
+  TBMaps maps;
+  std::memset(&maps, 0, sizeof(maps));
+  maps.b = tensor_map(g, b, kTBSX, G::RY);
+  if (!pre) maps.x = tensor_map(g, xin, kTBSX, G::SY);
+  const bool dots = dpart != nullptr && !pre;
+  static int slots[3] = {0, 0, 0};
+  int nblk = 0;
+  auto run = [&](auto kern, size_t smem, int& sl) {
+    if (!sl) {
+      int dev = 0, sms = 0, per = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kTBX * TY, smem);
+      sl = std::max(1, sms * std::max(per, 1));
+    }
+    const long long cols = (long long)((g.ex + G::OX - 1) / G::OX) * ((g.ey + G::OY - 1) / G::OY);
+    BoxGeo gt = g;
+    gt.zc = tb_zchunk(g, cols, sl);
+    const dim3 gr((g.ex + G::OX - 1) / G::OX, (g.ey + G::OY - 1) / G::OY, (g.ez + gt.zc - 1) / gt.zc);
+    nblk = (int)(gr.x * gr.y * gr.z);
+    if (dots && nblk > dmax) return false;  // partial buffer too small: caller falls back
+    kern<<<gr, dim3(kTBX, TY), smem, s>>>(maps, gt, op, xout, s_theta, c.c1, c.c2, dpart, dstride);
+    return true;
+  };
+  bool ok;
+  if (pre)
+    ok = run(k_cheb2_fast<true, false, NR, TY>, sizeof(TBFSmem<true, NR, TY>), slots[0]);
+  else if (dots)
+    ok = run(k_cheb2_fast<false, true, NR, TY>, sizeof(TBFSmem<false, NR, TY>), slots[1]);
+  else
+    ok = run(k_cheb2_fast<false, false, NR, TY>, sizeof(TBFSmem<false, NR, TY>), slots[2]);
+  return ok ? (dots ? nblk : 0) : -1;
+}
+
+template <int NR, int TY>
+static bool tbp_fits(const BoxGeo& g) {
+  return g.px >= TBPSmem<true, NR, TY>::XW && g.ey + 2 >= TBPSmem<true, NR, TY>::RY + 2;
+}
+template <int NR, int TY>
+static int launch_tbp(const BoxGeo& g, const OpParams& op, const double* b, const double* xin, double* xout,
+                      double s_theta, ChebStep c, bool pre, double* dpart, long long dstride, int dmax,
+                      cudaStream_t s) {
+  using SP = TBPSmem<true, NR, TY>;
+  TBMaps maps;
+  std::memset(&maps, 0, sizeof(maps));
+  maps.b = tensor_map(g, b, SP::BW, SP::RY);
+  if (!pre) maps.x = tensor_map(g, xin, SP::XW, SP::RY + 2);
+  const bool dots = dpart != nullptr && !pre;
+  static int slots[3] = {0, 0, 0};
+  int nblk = 0;
+  auto run = [&](auto kern, size_t smem, int& sl) {
+    if (!sl) {
+      int dev = 0, sms = 0, per = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kTBX * TY, smem);
+      sl = std::max(1, sms * std::max(per, 1));
+    }
+    const int OY = SP::RY - 2;
+    const long long cols = (long long)((g.ex + 1 + 29) / 30) * ((g.ey + OY - 1) / OY);
+    BoxGeo gt = g;
+    gt.zc = tb_zchunk(g, cols, sl);
+    const dim3 gr((g.ex + 1 + 29) / 30, (g.ey + OY - 1) / OY, (g.ez + gt.zc - 1) / gt.zc);
+    nblk = (int)(gr.x * gr.y * gr.z);
+    if (dots && nblk > dmax) return false;
+    kern<<<gr, dim3(kTBX, TY), smem, s>>>(maps, gt, op, xout, s_theta, c.c1, c.c2, dpart, dstride);
+    return true;
+  };
+  bool ok;
+  if (pre)
+    ok = run(k_cheb2_pair<true, false, NR, TY>, sizeof(TBPSmem<true, NR, TY>), slots[0]);
+  else if (dots)
+    ok = run(k_cheb2_pair<false, true, NR, TY>, sizeof(TBPSmem<false, NR, TY>), slots[1]);
+  else
+    ok = run(k_cheb2_pair<false, false, NR, TY>, sizeof(TBPSmem<false, NR, TY>), slots[2]);
+  return ok ? (dots ? nblk : 0) : -1;
+}
+
 template <int NR>
 static int launch_tb_rows(const BoxGeo& g, const OpParams& op, const double* b, const double* xin, double* xout,
                           double s_theta, ChebStep c, bool pre, double* dpart, long long dstride, int dmax,
@@ -1901,27 +2247,9 @@ static int launch_tb_rows(const BoxGeo& g, const OpParams& op, const double* b, 
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kTBNT, smem);
       slots = std::max(1, sms * std::max(per, 1));
     }
-    // z planes per block: minimise waves x (planes + pipeline fill) over the split count (a
-    // pure function of the geometry, so repeated launches agree on the block count)
     BoxGeo gt = g;
     const long long cols = (long long)((g.ex + G::OX - 1) / G::OX) * ((g.ey + G::OY - 1) / G::OY);
-    static const int zc_env = [] {
-      const char* e = std::getenv("TMGX_TB_ZC");
-      return e ? std::max(1, std::atoi(e)) : 0;
-    }();
-    int best = g.ez;
-    if (zc_env) {
-      best = std::min(zc_env, g.ez);
-    } else {
-      long long best_cost = -1;
-      for (int nzb = 1; nzb <= g.ez; ++nzb) {
-        const int zc = (g.ez + nzb - 1) / nzb;
-        const long long waves = (cols * nzb + slots - 1) / slots;
-        const long long cost = waves * (zc + 3);
-        if (best_cost < 0 || cost < best_cost) best_cost = cost, best = zc;
-      }
-    }
-    gt.zc = best;
+    gt.zc = tb_zchunk(g, cols, slots);
     const dim3 gr((g.ex + G::OX - 1) / G::OX, (g.ey + G::OY - 1) / G::OY, (g.ez + gt.zc - 1) / gt.zc);
     nblk = (int)(gr.x * gr.y * gr.z);
     return std::make_pair(gr, gt);
@@ -1932,17 +2260,10 @@ static int launch_tb_rows(const BoxGeo& g, const OpParams& op, const double* b, 
     kern<<<gr, bl, smem, s>>>(maps, gt, op, xout, s_theta, c.c1, c.c2, dpart, dstride);
     return true;
   };
-  static int slots[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  static int slots[6] = {0, 0, 0, 0, 0, 0};
   const bool dots = dpart != nullptr && !pre;
   bool ok;
-  if (NR == tbf_rows() && !op.fc && !op.k && !op.S && tb_fast()) {  // constant coefficients: issue-lean kernel
-    if (pre)
-      ok = run(k_cheb2_fast<true, false, NR>, sizeof(TBFSmem<true, NR>), slots[6], false);
-    else if (dots)
-      ok = run(k_cheb2_fast<false, true, NR>, sizeof(TBFSmem<false, NR>), slots[7], true);
-    else
-      ok = run(k_cheb2_fast<false, false, NR>, sizeof(TBFSmem<false, NR>), slots[8], false);
-  } else if (op.fc) {
+  if (op.fc) {
     if (pre)
       ok = run(k_cheb2_tb<true, true, NR>, sizeof(TBSmem<NR, true>), slots[0], false);
     else if (dots)
@@ -1963,9 +2284,16 @@ static int launch_tb_rows(const BoxGeo& g, const OpParams& op, const double* b, 
 int launch_cheb2_tb(const BoxGeo& g, const OpParams& op, const double* b, const double* xin, double* xout,
                     double s_theta, ChebStep c, bool pre, cudaStream_t s, double* dpart, long long dstride, int dmax,
                     int* dblocks) {
-  const int nr = (!op.fc && !op.k && !op.S && tb_fast()) ? tbf_rows() : tb_rows();
+  const int nr = tb_rows();
   int nb;
-  if (nr >= 4 && tb_fits<4>(g))
+  const bool cc = !op.fc && !op.k && !op.S && tb_fast();  // constant coefficients: issue-lean kernel
+  if (cc && tbf_ty() == 2 && tbp_fits<2, 8>(g))
+    nb = launch_tbp<2, 8>(g, op, b, xin, xout, s_theta, c, pre, dpart, dstride, dmax, s);
+  else if (cc && tbf_ty() != 4 && tbf_fits<4, 8>(g))
+    nb = launch_tbf<4, 8>(g, op, b, xin, xout, s_theta, c, pre, dpart, dstride, dmax, s);
+  else if (cc && tbf_ty() == 4 && tbf_fits<4, 4>(g))
+    nb = launch_tbf<4, 4>(g, op, b, xin, xout, s_theta, c, pre, dpart, dstride, dmax, s);
+  else if (nr >= 4 && tb_fits<4>(g))
     nb = launch_tb_rows<4>(g, op, b, xin, xout, s_theta, c, pre, dpart, dstride, dmax, s);
   else if (nr >= 2 && tb_fits<2>(g))
     nb = launch_tb_rows<2>(g, op, b, xin, xout, s_theta, c, pre, dpart, dstride, dmax, s);
