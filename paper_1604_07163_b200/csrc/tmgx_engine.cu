@@ -1296,11 +1296,14 @@ int Solver::solve(const double* b, double* x, bool on_device, int method, double
   CK(cudaEventRecord(e0, W.stream));
   *its = 0;
   *reason = 2;  // max_its
-  // b -> cw (temporary), x0 -> cx
+  // b -> cw (temporary), x0 -> cx. With a zero initial guess r0 = b - A 0 = b bit for bit (every
+  // row sum is +0), so b goes straight into r and the residual pass is skipped.
+  const bool x0_zero = method != 5 && !(x && !seeded && x0_nonzero);
+  Field& bdst = x0_zero ? cr : cw;
   if (seeded) {
-    for (size_t q = 0; q < nb; ++q) W.cnt.launches += launch_fill_rhs(D.geo[q], cw.p[q], seed, true, W.stream);
+    for (size_t q = 0; q < nb; ++q) W.cnt.launches += launch_fill_rhs(D.geo[q], bdst.p[q], seed, true, W.stream);
   } else {
-    upload(0, cw, b, on_device);
+    upload(0, bdst, b, on_device);
   }
   int rc = 0;
   if (method == 5) {  // preonly: x = M b
@@ -1311,13 +1314,14 @@ int Solver::solve(const double* b, double* x, bool on_device, int method, double
     *its = 1;
     *norm0 = *normf = 0.0;
   } else {
-    if (x && !seeded && x0_nonzero)
+    if (!x0_zero) {
       upload(0, cx, x, on_device);
-    else
+      halo(0, cx);
+      for (size_t q = 0; q < nb; ++q)
+        W.cnt.launches += launch_residual(D.geo[q], top.op[q], cw.p[q], cx.p[q], cr.p[q], W.stream);
+    } else {
       for (size_t q = 0; q < nb; ++q) CK(cudaMemsetAsync(cx.p[q], 0, sizeof(double) * D.geo[q].total, W.stream));
-    halo(0, cx);
-    for (size_t q = 0; q < nb; ++q)
-      W.cnt.launches += launch_residual(D.geo[q], top.op[q], cw.p[q], cx.p[q], cr.p[q], W.stream);
+    }
     vcycle(0);
     cg_dots(CG_INIT);  // also sets beta = 0 so that the first p = z + 0 p = z
     CK(cudaMemcpyAsync(host_scal, scal, sizeof(double) * S_NSLOTS, cudaMemcpyDeviceToHost, W.stream));
