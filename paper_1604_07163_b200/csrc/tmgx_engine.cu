@@ -387,6 +387,7 @@ Solver::Solver(World& W_, const ProblemDesc& P, const MGDesc& M) : W(W_), prob(P
   if (const char* e = std::getenv("TMGX_TB_MIN")) tb_min_extent = std::atoi(e);
   if (const char* e = std::getenv("TMGX_FUSE_DOTS")) fuse_dots = std::string(e) != "0";
   if (const char* e = std::getenv("TMGX_FUSE_RR")) fuse_rr = std::string(e) != "0";
+  if (const char* e = std::getenv("TMGX_CC_MAX")) cc_max_extent = std::atoi(e);
   if (mgd.nlevels < 1) throw tmg::ConfigError("mg: number of levels must be >= 1");
   if (mgd.m < 1) throw tmg::ConfigError("mg: smoother iterations must be >= 1");
   if (prob.kind == 1) {
@@ -569,6 +570,7 @@ void Solver::build_nodes() {
     }
   }
   sync();
+  cc_from = coarse_chain_start();
 }
 
 // Cross-process wiring (P > 1): one mailbox allocation per process holds the rank_sums slots
@@ -901,6 +903,59 @@ void Solver::smooth(int i, bool zero_x) {
   }
 }
 
+// First node of the trailing chain that the fused coarse V-cycle can run: single-box SMOOTH
+// levels owned by this process, at most cc_max_extent vertices across (launch-latency bound),
+// down to the COARSE (LU) node. -1: none (or TMGX_CC_MAX=0).
+int Solver::coarse_chain_start() const {
+  if (cc_max_extent <= 0 || nodes.empty() || nodes.back().kind != COARSE || nodes.back().dist->local.size() != 1 ||
+      !coarse_cycle_supported(nodes.back().nc) || mgd.m - 1 > kCCMaxM)
+    return -1;
+  int i0 = -1;
+  for (int i = (int)nodes.size() - 2; i >= 0; --i) {
+    const Node& nd = nodes[i];
+    const Dist& D = *nd.dist;
+    if (nd.kind != SMOOTH || D.h.n_ranks() != 1 || D.local.size() != 1 || D.geo[0].ex > cc_max_extent ||
+        D.geo[0].ey > cc_max_extent || D.geo[0].ez > cc_max_extent || (int)nodes.size() - 1 - i > kCCMaxLev)
+      break;
+    i0 = i;
+  }
+  return i0;
+}
+
+// The fused coarse V-cycle from node i0 (see tmgx_kernels.cuh): the same Chebyshev coefficients as
+// smooth(), the nodes' b, x, r, d, d2 buffers, the coarse node's LU.
+void Solver::coarse_cycle(int i0) {
+  CCParams P{};
+  P.m = mgd.m;
+  P.nlev = (int)nodes.size() - 1 - i0;
+  for (int l = 0; l <= P.nlev; ++l) {
+    Node& nd = nodes[i0 + l];
+    CCLevel& L = P.L[l];
+    L.g = nd.dist->geo[0];
+    L.b = nd.b.p[0];
+    L.x = nd.x.p[0];
+    if (nd.kind == COARSE) break;
+    L.op = nd.op[0];
+    L.r = nd.r.p[0];
+    L.d = nd.d.p[0];
+    L.d2 = nd.d2.p[0];
+    const double theta = 0.5 * (nd.hi + nd.lo), delta = 0.5 * (nd.hi - nd.lo), sigma = theta / delta;
+    L.s_theta = 1.0 / theta;
+    double rho = 1.0 / sigma;
+    for (int it = 0; it < mgd.m - 1; ++it) {
+      const double rho_new = 1.0 / (2.0 * sigma - rho);
+      L.cs[it] = ChebStep{rho_new * rho, 2.0 * rho_new / delta};
+      rho = rho_new;
+    }
+  }
+  const Node& cn = nodes.back();
+  P.A = cn.A_dev;
+  P.piv = cn.piv_dev;
+  P.map = cn.map_dev;
+  P.nc = cn.nc;
+  W.cnt.launches += launch_coarse_cycle(P, W.stream);
+}
+
 // mg_apply (Alg. 1) over the node list; TELESCOPE nodes realise
 // TelescopePC::apply: gather, inner V-cycle on the members, scatter back.
 void Solver::vcycle(int i) {
@@ -908,6 +963,10 @@ void Solver::vcycle(int i) {
   if (i == 0) dots_nblk = 0;
   if (nd.kind == COARSE) {
     coarse_solve(i);
+    return;
+  }
+  if (i == cc_from) {
+    coarse_cycle(i);
     return;
   }
   if (nd.kind == TELESCOPE) {

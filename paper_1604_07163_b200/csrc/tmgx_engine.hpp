@@ -277,6 +277,11 @@ class Solver {
   bool fuse_rr = false;    // fused residual + restriction on single-box levels (TMGX_FUSE_RR=1; measured
                            // slower than residual + restriction on B200)
   bool use_tb(int i) const;
+  int cc_max_extent = 0;  // fused coarse V-cycle on single-box levels up to this size (TMGX_CC_MAX; off: measured
+                          // no faster than per-phase launches)
+  int cc_from = -1;        // first node of the fused coarse chain (set after setup)
+  int coarse_chain_start() const;
+  void coarse_cycle(int i0);
   ChebStep cheb_first_step(const Node& nd) const;
   cudaGraphExec_t iter_exec[2] = {nullptr, nullptr};  // one captured CG iteration per p parity
   long long iter_launches = 0;

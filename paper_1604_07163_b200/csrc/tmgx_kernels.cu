@@ -1964,6 +1964,244 @@ __global__ void k_lu_solve(const double* __restrict__ lu, const long long* __res
   for (int t = threadIdx.x; t < n; t += blockDim.x) x[map[t]] = y[n + t];
 }
 
+// ------------------------------------------------------------------------------------------
+// Fused coarse V-cycle (one cluster; see tmgx_kernels.cuh). Data written in the kernel is read
+// back by other CTAs after a cluster barrier (release/acquire), so every load here is a plain
+// coherent ld.global (no __ldg / non-coherent path).
+// ------------------------------------------------------------------------------------------
+constexpr int kCCThreads = 1024;
+
+__device__ __forceinline__ void cc_sync(unsigned ncta) {
+  if (ncta > 1)
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+  else
+    __syncthreads();
+}
+
+// A u at vertex (i, j, k) and the Jacobi reciprocal, exactly as k_march / k_march27 evaluate it.
+__device__ __forceinline__ double cc_row(const BoxGeo& g, const OpParams& op, const double* u, int i, int j, int k,
+                                         double& invd) {
+  const long long v = vidx(g, i, j, k);
+  if (op.S) {
+    double acc = 0.0;
+#pragma unroll
+    for (int s = 0; s < 27; ++s) {
+      const long long o = (long long)(s / 9 - 1) * g.pxy + (long long)((s / 3) % 3 - 1) * g.px + (s % 3 - 1);
+      acc += op.S[s * op.S_stride + v] * u[v + o];
+    }
+    invd = 1.0 / op.S[13 * op.S_stride + v];
+    return acc;
+  }
+  const Pt p = make_pt(g, i, j, k);
+  Coef c;
+  if (op.fc) {
+    const double *fD = op.fc, *fX = op.fc + op.fc_stride, *fY = op.fc + 2 * op.fc_stride, *fZ = op.fc + 3 * op.fc_stride;
+    c.dg = fD[v];
+    c.invd = 1.0 / c.dg;
+    c.azm = -fZ[v - g.pxy];
+    c.aym = -fY[v - g.px];
+    c.axm = -fX[v - 1];
+    c.axp = -fX[v];
+    c.ayp = -fY[v];
+    c.azp = -fZ[v];
+  } else {
+    c = coef_at<false>(op, p, 0, 0, 0, 0, 0, 0, 0);
+  }
+  invd = c.invd;
+  return row_apply(p, c, u[v - g.pxy], u[v - g.px], u[v - 1], u[v], u[v + 1], u[v + g.px], u[v + g.pxy]);
+}
+
+__device__ __forceinline__ double cc_invd(const BoxGeo& g, const OpParams& op, long long v) {
+  if (op.S) return 1.0 / op.S[13 * op.S_stride + v];
+  if (op.fc) return 1.0 / op.fc[v];
+  return op.cinvd;
+}
+
+template <class Fn>
+__device__ __forceinline__ void cc_for(const BoxGeo& g, unsigned gt, unsigned nt, Fn fn) {
+  const unsigned exy = (unsigned)g.ex * (unsigned)g.ey, n = exy * (unsigned)g.ez;
+  for (unsigned e = gt; e < n; e += nt) {
+    const unsigned k = e / exy, rem = e - k * exy, j = rem / (unsigned)g.ex, i = rem - j * (unsigned)g.ex;
+    fn((int)i, (int)j, (int)k);
+  }
+}
+
+__global__ void __launch_bounds__(kCCThreads, 1) k_coarse_cycle(const __grid_constant__ CCParams P, int parity) {
+  extern __shared__ double cc_sh[];
+  unsigned ncta = 1, rank = 0;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;\n" : "=r"(ncta));
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(rank));
+  const unsigned tid = threadIdx.x, gt = rank * blockDim.x + tid, nt = ncta * blockDim.x;
+  const int m = P.m;
+  double* dcur[kCCMaxLev];
+  double* dnxt[kCCMaxLev];
+  for (int l = 0; l < P.nlev; ++l) dcur[l] = P.L[l].d, dnxt[l] = P.L[l].d2;
+
+  // Chebyshev passes after the start (solver.cpp:100-110); first_zero: x = 0, r = b before it
+  auto passes = [&](int l, bool from_zero) {
+    const CCLevel& L = P.L[l];
+    for (int it = 0; it < m - 1; ++it) {
+      const bool first_zero = from_zero && it == 0, last = it == m - 2;
+      const double c1 = L.cs[it].c1, c2 = L.cs[it].c2;
+      const double* d = dcur[l];
+      double* dn = dnxt[l];
+      cc_for(L.g, gt, nt, [&](int i, int j, int k) {
+        const long long v = vidx(L.g, i, j, k);
+        double invd;
+        const double au = cc_row(L.g, L.op, d, i, j, k, invd);
+        const double uc = d[v];
+        const double x1 = first_zero ? uc : L.x[v] + uc;
+        const double r1 = (first_zero ? L.b[v] : L.r[v]) - au;
+        const double z = r1 * invd;
+        const double dnew = c1 * uc + c2 * z;
+        if (last) {
+          L.x[v] = x1 + dnew;
+        } else {
+          L.x[v] = x1;
+          L.r[v] = r1;
+          dn[v] = dnew;
+        }
+      });
+      dcur[l] = dn;
+      dnxt[l] = const_cast<double*>(d);
+      cc_sync(ncta);
+    }
+  };
+
+  // ---- down: pre-smooth from zero, residual, restriction
+  for (int l = 0; l < P.nlev; ++l) {
+    const CCLevel& L = P.L[l];
+    double* start = m == 1 ? L.x : dcur[l];
+    cc_for(L.g, gt, nt, [&](int i, int j, int k) {  // k_cheb_start_zero
+      const long long v = vidx(L.g, i, j, k);
+      start[v] = (L.b[v] * cc_invd(L.g, L.op, v)) * L.s_theta;
+    });
+    cc_sync(ncta);
+    passes(l, true);
+    cc_for(L.g, gt, nt, [&](int i, int j, int k) {  // residual (FApply<1>)
+      double invd;
+      const double au = cc_row(L.g, L.op, L.x, i, j, k, invd);
+      const long long v = vidx(L.g, i, j, k);
+      L.r[v] = L.b[v] - au;
+    });
+    cc_sync(ncta);
+    const CCLevel& C = P.L[l + 1];
+    cc_for(C.g, gt, nt, [&](int I, int J, int K) {  // k_restrict (R = 2^-3 P^T)
+      const BoxGeo& F = L.g;
+      const int GI = C.g.gx + I, GJ = C.g.gy + J, GK = C.g.gz + K;
+      double acc = 0.0;
+      for (int dk = -1; dk <= 1; ++dk) {
+        const int fk = 2 * GK + dk;
+        if (fk < 0 || fk >= F.Nz) continue;
+        const double wz = dk == 0 ? 1.0 : 0.5;
+        for (int dj = -1; dj <= 1; ++dj) {
+          const int fj = 2 * GJ + dj;
+          if (fj < 0 || fj >= F.Ny) continue;
+          const double wy = dj == 0 ? 1.0 : 0.5;
+          const long long row = vidx(F, 0, fj - F.gy, fk - F.gz);
+          for (int di = -1; di <= 1; ++di) {
+            const int fi = 2 * GI + di;
+            if (fi < 0 || fi >= F.Nx) continue;
+            const double wx = di == 0 ? 1.0 : 0.5;
+            const double w = wx * wy * wz;
+            acc += w * L.r[row + (fi - F.gx)];
+          }
+        }
+      }
+      C.b[vidx(C.g, I, J, K)] = 0.125 * acc;
+    });
+    cc_sync(ncta);
+  }
+
+  // ---- coarse direct solve on L[nlev]
+  {
+    const CCLevel& C = P.L[P.nlev];
+    const int n = P.nc;
+    if (!parity) {  // k_dense_matvec: one warp per row, fixed shuffle tree
+      const unsigned lane = tid & 31;
+      for (unsigned w = gt >> 5; w < (unsigned)n; w += nt >> 5) {
+        double acc = 0.0;
+        for (int c = lane; c < n; c += 32) acc += P.A[(long long)w * n + c] * C.b[P.map[c]];
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+        if (lane == 0) C.x[P.map[w]] = acc;
+      }
+    } else if (rank == 0) {  // k_lu_solve: DenseLU::solve order (precond.cpp:50-66)
+      double* y = cc_sh;
+      const double* lu = P.A;
+      for (int t = tid; t < n; t += blockDim.x) y[t] = C.b[P.map[t]];
+      __syncthreads();
+      if (tid == 0)
+        for (int k = 0; k < n; ++k) {
+          const long long p = P.piv[k];
+          if (p != k) {
+            const double tmp = y[k];
+            y[k] = y[p];
+            y[p] = tmp;
+          }
+        }
+      __syncthreads();
+      for (int j = 0; j < n; ++j) {
+        const double yj = y[j];
+        for (int k = j + 1 + tid; k < n; k += blockDim.x) y[k] -= lu[(long long)k * n + j] * yj;
+        __syncthreads();
+      }
+      if (tid == 0)
+        for (int k = n - 1; k >= 0; --k) {
+          double acc = y[k];
+          for (int j = k + 1; j < n; ++j) acc -= lu[(long long)k * n + j] * y[n + j];
+          y[n + k] = acc / lu[(long long)k * n + k];
+        }
+      __syncthreads();
+      for (int t = tid; t < n; t += blockDim.x) C.x[P.map[t]] = y[n + t];
+    }
+    cc_sync(ncta);
+  }
+
+  // ---- up: prolongation x += P x_c, post-smooth
+  for (int l = P.nlev - 1; l >= 0; --l) {
+    const CCLevel& L = P.L[l];
+    const CCLevel& C = P.L[l + 1];
+    cc_for(L.g, gt, nt, [&](int i, int j, int k) {  // k_prolong_add
+      const BoxGeo& F = L.g;
+      const int fx = F.gx + i, fy = F.gy + j, fz = F.gz + k;
+      const int nx = 1 + (fx & 1), ny = 1 + (fy & 1), nz = 1 + (fz & 1);
+      const int cx0 = (fx >> 1) - C.g.gx, cy0 = (fy >> 1) - C.g.gy, cz0 = (fz >> 1) - C.g.gz;
+      const double wx = nx == 2 ? 0.5 : 1.0, wy = ny == 2 ? 0.5 : 1.0, wz = nz == 2 ? 0.5 : 1.0;
+      double acc = 0.0;
+      for (int tz = 0; tz < nz; ++tz)
+        for (int ty = 0; ty < ny; ++ty) {
+          const double* row = C.x + vidx(C.g, cx0, cy0 + ty, cz0 + tz);
+          for (int tx = 0; tx < nx; ++tx) {
+            const double ww = wx * wy * wz;
+            acc += ww * row[tx];
+          }
+        }
+      const long long v = vidx(F, i, j, k);
+      L.x[v] = L.x[v] + acc;
+    });
+    cc_sync(ncta);
+    double* d0 = dcur[l];
+    cc_for(L.g, gt, nt, [&](int i, int j, int k) {  // k_cheb_start_res (FStartRes)
+      double invd;
+      const double au = cc_row(L.g, L.op, L.x, i, j, k, invd);
+      const long long v = vidx(L.g, i, j, k);
+      const double rr = L.b[v] - au;
+      L.r[v] = rr;
+      d0[v] = (rr * invd) * L.s_theta;
+    });
+    cc_sync(ncta);
+    if (m == 1) {
+      cc_for(L.g, gt, nt, [&](int i, int j, int k) {  // k_axpy(1.0, d, x)
+        const long long v = vidx(L.g, i, j, k);
+        L.x[v] += 1.0 * d0[v];
+      });
+      cc_sync(ncta);
+    } else {
+      passes(l, false);
+    }
+  }
+}
+
 }  // namespace
 
 // ============================================================================================
@@ -2459,6 +2697,47 @@ int launch_lu_solve(const double* lu, const long long* piv, int n, const long lo
   const size_t shmem = sizeof(double) * 2 * (size_t)n;
   if (shmem > 48 * 1024) cudaFuncSetAttribute(k_lu_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem);
   k_lu_solve<<<1, 256, shmem, s>>>(lu, piv, n, map, b, x);
+  return 1;
+}
+
+// The cluster: 8 CTAs x 1024 threads (portable cluster size); the parity build's serial LU needs
+// 2 nc doubles of shared memory on CTA 0.
+static int cc_cluster() {
+  static const int c = [] {
+    const char* e = std::getenv("TMGX_CC_CLUSTER");
+    return e ? std::max(1, std::min(16, std::atoi(e))) : 8;
+  }();
+  return c;
+}
+bool coarse_cycle_supported(int nc) { return 2 * (long long)nc * 8 <= 200 * 1024; }
+
+int launch_coarse_cycle(const CCParams& p, cudaStream_t s) {
+  const size_t shmem = 2 * (size_t)p.nc * sizeof(double);
+  static size_t shmem_set = 0;
+  static bool np_set = false;
+  if (!np_set) {  // cluster sizes above 8 are non-portable (B200 allows 16)
+    cudaFuncSetAttribute(k_coarse_cycle, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    np_set = true;
+  }
+  if (shmem > 48 * 1024 && shmem > shmem_set) {
+    cudaFuncSetAttribute(k_coarse_cycle, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem);
+    shmem_set = shmem;
+  }
+  cudaLaunchConfig_t cfg{};
+  const int cl = cc_cluster();
+  cfg.gridDim = dim3(cl, 1, 1);
+  cfg.blockDim = dim3(kCCThreads, 1, 1);
+  cfg.dynamicSmemBytes = shmem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cl;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, k_coarse_cycle, p, parity_build() ? 1 : 0);
+  if (e != cudaSuccess) throw std::runtime_error(std::string("coarse cycle launch: ") + cudaGetErrorString(e));
   return 1;
 }
 

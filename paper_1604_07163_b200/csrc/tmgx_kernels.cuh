@@ -180,6 +180,30 @@ int launch_dense_matvec(const double* A, int n, const long long* map, const doub
 int launch_lu_solve(const double* lu, const long long* piv, int n, const long long* map, const double* b,
                     double* x, cudaStream_t s);
 
+// Fused coarse V-cycle: every single-box level from L[0] (finest of the group) down to the coarse
+// LU, run by one thread-block cluster with cluster barriers between dependent phases instead of
+// one kernel launch per phase (levels <= 33^3 are launch-latency bound). Same arithmetic as the
+// per-phase kernels (bitwise identical in both builds).
+constexpr int kCCMaxLev = 6, kCCMaxM = 6;
+struct CCLevel {
+  BoxGeo g;
+  OpParams op;
+  double *b, *x, *r, *d, *d2;
+  double s_theta;
+  ChebStep cs[kCCMaxM];  // Chebyshev pass coefficients (solver.cpp:90-93, 106-108)
+};
+struct CCParams {
+  int nlev;               // smoothing levels; L[nlev] is the coarse (LU) level (g, b, x only)
+  int m;                  // smoothing passes per side
+  CCLevel L[kCCMaxLev + 1];
+  const double* A;        // Ainv (perf) or LU factors (parity)
+  const long long* piv;
+  const long long* map;
+  int nc;
+};
+bool coarse_cycle_supported(int nc);
+int launch_coarse_cycle(const CCParams& p, cudaStream_t s);
+
 bool parity_build();
 
 }  // namespace tmgx

@@ -80,3 +80,13 @@ def test_cross_process_bitwise():
     other = json.loads(out.stdout.strip().splitlines()[-1])
     for n in names:
         assert other[n] == _digest(*_solve(n)[1:]), n
+
+
+@pytest.mark.parametrize("name", ["cfg1", "galerkin129"])
+def test_fused_coarse_cycle_bitwise(name, monkeypatch):
+    """The cluster-resident coarse V-cycle (TMGX_CC_MAX) runs the per-phase kernels' arithmetic:
+    a solve with it is bit for bit the solve without it."""
+    monkeypatch.setenv("TMGX_CC_MAX", "0")
+    ref = _digest(*_solve(name)[1:])
+    monkeypatch.setenv("TMGX_CC_MAX", "33")
+    assert _digest(*_solve(name)[1:]) == ref
