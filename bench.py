@@ -378,9 +378,15 @@ def main():
     # The finest level runs the temporally blocked post-smooth (TMA-staged, 24 B/pt) when the
     # blocked smoother applies (m = 2, single-box level), else the fused Chebyshev pass.
     peak, peak_kind = read_peaks()
-    tb = m == 2 and world == 1 and os.environ.get("TMGX_TB", "1") != "0" and not galerkin
-    dom_id, dom_key, dom_name = ((9, "tb_post", "k_cheb2_fast<post> (blocked V(2,2) post-smooth, TMA-staged, fine level)") if tb
-                                 else (1, "cheb_step_last", "k_cheb_step (last pass, fine level)"))
+    tb = m in (2, 3) and world == 1 and os.environ.get("TMGX_TB", "1") != "0"
+    if tb and m == 3:
+        dom_id, dom_key, dom_name = (13, "tb3_post", "k_cheb3_tb<post> (blocked V(3,3) post-smooth, TMA-staged "
+                                     "b, x~ and row planes, fine level)")
+    elif tb:
+        dom_id, dom_key, dom_name = (9, "tb_post", "k_cheb2_fast<post> (blocked V(2,2) post-smooth, TMA-staged, fine level)"
+                                     if kind == 0 else "k_cheb2_tb<post> (blocked V(2,2) post-smooth, fine level)")
+    else:
+        dom_id, dom_key, dom_name = (1, "cheb_step_last", "k_cheb_step (last pass, fine level)")
     ms, by = s.bench_kernel(dom_id, nlevels - 1, iters=20)
     ms_all = max_over_ranks(ms)
     achieved = by / (ms_all * 1e-3) / 1e9
@@ -393,7 +399,11 @@ def main():
     # every fine-level kernel of the path: live us/launch and algorithmic GB/s
     kernels = {}
     names = {1: "cheb_step_last", 3: "residual", 4: "restrict", 5: "prolong_add", 6: "cg_update", 7: "spmv_dot",
-             8: "tb_pre", 9: "tb_post", 10: "prolong_to", 11: "resid_restrict"}
+             8: "tb_pre", 9: "tb_post", 10: "prolong_to", 11: "resid_restrict", 12: "tb3_pre", 13: "tb3_post"}
+    if m == 3:
+        names = {k: v for k, v in names.items() if k not in (8, 9)}
+    else:
+        names = {k: v for k, v in names.items() if k not in (12, 13)}
     for kid, kname in names.items():
         try:
             kms, kby = s.bench_kernel(kid, nlevels - 1, iters=10)
@@ -421,7 +431,10 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": dom_name, "peak_kind": peak_kind,
-                         "bytes_per_launch": by, "ms_per_launch": ms_all, "fine_level_kernels": kernels},
+                         "bytes_per_launch": by, "ms_per_launch": ms_all, "fine_level_kernels": kernels,
+                         "bytes_note": ("algorithmic bytes count the coefficient as 8 B/pt (k, SURVEY §8(d)); the "
+                                        "var-coef kernels stream 4 precomputed row planes (32 B/pt)" if kind == 1
+                                        else "algorithmic bytes (SURVEY §8(d))")},
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
         }

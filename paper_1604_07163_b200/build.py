@@ -76,7 +76,9 @@ def build(parity=False, verbose=False, force=False):
 
 
 def build_all(verbose=False, force=False):
-    return [build(False, verbose, force), build(True, verbose, force)]
+    with ThreadPoolExecutor(max_workers=2) as ex:  # the two builds in parallel
+        fut = [ex.submit(build, p, verbose, force) for p in (False, True)]
+        return [f.result() for f in fut]
 
 
 if __name__ == "__main__":

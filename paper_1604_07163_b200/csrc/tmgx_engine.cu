@@ -385,6 +385,7 @@ Solver::Solver(World& W_, const ProblemDesc& P, const MGDesc& M) : W(W_), prob(P
   if (const char* e = std::getenv("TMGX_TB")) tb_enabled = std::string(e) != "0";
   if (const char* e = std::getenv("TMGX_FUSE_CG")) fuse_cg = std::string(e) != "0";
   if (const char* e = std::getenv("TMGX_TB_MIN")) tb_min_extent = std::atoi(e);
+  if (const char* e = std::getenv("TMGX_TB3")) tb3_enabled = std::string(e) != "0";
   if (const char* e = std::getenv("TMGX_FUSE_DOTS")) fuse_dots = std::string(e) != "0";
   if (const char* e = std::getenv("TMGX_FUSE_RR")) fuse_rr = std::string(e) != "0";
   if (const char* e = std::getenv("TMGX_CC_MAX")) cc_max_extent = std::atoi(e);
@@ -866,12 +867,9 @@ void Solver::smooth(int i, bool zero_x) {
   const double s_theta = 1.0 / theta;
   const size_t nb = D.local.size();
   if (use_tb(i)) {  // one temporally blocked kernel per side (bitwise identical arithmetic)
-    const ChebStep cs = cheb_first_step(nd);
     if (!zero_x)  // the kernel reads x out of place
       for (size_t q = 0; q < nb; ++q) W.cnt.launches += launch_copy_interior(D.geo[q], nd.x.p[q], nd.d.p[q], W.stream);
-    for (size_t q = 0; q < nb; ++q)
-      W.cnt.launches += launch_cheb2_tb(D.geo[q], nd.op[q], nd.b.p[q], nd.d.p[q], nd.x.p[q], s_theta, cs, zero_x,
-                                        W.stream);
+    for (size_t q = 0; q < nb; ++q) tb_side(nd, q, nd.d.p[q], nd.x.p[q], zero_x);
     return;
   }
   if (zero_x) {
@@ -980,22 +978,16 @@ void Solver::vcycle(int i) {
   if (use_tb(i)) {
     // blocked pre-smooth b -> d (x after pre-smoothing), residual, restriction, coarse
     // correction x~ = d + P x_c into r (free after the restriction), blocked post-smooth r -> x
-    const ChebStep cs = cheb_first_step(nd);
-    const double s_theta = 1.0 / (0.5 * (nd.hi + nd.lo));
-    for (size_t q = 0; q < D.local.size(); ++q)
-      W.cnt.launches += launch_cheb2_tb(D.geo[q], nd.op[q], nd.b.p[q], nullptr, nd.d.p[q], s_theta, cs, true, W.stream);
+    for (size_t q = 0; q < D.local.size(); ++q) tb_side(nd, q, nullptr, nd.d.p[q], true);
     residual_restrict(i, nd.d);
     vcycle(i + 1);
     halo(i + 1, cn.x);
     for (size_t q = 0; q < D.local.size(); ++q)
       W.cnt.launches += launch_prolong_to(D.geo[q], cn.dist->geo[q], cn.x.p[q], nd.d.p[q], nd.r.p[q], W.stream);
     if (i == 0 && D.local.size() == 1 && !parity_build() && fuse_dots)  // + the CG's r.z, z.z partials
-      W.cnt.launches += launch_cheb2_tb(D.geo[0], nd.op[0], nd.b.p[0], nd.r.p[0], nd.x.p[0], s_theta, cs, false,
-                                        W.stream, part + part_off[0], nblk_max, nblk_max, &dots_nblk);
+      tb_side(nd, 0, nd.r.p[0], nd.x.p[0], false, true);
     else
-      for (size_t q = 0; q < D.local.size(); ++q)
-        W.cnt.launches += launch_cheb2_tb(D.geo[q], nd.op[q], nd.b.p[q], nd.r.p[q], nd.x.p[q], s_theta, cs, false,
-                                          W.stream);
+      for (size_t q = 0; q < D.local.size(); ++q) tb_side(nd, q, nd.r.p[q], nd.x.p[q], false);
     return;
   }
   smooth(i, true);
@@ -1035,12 +1027,39 @@ ChebStep Solver::cheb_first_step(const Node& nd) const {
   return ChebStep{rho_new * rho, 2.0 * rho_new / delta};
 }
 
-// The temporally blocked m = 2 smoother runs on single-box levels of 7-point operators
-// (TMGX_TB=0 disables it).
+// The temporally blocked smoothers (m = 2 and m = 3) run on single-box levels of 7-point
+// operators (TMGX_TB=0 disables them).
 bool Solver::use_tb(int i) const {
   const Node& nd = nodes[i];
-  return tb_enabled && mgd.m == 2 && nd.kind == SMOOTH && nd.dist->h.n_ranks() == 1 && !nd.dist->local.empty() &&
-         nd.op[0].S == nullptr && cheb2_tb_supported(nd.dist->geo[0]) && nd.dist->geo[0].ex >= tb_min_extent;
+  if (!tb_enabled || nd.kind != SMOOTH || nd.dist->h.n_ranks() != 1 || nd.dist->local.empty() ||
+      nd.op[0].S != nullptr || nd.dist->geo[0].ex < tb_min_extent)
+    return false;
+  if (mgd.m == 2) return cheb2_tb_supported(nd.dist->geo[0]);
+  if (mgd.m == 3) return tb3_enabled && cheb3_tb_supported(nd.dist->geo[0]);
+  return false;
+}
+
+// One blocked smoother side on local box q: pre (x = 0): b -> xout; post: (b, xin) -> xout.
+// dots: also the CG's r.z, z.z block partials (finest level, single box).
+void Solver::tb_side(Node& nd, size_t q, const double* xin, double* xout, bool pre, bool dots) {
+  const Dist& D = *nd.dist;
+  const double s_theta = 1.0 / (0.5 * (nd.hi + nd.lo));
+  const ChebStep cs = cheb_first_step(nd);
+  double* dp = dots ? part + part_off[0] : nullptr;
+  const int dmax = dots ? nblk_max : 0;
+  int* nbp = dots ? &dots_nblk : nullptr;
+  if (mgd.m == 2) {
+    W.cnt.launches += launch_cheb2_tb(D.geo[q], nd.op[q], nd.b.p[q], xin, xout, s_theta, cs, pre, W.stream, dp,
+                                      nblk_max, dmax, nbp);
+    return;
+  }
+  // second step (solver.cpp:100-108 recurrence)
+  const double theta = 0.5 * (nd.hi + nd.lo), delta = 0.5 * (nd.hi - nd.lo), sigma = theta / delta;
+  const double rho1 = 1.0 / (2.0 * sigma - 1.0 / sigma);
+  const double rho2 = 1.0 / (2.0 * sigma - rho1);
+  const ChebStep cs2{rho2 * rho1, 2.0 * rho2 / delta};
+  W.cnt.launches += launch_cheb3_tb(D.geo[q], nd.op[q], nd.b.p[q], xin, xout, s_theta, cs, cs2, pre, W.stream, dp,
+                                    nblk_max, dmax, nbp);
 }
 
 // Cross-process scalar reduction: every process stores its rank slots into every peer's

@@ -270,6 +270,7 @@ class Solver {
   // CG iteration as one CUDA graph (TMGX_GRAPHS=0 disables capture)
   bool use_graphs = true;
   bool tb_enabled = true;  // temporally blocked V(2,2) smoother (TMGX_TB=0 disables)
+  bool tb3_enabled = true;  // temporally blocked V(3,3) smoother (TMGX_TB3=0 disables)
   int tb_min_extent = 0;    // blocked smoother only on levels at least this wide (TMGX_TB_MIN)
   bool fuse_dots = true;   // CG r.z, z.z from the finest blocked post-smooth (TMGX_FUSE_DOTS=0)
   int dots_nblk = 0;       // partials written by the last finest post-smooth (0: none)
@@ -277,6 +278,7 @@ class Solver {
   bool fuse_rr = false;    // fused residual + restriction on single-box levels (TMGX_FUSE_RR=1; measured
                            // slower than residual + restriction on B200)
   bool use_tb(int i) const;
+  void tb_side(Node& nd, size_t q, const double* xin, double* xout, bool pre, bool dots = false);
   int cc_max_extent = 0;  // fused coarse V-cycle on single-box levels up to this size (TMGX_CC_MAX; off: measured
                           // no faster than per-phase launches)
   int cc_from = -1;        // first node of the fused coarse chain (set after setup)

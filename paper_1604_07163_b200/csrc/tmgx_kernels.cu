@@ -223,9 +223,12 @@ __global__ void k_fill_faces(BoxGeo g, OpParams op, double* __restrict__ fc, lon
   const long long v = vidx(g, i, j, k);
   const double* K = op.k;
   const double kc = K[v];
-  fc[1 * st + v] = gi + 1 < g.Nx ? harm(kc, K[v + 1]) * op.ih2x : 0.0;
-  fc[2 * st + v] = gj + 1 < g.Ny ? harm(kc, K[v + g.px]) * op.ih2y : 0.0;
-  fc[3 * st + v] = gk + 1 < g.Nz ? harm(kc, K[v + g.pxy]) * op.ih2z : 0.0;
+  // couplings: zero across a Dirichlet vertex (boundary rows are diagonal-only,
+  // interior rows drop couplings to boundary vertices), so a row may sum all six terms
+  const bool bnd = gi == 0 || gj == 0 || gk == 0 || gi >= g.Nx - 1 || gj >= g.Ny - 1 || gk >= g.Nz - 1;
+  fc[1 * st + v] = !bnd && gi + 1 <= g.Nx - 2 ? harm(kc, K[v + 1]) * op.ih2x : 0.0;
+  fc[2 * st + v] = !bnd && gj + 1 <= g.Ny - 2 ? harm(kc, K[v + g.px]) * op.ih2y : 0.0;
+  fc[3 * st + v] = !bnd && gk + 1 <= g.Nz - 2 ? harm(kc, K[v + g.pxy]) * op.ih2z : 0.0;
   if (i >= 0 && j >= 0 && k >= 0) {
     const Pt p = make_pt(g, i, j, k);
     fc[v] = coef_at<true>(op, p, kc, K[v - 1], K[v + 1], K[v - g.px], K[v + g.px], K[v - g.pxy], K[v + g.pxy]).dg;
@@ -763,6 +766,574 @@ __global__ void __launch_bounds__(kTBNT, NR >= 4 ? 2 : (NR == 2 ? (PRE ? TMGX_TB
   }
   if (DOTS) {  // block reduction through the (now idle) d buffer: no extra shared memory, so the
                // dots variant keeps the plain kernel's 4 blocks per SM
+    __syncthreads();
+    double* sh = &S.d[0][0][0];
+    const double s0 = block_sum(dot_bz, sh);
+    const double s1 = block_sum(dot_zz, sh);
+    if (tid == 0) {
+      dpart[blk_linear()] = s0;
+      dpart[dstride + blk_linear()] = s1;
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// Temporally blocked m = 3 Chebyshev (round 2: the V(3,3) smoother of BASELINE configs[2], the
+// north-star problem). k_cheb2_tb with one more pass:
+//   pass 1 (32 x RY ring, plane p1):        r0 = b - A x0, d0 = D^-1 r0 / theta   (PRE: r0 = b)
+//   pass 2 (ring minus one, plane p1 - 1):  x1 = x0 + d0, r1 = r0 - A d0, d1 = c1 d0 + c2 D^-1 r1
+//   pass 3 (ring minus two = the 28 x (RY - 4) output tile, plane p1 - 2):
+//                                           x' = (x1 + d1) + (c1' d1 + c2' D^-1 (r1 - A d1))
+// d0 and d1 are exchanged in-plane through two double-buffered shared planes; every z neighbour
+// and the r / x values a point carries from one pass to the next stay in per-thread register
+// queues (one __syncthreads per plane). The arithmetic is the unfused kernels' sequence
+// (k_cheb_start_zero / FStartRes, then two FStep passes), so the parity build is bitwise
+// identical to them and to the oracle.
+// Every operand arrives by TMA, kTBPF plane groups ahead: b (32 x RY box from column ox - 2, the
+// ring), x~ (36 x (RY + 2) from column ox - 4: TMA needs an even start column) and, for variable
+// coefficients, the row planes D, FX (36 wide: the -x face is the left neighbour's +x face), FY
+// (RY + 1 rows: the -y face) and FZ (the -z face is the previous group's FZ). A plane step then
+// never waits on a global load: the unstaged r02 kernel, which read the coefficient planes from
+// global memory inside each barrier-synchronised step, was DRAM-latency bound on var-coef levels.
+// HBM per point: pre b -> x 16 B, post (b, x~) -> x 24 B, + 32 B of row planes (var-coef),
+// against 160 / 208 B + 3 x 32 B for the five unfused passes of a V(3,3) side pair.
+// ------------------------------------------------------------------------------------------
+#ifndef TMGX_T3_MINB
+#define TMGX_T3_MINB 2
+#endif
+constexpr int kT3SX = 36;  // staged x / FX width
+template <int NR, int TY>
+struct T3G {
+  static constexpr int RY = TY * NR;
+  static constexpr int OX = kTBX - 4, OY = RY - 4;
+  static constexpr int SY = RY + 2;
+  static constexpr int BB = kTBX * RY * 8, XB = kT3SX * SY * 8;
+  static constexpr int FXB = kT3SX * RY * 8, FYB = kTBX * (RY + 1) * 8;
+};
+template <int NR, int TY, bool PRE, bool VAR>
+struct alignas(128) T3Smem {
+  using G = T3G<NR, TY>;
+  // one ring of plane groups, sized for the longest lifetime: coefficient planes of p1, p1 - 1,
+  // p1 - 2 (VAR), x~ of groups t and t - 1 (POST), b of group t
+  static constexpr int NS = VAR ? kTBPF + 3 : (PRE ? kTBPF + 1 : kTBPF + 2);
+  static constexpr int NCS = VAR ? NS : 1;
+  alignas(128) unsigned char b[NS][tb_al128(G::BB)];
+  alignas(128) unsigned char x[PRE ? 1 : NS][tb_al128(G::XB)];
+  alignas(128) unsigned char cd[NCS][VAR ? tb_al128(G::BB) : 128];
+  alignas(128) unsigned char cx[NCS][VAR ? tb_al128(G::FXB) : 128];
+  alignas(128) unsigned char cy[NCS][VAR ? tb_al128(G::FYB) : 128];
+  alignas(128) unsigned char cz[NCS][VAR ? tb_al128(G::BB) : 128];
+  double d[2][G::RY][kTBX];  // d0 planes (pass 1 -> pass 2)
+  double e[2][G::RY][kTBX];  // d1 planes (pass 2 -> pass 3)
+  unsigned long long bar[NS];
+};
+struct T3Maps {  // TMA descriptors: b, x~ and the variable-coefficient row planes
+  CUtensorMap b, x, D, FX, FY, FZ;
+};
+
+template <bool VAR, bool PRE, int NR, int TY, bool DOTS = false>
+__global__ void __launch_bounds__(kTBX* TY, TY >= 16 ? 1 : TMGX_T3_MINB)
+    k_cheb3_tb(const __grid_constant__ T3Maps maps, BoxGeo g, OpParams op, double* __restrict__ xout, double s_theta,
+               double c1a, double c2a, double c1b, double c2b, double* __restrict__ dpart, long long dstride) {
+  using G = T3G<NR, TY>;
+  using SM = T3Smem<NR, TY, PRE, VAR>;
+  constexpr int NS = SM::NS;
+  extern __shared__ __align__(1024) unsigned char tb_smem_raw[];
+  SM& S = *reinterpret_cast<SM*>(tb_smem_raw);
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = tx + kTBX * ty;
+  const int ox = blockIdx.x * G::OX, oy = blockIdx.y * G::OY;
+  const int k0 = blockIdx.z * g.zc, k1 = min(k0 + g.zc, g.ez);
+  const int jr0 = ty * NR;  // first ring row of this thread
+  const int i = ox - 2 + tx, j0 = oy - 2 + jr0;
+  const int gi = g.gx + i;
+  const long long vrow = g.base + i + g.px * (long long)j0;
+  const bool in_x = gi >= 0 && gi < g.Nx, fast_x = gi >= 2 && gi <= g.Nx - 3;
+  const bool m2_x = tx >= 1 && tx <= kTBX - 2 && in_x;
+  const bool out_x = tx >= 2 && tx <= kTBX - 3 && i < g.ex;
+  unsigned in_y = 0, fast_y = 0, m2_y = 0, out_y = 0;
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    const int gj = g.gy + j0 + r, jr = jr0 + r;
+    in_y |= (gj >= 0 && gj < g.Ny) ? 1u << r : 0u;
+    fast_y |= (gj >= 2 && gj <= g.Ny - 3) ? 1u << r : 0u;
+    m2_y |= (jr >= 1 && jr <= G::RY - 2) ? 1u << r : 0u;
+    out_y |= (jr >= 2 && jr <= G::RY - 3 && j0 + r < g.ey) ? 1u << r : 0u;
+  }
+  if (!in_x) in_y = 0;
+  if (!fast_x) fast_y = 0;
+  m2_y &= in_y;
+  if (!m2_x) m2_y = 0;
+  if (!out_x) out_y = 0;
+
+  // step t brings group t = {b(t - LAG1), row planes (t - LAG1), x~(t)}; pass 1 on p1 = t - LAG1,
+  // pass 2 on p1 - 1, pass 3 on p1 - 2. Pass 1 covers [k0 - 2, k1 + 1], pass 2 [k0 - 1, k1],
+  // pass 3 [k0, k1). VAR: one leading group more (the -z faces of plane k0 - 2).
+  constexpr int LAG1 = PRE ? 0 : 1;
+  const int T0 = k0 - 2 - LAG1 - (VAR ? 1 : 0), T1 = k1 + 1 + LAG1;
+  const unsigned sbar = smem_u32(&S.bar[0]);
+  auto issue = [&](int t, int sl) {  // elected thread only
+    if (t > T1) return;
+    const unsigned bar = sbar + 8 * sl;
+    mbar_expect_tx(&S.bar[sl], G::BB + (PRE ? 0 : G::XB) + (VAR ? 2 * G::BB + G::FXB + G::FYB : 0));
+    const int zc = t - LAG1 + 1;
+    tma_load3(smem_u32(S.b[sl]), &maps.b, kXO + ox - 2, oy - 1, zc, bar);
+    if (!PRE) tma_load3(smem_u32(S.x[sl]), &maps.x, kXO + ox - 4, oy - 2, t + 1, bar);
+    if (VAR) {
+      tma_load3(smem_u32(S.cd[sl]), &maps.D, kXO + ox - 2, oy - 1, zc, bar);
+      tma_load3(smem_u32(S.cx[sl]), &maps.FX, kXO + ox - 4, oy - 1, zc, bar);
+      tma_load3(smem_u32(S.cy[sl]), &maps.FY, kXO + ox - 2, oy - 2, zc, bar);
+      tma_load3(smem_u32(S.cz[sl]), &maps.FZ, kXO + ox - 2, oy - 1, zc, bar);
+    }
+  };
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) mbar_init(&S.bar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    for (int s = 0; s < kTBPF; ++s) issue(T0 + s, s);
+  }
+  __syncthreads();
+
+  // row r of slot s (ring point of this thread), -z faces from slot sm; constant coefficients
+  // from op
+  auto coef = [&](int s, int sm, int r) -> Coef {
+    if (!VAR) return coef_fc<false>(g, op, 0);
+    const int jr = jr0 + r;
+    Coef c;
+    c.dg = reinterpret_cast<const double*>(S.cd[s])[jr * kTBX + tx];
+    c.invd = 1.0 / c.dg;
+    const double* FX = reinterpret_cast<const double*>(S.cx[s]) + jr * kT3SX + tx + 2;
+    const double* FY = reinterpret_cast<const double*>(S.cy[s]) + (jr + 1) * kTBX + tx;
+    c.azm = -reinterpret_cast<const double*>(S.cz[sm])[jr * kTBX + tx];
+    c.aym = -FY[-kTBX];
+    c.axm = -FX[-1];
+    c.axp = -FX[0];
+    c.ayp = -FY[0];
+    c.azp = -reinterpret_cast<const double*>(S.cz[s])[jr * kTBX + tx];
+    return c;
+  };
+
+  double xq0[NR], xq1[NR], xq2[NR];  // x~: planes p1 - 1, p1, p1 + 1 (POST)
+  double dq0[NR], dq1[NR], dq2[NR];  // d0: planes p2 - 1, p2, p2 + 1 = p1
+  double rq1[NR], rq2[NR];           // r0: planes p2, p1
+  double yq1[NR], yq2[NR];           // x1: planes p3, p2
+  double eq0[NR], eq1[NR], eq2[NR];  // d1: planes p3 - 1, p3, p3 + 1 = p2
+  double sq1[NR], sq2[NR];           // r1: planes p3, p2
+  double bq0[DOTS ? NR : 1], bq1[DOTS ? NR : 1], bq2[DOTS ? NR : 1];  // b: p3, p2, p1 (dots)
+  double zq1[VAR ? NR : 1], zq2[VAR ? NR : 1];  // -z face coefficient of planes p3, p2 (pass 2 -> 3)
+#pragma unroll
+  for (int r = 0; r < NR; ++r)
+    xq0[r] = xq1[r] = xq2[r] = dq0[r] = dq1[r] = dq2[r] = rq1[r] = rq2[r] = yq1[r] = yq2[r] = eq0[r] = eq1[r] =
+        eq2[r] = sq1[r] = sq2[r] = 0.0;
+#pragma unroll
+  for (int r = 0; r < (DOTS ? NR : 1); ++r) bq0[r] = bq1[r] = bq2[r] = 0.0;
+#pragma unroll
+  for (int r = 0; r < (VAR ? NR : 1); ++r) zq1[r] = zq2[r] = 0.0;
+  // slots of groups t, t + kTBPF, t - 1, t - 2
+  int sl = 0, isl = kTBPF, psl = NS - 1, ppsl = NS - 2;
+  unsigned ph = 0;
+  double dot_bz = 0.0, dot_zz = 0.0;
+  auto zin = [&](int p) { return g.gz + p >= 0 && g.gz + p < g.Nz; };
+  auto zfast = [&](int p) { return g.gz + p >= 2 && g.gz + p <= g.Nz - 3; };
+  for (int t = T0; t <= T1; ++t) {
+    const int p1 = t - LAG1, p2 = p1 - 1, p3 = p1 - 2;
+    mbar_wait(sbar + 8 * sl, ph);
+    __syncthreads();  // group t visible; the slot of group t - NS and the d / e planes of step t - 2 are free
+    if (tid == 0) {
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      issue(t + kTBPF, isl);
+    }
+    if (!PRE) {
+      const double* xs = reinterpret_cast<const double*>(S.x[sl]);
+#pragma unroll
+      for (int r = 0; r < NR; ++r) xq2[r] = xs[(jr0 + r + 1) * kT3SX + tx + 2];
+    }
+    // pass 1 on plane p1 (whole ring)
+    if (p1 >= k0 - 2) {
+      const bool in_z = zin(p1), fz = zfast(p1);
+      const double* bsm = reinterpret_cast<const double*>(S.b[sl]);
+      const double* X = reinterpret_cast<const double*>(S.x[psl]);  // x~ plane p1
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        double d0 = 0.0, rr = 0.0;
+        const double bb = bsm[(jr0 + r) * kTBX + tx];
+        if (DOTS) bq2[r] = bb;
+        if (((in_y >> r) & 1) && in_z) {
+          const Coef c = coef(sl, psl, r);
+          if (PRE) {
+            d0 = (bb * c.invd) * s_theta;
+            rr = bb;
+          } else {
+            const int ly = jr0 + r + 1, cx = tx + 2;
+            const double xw = X[ly * kT3SX + cx - 1], xe = X[ly * kT3SX + cx + 1];
+            const double xs_ = r == 0 ? X[(ly - 1) * kT3SX + cx] : xq1[r > 0 ? r - 1 : 0];
+            const double xn = r == NR - 1 ? X[(ly + 1) * kT3SX + cx] : xq1[r < NR - 1 ? r + 1 : 0];
+            double ax;
+            if (((fast_y >> r) & 1) && fz)
+              ax = row_full(c, xq0[r], xs_, xw, xq1[r], xe, xn, xq2[r]);
+            else
+              ax = row_apply(make_pt(g, i, j0 + r, p1), c, xq0[r], xs_, xw, xq1[r], xe, xn, xq2[r]);
+            rr = bb - ax;
+            d0 = (rr * c.invd) * s_theta;
+          }
+        }
+        dq2[r] = d0;
+        rq2[r] = rr;
+        S.d[p1 & 1][jr0 + r][tx] = d0;
+      }
+    }
+    // pass 2 on plane p2 (ring minus one); in-plane d0 of p2 came from step t - 1
+#pragma unroll
+    for (int r = 0; r < NR; ++r) yq2[r] = sq2[r] = eq2[r] = 0.0;
+    if (m2_y && p2 >= k0 - 1 && p2 <= k1 && zin(p2)) {
+      const bool fz = zfast(p2);
+      const double(*D)[kTBX] = S.d[p2 & 1];
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        if (!((m2_y >> r) & 1)) continue;
+        const Coef c = coef(psl, ppsl, r);
+        const double d0 = dq1[r];
+        const int jr = jr0 + r;
+        const double dw = D[jr][tx - 1], de = D[jr][tx + 1];
+        const double ds = r == 0 ? D[jr - 1][tx] : dq1[r > 0 ? r - 1 : 0];
+        const double dn_ = r == NR - 1 ? D[jr + 1][tx] : dq1[r < NR - 1 ? r + 1 : 0];
+        double ad;
+        if (((fast_y >> r) & 1) && fz)
+          ad = row_full(c, dq0[r], ds, dw, d0, de, dn_, dq2[r]);
+        else
+          ad = row_apply(make_pt(g, i, j0 + r, p2), c, dq0[r], ds, dw, d0, de, dn_, dq2[r]);
+        const double r1 = rq1[r] - ad;
+        const double z = r1 * c.invd;
+        yq2[r] = PRE ? d0 : xq0[r] + d0;
+        sq2[r] = r1;
+        eq2[r] = c1a * d0 + c2a * z;
+        if (VAR) zq2[VAR ? r : 0] = c.azm;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < NR; ++r) S.e[p2 & 1][jr0 + r][tx] = eq2[r];
+    // pass 3 on plane p3 (output tile); in-plane d1 of p3 came from step t - 1
+    if (out_y && p3 >= k0 && p3 < k1) {
+      const bool fz = zfast(p3);
+      const double(*E)[kTBX] = S.e[p3 & 1];
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        if (!((out_y >> r) & 1)) continue;
+        const long long v = vrow + g.px * r + g.pxy * (long long)p3;
+        Coef c = coef(ppsl, ppsl, r);
+        if (VAR) c.azm = zq1[VAR ? r : 0];  // the group of plane p3 - 1 has left the ring
+        const double d1 = eq1[r];
+        const double x2 = yq1[r] + d1;
+        const int jr = jr0 + r;
+        const double ew = E[jr][tx - 1], ee = E[jr][tx + 1];
+        const double es = r == 0 ? E[jr - 1][tx] : eq1[r > 0 ? r - 1 : 0];
+        const double en = r == NR - 1 ? E[jr + 1][tx] : eq1[r < NR - 1 ? r + 1 : 0];
+        double ae;
+        if (((fast_y >> r) & 1) && fz)
+          ae = row_full(c, eq0[r], es, ew, d1, ee, en, eq2[r]);
+        else
+          ae = row_apply(make_pt(g, i, j0 + r, p3), c, eq0[r], es, ew, d1, ee, en, eq2[r]);
+        const double r2 = sq1[r] - ae;
+        const double z = r2 * c.invd;
+        const double dn = c1b * d1 + c2b * z;
+        const double xo = x2 + dn;
+        xout[v] = xo;
+        if (DOTS) {
+          dot_bz += bq0[r] * xo;
+          dot_zz += xo * xo;
+        }
+      }
+    }
+    // rotate the queues and the slot ring
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      xq0[r] = xq1[r];
+      xq1[r] = xq2[r];
+      dq0[r] = dq1[r];
+      dq1[r] = dq2[r];
+      rq1[r] = rq2[r];
+      yq1[r] = yq2[r];
+      eq0[r] = eq1[r];
+      eq1[r] = eq2[r];
+      sq1[r] = sq2[r];
+    }
+#pragma unroll
+    for (int r = 0; r < (DOTS ? NR : 1); ++r) {
+      bq0[r] = bq1[r];
+      bq1[r] = bq2[r];
+    }
+#pragma unroll
+    for (int r = 0; r < (VAR ? NR : 1); ++r) zq1[r] = zq2[r];
+    ppsl = psl;
+    psl = sl;
+    if (++sl == NS) sl = 0, ph ^= 1u;
+    if (++isl == NS) isl = 0;
+  }
+  if (DOTS) {
+    __syncthreads();
+    double* sh = &S.d[0][0][0];
+    const double s0 = block_sum(dot_bz, sh);
+    const double s1 = block_sum(dot_zz, sh);
+    if (tid == 0) {
+      dpart[blk_linear()] = s0;
+      dpart[dstride + blk_linear()] = s1;
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// Issue-lean temporally blocked m = 3 Chebyshev for variable coefficients (the fine level of
+// BASELINE configs[2]). Same tiles, TMA groups and pass schedule as k_cheb3_tb, restructured to
+// cut the instructions per point (k_cheb3_tb<VAR> issued ~350 warp instructions per ring point
+// and plane at IPC 3, 2-3x over the HBM time of its 48-56 B/pt):
+//  * the stored face planes hold the COUPLINGS: zero across a Dirichlet vertex (k_fill_faces),
+//    so every row, interior or boundary, is the same 7-term sum with no topology masks. The
+//    partial sum of a row is never -0, so acc + (+-0) == acc bit for bit (contracted or not):
+//    the same values as the masked row. Out-of-grid ring points read D = 0 (ghost ring / TMA
+//    zero fill) and get invd = 0, hence d0 = d1 = 0 there.
+//  * 1/D is computed once per point (pass 1) and queued with D for passes 2 and 3; the -z face
+//    of a plane is the +z face of the previous one (queued too).
+//  * the plane loop is unrolled by three (queue period) so the register queues never move; every
+//    step computes all three passes unconditionally (prologue / epilogue steps on planes outside
+//    the chunk compute finite garbage that nothing valid reads: shared memory is zeroed first)
+//    and only the stores are predicated.
+// ------------------------------------------------------------------------------------------
+template <int NR, int TY, bool PRE>
+struct alignas(128) T3VSmem {
+  using G = T3G<NR, TY>;
+  static constexpr int NS = kTBPF + 3;  // row planes of p1, p1 - 1, p1 - 2 stay resident
+  alignas(128) unsigned char b[NS][tb_al128(G::BB)];
+  alignas(128) unsigned char x[PRE ? 1 : NS][tb_al128(G::XB)];
+  alignas(128) unsigned char cd[NS][tb_al128(G::BB)];
+  alignas(128) unsigned char cx[NS][tb_al128(G::FXB)];
+  alignas(128) unsigned char cy[NS][tb_al128(G::FYB)];
+  alignas(128) unsigned char cz[NS][tb_al128(G::BB)];
+  double d[2][G::RY + 2][kTBX];  // d0 planes, one pad row each side
+  double e[2][G::RY + 2][kTBX];  // d1 planes
+  unsigned long long bar[NS];
+};
+
+template <bool PRE, int NR, int TY, bool DOTS>
+__global__ void __launch_bounds__(kTBX* TY, 1)
+    k_cheb3_var(const __grid_constant__ T3Maps maps, BoxGeo g, OpParams, double* __restrict__ xout, double s_theta, double c1a,
+                double c2a, double c1b, double c2b, double* __restrict__ dpart, long long dstride) {
+  using G = T3G<NR, TY>;
+  using SM = T3VSmem<NR, TY, PRE>;
+  constexpr int NS = SM::NS;
+  extern __shared__ __align__(1024) unsigned char tb_smem_raw[];
+  SM& S = *reinterpret_cast<SM*>(tb_smem_raw);
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = tx + kTBX * ty;
+  const int ox = blockIdx.x * G::OX, oy = blockIdx.y * G::OY;
+  const int k0 = blockIdx.z * g.zc, k1 = min(k0 + g.zc, g.ez);
+  const int jr0 = ty * NR;
+  const int i = ox - 2 + tx, j0 = oy - 2 + jr0;
+  double* const orow = xout + g.base + i + g.px * (long long)j0;
+  const bool out_x = tx >= 2 && tx <= kTBX - 3 && i < g.ex;
+  bool out_r[NR];
+#pragma unroll
+  for (int r = 0; r < NR; ++r) out_r[r] = out_x && jr0 + r >= 2 && jr0 + r <= G::RY - 3 && j0 + r < g.ey;
+
+  constexpr int LAG1 = PRE ? 0 : 1;
+  const int T0 = k0 - 3, T1 = k1 + 1 + LAG1;  // pass 1 needs the -z faces / x~ of plane k0 - 3
+  const unsigned sbar = smem_u32(&S.bar[0]);
+  auto issue = [&](int t, int sl) {  // elected thread only
+    if (t > T1) return;
+    const unsigned bar = sbar + 8 * sl;
+    mbar_expect_tx(&S.bar[sl], 3 * G::BB + (PRE ? 0 : G::XB) + G::FXB + G::FYB);
+    const int zc = t - LAG1 + 1;
+    tma_load3(smem_u32(S.b[sl]), &maps.b, kXO + ox - 2, oy - 1, zc, bar);
+    if (!PRE) tma_load3(smem_u32(S.x[sl]), &maps.x, kXO + ox - 4, oy - 2, t + 1, bar);
+    tma_load3(smem_u32(S.cd[sl]), &maps.D, kXO + ox - 2, oy - 1, zc, bar);
+    tma_load3(smem_u32(S.cx[sl]), &maps.FX, kXO + ox - 4, oy - 1, zc, bar);
+    tma_load3(smem_u32(S.cy[sl]), &maps.FY, kXO + ox - 2, oy - 2, zc, bar);
+    tma_load3(smem_u32(S.cz[sl]), &maps.FZ, kXO + ox - 2, oy - 1, zc, bar);
+  };
+  {  // zero the whole staging area: steps outside the chunk read slots no group has filled yet
+    double* z = reinterpret_cast<double*>(tb_smem_raw);
+    const int n = (int)(offsetof(SM, bar) / sizeof(double));
+    for (int e = tid; e < n; e += kTBX * TY) z[e] = 0.0;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) mbar_init(&S.bar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    for (int s = 0; s < kTBPF; ++s) issue(T0 + s, s);
+  }
+  __syncthreads();
+
+  // register queues, slot = plane mod 3 relative to T0 - LAG1 (static after the unroll)
+  double XQ[3][NR], D0[3][NR], R0[3][NR], IV[3][NR], DG[3][NR], AZ[3][NR], D1[3][NR], R1[3][NR], X1[3][NR];
+  double CXM[3][NR], CXP[3][NR], CYM[3][NR], CYP[3][NR];  // in-plane couplings of p1, p1 - 1, p1 - 2
+  double BQ[3][DOTS ? NR : 1];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+#pragma unroll
+    for (int r = 0; r < NR; ++r)
+      XQ[a][r] = D0[a][r] = R0[a][r] = IV[a][r] = DG[a][r] = AZ[a][r] = D1[a][r] = R1[a][r] = X1[a][r] = CXM[a][r] =
+          CXP[a][r] = CYM[a][r] = CYP[a][r] = 0.0;
+#pragma unroll
+    for (int r = 0; r < (DOTS ? NR : 1); ++r) BQ[a][r] = 0.0;
+  }
+  int sl = 0, isl = kTBPF, psl = NS - 1, ppsl = NS - 2;
+  unsigned ph = 0;
+  double dot_bz = 0.0, dot_zz = 0.0;
+  const int cb = jr0 * kTBX + tx;            // this thread's first ring row in a 32-wide plane
+  const int cw = jr0 * kT3SX + tx + 2;       // ... in a 36-wide plane (FX)
+  const int xb = (jr0 + 1) * kT3SX + tx + 2;  // ... in the staged x~ plane (rows + 1)
+
+  auto step = [&](auto phase, int t) {
+    constexpr int P1 = decltype(phase)::value, P2 = (P1 + 2) % 3, P3 = (P1 + 1) % 3;
+    const int p1 = t - LAG1;
+    mbar_wait(sbar + 8 * sl, ph);
+    __syncthreads();  // group t visible; slot of group t - 3 and the d / e planes of step t - 2 free
+    if (tid == 0) {
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      issue(t + kTBPF, isl);
+    }
+    const double* Bs = reinterpret_cast<const double*>(S.b[sl]) + cb;
+    const double* Xs = reinterpret_cast<const double*>(S.x[sl]) + xb;   // x~(p1 + 1)
+    const double* Xp = reinterpret_cast<const double*>(S.x[psl]) + xb;  // x~(p1)
+    const double* Cd = reinterpret_cast<const double*>(S.cd[sl]) + cb;
+    const double* Cx1 = reinterpret_cast<const double*>(S.cx[sl]) + cw;
+    const double* Cy1 = reinterpret_cast<const double*>(S.cy[sl]) + cb;
+    const double* Cz = reinterpret_cast<const double*>(S.cz[sl]) + cb;
+    const double* Dd = &S.d[(p1 - 1) & 1][jr0 + 1][tx];  // d0(p2)
+    const double* Ee = &S.e[(p1 - 2) & 1][jr0 + 1][tx];  // d1(p3)
+    double* Dw = &S.d[p1 & 1][jr0 + 1][tx];
+    double* Ew = &S.e[(p1 - 1) & 1][jr0 + 1][tx];
+    // ---- pass 1 on p1: coefficients of p1 (1/D once), d0, r0
+    double fz3[NR];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const double bb = Bs[r * kTBX];
+      if (DOTS) BQ[P1][DOTS ? r : 0] = bb;
+      const double dg = Cd[r * kTBX];
+      const double fxm = Cx1[r * kT3SX - 1], fxp = Cx1[r * kT3SX];
+      const double fym = r == 0 ? Cy1[0] : CYP[P1][r > 0 ? r - 1 : 0], fyp = Cy1[(r + 1) * kTBX];
+      const double fzp = Cz[r * kTBX], fzm = AZ[P2][r];
+      CXM[P1][r] = fxm;
+      CXP[P1][r] = fxp;
+      CYM[P1][r] = fym;
+      CYP[P1][r] = fyp;
+      fz3[r] = AZ[P1][r];  // +z face of p1 - 3 = -z face of p3 (leaves the queue now)
+      AZ[P1][r] = fzp;
+      const double invd = dg != 0.0 ? 1.0 / dg : 0.0;
+      IV[P1][r] = invd;
+      DG[P1][r] = dg;
+      double d0, rr;
+      if (PRE) {
+        d0 = (bb * invd) * s_theta;
+        rr = bb;
+      } else {
+        const double xn1 = Xs[r * kT3SX];  // x~(p1 + 1), the next step's centre
+        const double xc = XQ[P1][r], xw = Xp[r * kT3SX - 1], xe = Xp[r * kT3SX + 1];
+        const double xs_ = r == 0 ? Xp[-kT3SX] : XQ[P1][r > 0 ? r - 1 : 0];
+        const double xn_ = r == NR - 1 ? Xp[NR * kT3SX] : XQ[P1][r < NR - 1 ? r + 1 : 0];
+        XQ[P3][r] = xn1;
+        double acc = 0.0;
+        acc += (-fzm) * XQ[P2][r];
+        acc += (-fym) * xs_;
+        acc += (-fxm) * xw;
+        acc += dg * xc;
+        acc += (-fxp) * xe;
+        acc += (-fyp) * xn_;
+        acc += (-fzp) * xn1;
+        rr = bb - acc;
+        d0 = (rr * invd) * s_theta;
+      }
+      D0[P1][r] = d0;
+      R0[P1][r] = rr;
+    }
+    // ---- pass 2 on p2 = p1 - 1: x1, r1, d1 (row planes of group t - 1; d0 of p2 in-plane)
+    double dwv[NR], dev[NR];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      dwv[r] = Dd[r * kTBX - 1];
+      dev[r] = Dd[r * kTBX + 1];
+    }
+    const double ds0 = Dd[-kTBX], dnN = Dd[NR * kTBX];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const double fxm = CXM[P2][r], fxp = CXP[P2][r], fym = CYM[P2][r], fyp = CYP[P2][r];
+      const double fzm = AZ[P3][r], fzp = AZ[P2][r];
+      const double d0 = D0[P2][r];
+      const double ds = r == 0 ? ds0 : D0[P2][r > 0 ? r - 1 : 0];
+      const double dn = r == NR - 1 ? dnN : D0[P2][r < NR - 1 ? r + 1 : 0];
+      double acc = 0.0;
+      acc += (-fzm) * D0[P3][r];
+      acc += (-fym) * ds;
+      acc += (-fxm) * dwv[r];
+      acc += DG[P2][r] * d0;
+      acc += (-fxp) * dev[r];
+      acc += (-fyp) * dn;
+      acc += (-fzp) * D0[P1][r];
+      const double r1 = R0[P2][r] - acc;
+      const double z = r1 * IV[P2][r];
+      const double d1 = c1a * d0 + c2a * z;
+      X1[P2][r] = PRE ? d0 : XQ[P2][r] + d0;
+      R1[P2][r] = r1;
+      D1[P2][r] = d1;
+    }
+    // ---- pass 3 on p3 = p1 - 2: the output (row planes of group t - 2; d1 of p3 in-plane)
+    double ewv[NR], eev[NR], xo[NR];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      ewv[r] = Ee[r * kTBX - 1];
+      eev[r] = Ee[r * kTBX + 1];
+    }
+    const double es0 = Ee[-kTBX], enN = Ee[NR * kTBX];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const double fxm = CXM[P3][r], fxp = CXP[P3][r], fym = CYM[P3][r], fyp = CYP[P3][r];
+      const double fzm = fz3[r], fzp = AZ[P3][r];
+      const double d1 = D1[P3][r];
+      const double es = r == 0 ? es0 : D1[P3][r > 0 ? r - 1 : 0];
+      const double en = r == NR - 1 ? enN : D1[P3][r < NR - 1 ? r + 1 : 0];
+      double acc = 0.0;
+      acc += (-fzm) * D1[P1][r];  // d1(p3 - 1): written when pass 2 ran on p1 - 3 (slot P1)
+      acc += (-fym) * es;
+      acc += (-fxm) * ewv[r];
+      acc += DG[P3][r] * d1;
+      acc += (-fxp) * eev[r];
+      acc += (-fyp) * en;
+      acc += (-fzp) * D1[P2][r];
+      const double r2 = R1[P3][r] - acc;
+      const double z = r2 * IV[P3][r];
+      const double dn = c1b * d1 + c2b * z;
+      xo[r] = (X1[P3][r] + d1) + dn;
+    }
+    // ---- stores: in-plane d0 / d1 for the next step, the output tile
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      Dw[r * kTBX] = D0[P1][r];
+      Ew[r * kTBX] = D1[P2][r];
+    }
+    const int p3 = p1 - 2;
+    if (p3 >= k0 && p3 < k1) {
+      double* o = orow + g.pxy * (long long)p3;
+#pragma unroll
+      for (int r = 0; r < NR; ++r)
+        if (out_r[r]) {
+          o[g.px * r] = xo[r];
+          if (DOTS) {
+            dot_bz += BQ[P3][DOTS ? r : 0] * xo[r];
+            dot_zz += xo[r] * xo[r];
+          }
+        }
+    }
+    ppsl = psl;
+    psl = sl;
+    if (++sl == NS) sl = 0, ph ^= 1u;
+    if (++isl == NS) isl = 0;
+  };
+  for (int t = T0;;) {
+    if (t > T1) break;
+    step(std::integral_constant<int, 0>{}, t++);
+    if (t > T1) break;
+    step(std::integral_constant<int, 1>{}, t++);
+    if (t > T1) break;
+    step(std::integral_constant<int, 2>{}, t++);
+  }
+  if (DOTS) {
     __syncthreads();
     double* sh = &S.d[0][0][0];
     const double s0 = block_sum(dot_bz, sh);
@@ -2359,10 +2930,8 @@ static CUtensorMap tensor_map(const BoxGeo& g, const double* base_ptr, int bx, i
 // function of the geometry and the kernel's residency, so repeated launches agree on the block
 // count and hence on the fused dot-product partials).
 static int tb_zchunk(const BoxGeo& g, long long cols, int slots) {
-  static const int zc_env = [] {
-    const char* e = std::getenv("TMGX_TB_ZC");
-    return e ? std::max(1, std::atoi(e)) : 0;
-  }();
+  const char* zce = std::getenv("TMGX_TB_ZC");  // read per launch (tests vary it in-process)
+  const int zc_env = zce ? std::max(1, std::atoi(zce)) : 0;
   if (zc_env) return std::min(zc_env, g.ez);
   int best = g.ez;
   long long best_cost = -1;
@@ -2542,6 +3111,103 @@ int launch_cheb2_tb(const BoxGeo& g, const OpParams& op, const double* b, const 
   if (nb < 0) {  // no room for the fused partials: plain launch
     nb = 0;
     launch_cheb2_tb(g, op, b, xin, xout, s_theta, c, pre, s);
+  }
+  if (dblocks) *dblocks = nb;
+  return 1;
+}
+
+// m = 3 blocked smoother: NR rows per thread, TY warps per block (TMGX_T3_NR / TMGX_T3_TY).
+template <int NR, int TY>
+static bool t3_fits(const BoxGeo& g) {
+  return g.px >= kT3SX && g.ey + 2 >= T3G<NR, TY>::SY;
+}
+static int t3_env(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : dflt;
+}
+bool cheb3_tb_supported(const BoxGeo& g) { return t3_fits<2, 8>(g); }
+
+template <int NR, int TY>
+static int launch_t3_rows(const BoxGeo& g, const OpParams& op, const double* b, const double* xin, double* xout,
+                          double s_theta, ChebStep c, ChebStep c2, bool pre, double* dpart, long long dstride,
+                          int dmax, cudaStream_t s) {
+  using G = T3G<NR, TY>;
+  T3Maps maps;
+  std::memset(&maps, 0, sizeof(maps));
+  maps.b = tensor_map(g, b, kTBX, G::RY);
+  if (!pre) maps.x = tensor_map(g, xin, kT3SX, G::SY);
+  if (op.fc) {
+    maps.D = tensor_map(g, op.fc, kTBX, G::RY);
+    maps.FX = tensor_map(g, op.fc + op.fc_stride, kT3SX, G::RY);
+    maps.FY = tensor_map(g, op.fc + 2 * op.fc_stride, kTBX, G::RY + 1);
+    maps.FZ = tensor_map(g, op.fc + 3 * op.fc_stride, kTBX, G::RY);
+  }
+  const bool dots = dpart != nullptr && !pre;
+  static int slots[6] = {0, 0, 0, 0, 0, 0};
+  int nblk = 0;
+  auto run = [&](auto kern, size_t smem, int& sl) {
+    if (!sl) {
+      int dev = 0, sms = 0, per = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kTBX * TY, smem);
+      sl = std::max(1, sms * std::max(per, 1));
+    }
+    const long long cols = (long long)((g.ex + G::OX - 1) / G::OX) * ((g.ey + G::OY - 1) / G::OY);
+    BoxGeo gt = g;
+    gt.zc = tb_zchunk(g, cols, sl);
+    const dim3 gr((g.ex + G::OX - 1) / G::OX, (g.ey + G::OY - 1) / G::OY, (g.ez + gt.zc - 1) / gt.zc);
+    nblk = (int)(gr.x * gr.y * gr.z);
+    if (dots && nblk > dmax) return false;  // partial buffer too small: caller falls back
+    kern<<<gr, dim3(kTBX, TY), smem, s>>>(maps, gt, op, xout, s_theta, c.c1, c.c2, c2.c1, c2.c2, dpart, dstride);
+    return true;
+  };
+  bool ok;
+  if (op.fc && t3_env("TMGX_T3_LEAN", 1)) {
+    if (pre)
+      ok = run(k_cheb3_var<true, NR, TY, false>, sizeof(T3VSmem<NR, TY, true>), slots[0]);
+    else if (dots)
+      ok = run(k_cheb3_var<false, NR, TY, true>, sizeof(T3VSmem<NR, TY, false>), slots[1]);
+    else
+      ok = run(k_cheb3_var<false, NR, TY, false>, sizeof(T3VSmem<NR, TY, false>), slots[2]);
+  } else if (op.fc) {
+    if (pre)
+      ok = run(k_cheb3_tb<true, true, NR, TY>, sizeof(T3Smem<NR, TY, true, true>), slots[0]);
+    else if (dots)
+      ok = run(k_cheb3_tb<true, false, NR, TY, true>, sizeof(T3Smem<NR, TY, false, true>), slots[1]);
+    else
+      ok = run(k_cheb3_tb<true, false, NR, TY>, sizeof(T3Smem<NR, TY, false, true>), slots[2]);
+  } else {
+    if (pre)
+      ok = run(k_cheb3_tb<false, true, NR, TY>, sizeof(T3Smem<NR, TY, true, false>), slots[3]);
+    else if (dots)
+      ok = run(k_cheb3_tb<false, false, NR, TY, true>, sizeof(T3Smem<NR, TY, false, false>), slots[4]);
+    else
+      ok = run(k_cheb3_tb<false, false, NR, TY>, sizeof(T3Smem<NR, TY, false, false>), slots[5]);
+  }
+  return ok ? (dots ? nblk : 0) : -1;
+}
+
+int launch_cheb3_tb(const BoxGeo& g, const OpParams& op, const double* b, const double* xin, double* xout,
+                    double s_theta, ChebStep c, ChebStep c2, bool pre, cudaStream_t s, double* dpart,
+                    long long dstride, int dmax, int* dblocks) {
+  if (op.S || (op.k && !op.fc)) throw std::runtime_error("blocked m = 3 smoother: 7-point rows (fc or constant) only");
+  // variable coefficients: one 16-warp block per SM (the staged row planes fill shared memory);
+  // constant: 8-warp blocks, 2 per SM
+  const int nr = t3_env("TMGX_T3_NR", op.fc ? 1 : 2), ty = t3_env("TMGX_T3_TY", op.fc ? 16 : 8);
+  int nb;
+  if (nr == 1 && ty == 16 && t3_fits<1, 16>(g))
+    nb = launch_t3_rows<1, 16>(g, op, b, xin, xout, s_theta, c, c2, pre, dpart, dstride, dmax, s);
+  else if (nr == 2 && ty == 16 && t3_fits<2, 16>(g))
+    nb = launch_t3_rows<2, 16>(g, op, b, xin, xout, s_theta, c, c2, pre, dpart, dstride, dmax, s);
+  else if (t3_fits<2, 8>(g))
+    nb = launch_t3_rows<2, 8>(g, op, b, xin, xout, s_theta, c, c2, pre, dpart, dstride, dmax, s);
+  else
+    throw std::runtime_error("blocked m = 3 smoother: level too small for the TMA boxes");
+  if (nb < 0) {
+    nb = 0;
+    launch_cheb3_tb(g, op, b, xin, xout, s_theta, c, c2, pre, s);
   }
   if (dblocks) *dblocks = nb;
   return 1;

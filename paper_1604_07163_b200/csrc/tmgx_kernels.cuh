@@ -99,6 +99,11 @@ int launch_cheb2_tb(const BoxGeo& g, const OpParams& op, const double* b, const 
                     double s_theta, ChebStep c, bool pre, cudaStream_t s, double* dpart = nullptr,
                     long long dstride = 0, int dmax = 0, int* dblocks = nullptr);
 bool cheb2_tb_supported(const BoxGeo& g);
+// Temporally blocked m = 3 Chebyshev side (same contract; c = first step, c2 = second step).
+int launch_cheb3_tb(const BoxGeo& g, const OpParams& op, const double* b, const double* xin, double* xout,
+                    double s_theta, ChebStep c, ChebStep c2, bool pre, cudaStream_t s, double* dpart = nullptr,
+                    long long dstride = 0, int dmax = 0, int* dblocks = nullptr);
+bool cheb3_tb_supported(const BoxGeo& g);
 // xo = xf + P xc (out of place)
 int launch_prolong_to(const BoxGeo& fine, const BoxGeo& coarse, const double* xc, const double* xf, double* xo,
                       cudaStream_t s);

@@ -94,6 +94,27 @@ def test_smoother(parity, kind, m):
 
 
 @pytest.mark.parametrize("parity", [True, False])
+@pytest.mark.parametrize("kind", KINDS)
+@pytest.mark.parametrize("zc", [None, "3", "64"])
+def test_smoother_blocked_m3(parity, kind, zc, monkeypatch):
+    """The temporally blocked V(3,3) smoother (k_cheb3_tb: three Chebyshev passes per kernel) on a
+    level wide enough for it, odd extents, z-chunks of 1 plane (default split), 3 and all planes:
+    bitwise the oracle in the parity build, 1e-12 in the performance build, from x = 0 and from
+    a non-zero x."""
+    if zc:
+        monkeypatch.setenv("TMGX_TB_ZC", zc)
+    np3, nl = (65, 41, 49), 3
+    om = oracle_mg(np3, nl, kind[1], m=3)
+    w, s = make(np3, nl, kind[0], m=3, parity=parity, bounds=oracle_bounds(om, nl))
+    rng = np.random.default_rng(5)
+    n = om.level_size(2)
+    b = rng.standard_normal(n)
+    check(s.level_smooth(2, b), om.smooth(2, b), parity)
+    x0 = rng.standard_normal(n)
+    check(s.level_smooth(2, b, x0), om.smooth(2, b, x0), parity)
+
+
+@pytest.mark.parametrize("parity", [True, False])
 def test_transfer_and_coarse(parity):
     np3, nl = (17, 33, 17), 3
     om = oracle_mg(np3, nl, O.VARCOEF7)
