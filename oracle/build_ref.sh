@@ -33,3 +33,13 @@ done
 for p in "${pids[@]}"; do wait "$p"; done
 $CXX $FLAGS "$HERE/ref_glue/tmg_ref_bench.cpp" "$OUT"/obj/*.o -o "$OUT/tmg_ref_bench"
 echo "build_ref: $OUT/tmg_ref_bench"
+# the reference-side binding of the drop-in against the built libtmgx.so
+LIB="$HERE/../paper_1604_07163_b200"
+if [ -f "$LIB/libtmgx.so" ]; then
+  $CXX $FLAGS -I"$HERE/../include" "$HERE/ref_glue/tmg_ref_gpupc.cpp" "$OUT"/obj/*.o -L"$LIB" -ltmgx \
+    -Wl,-rpath,'$ORIGIN/../../paper_1604_07163_b200' -ldl -lrt -o "$OUT/tmg_ref_gpupc"
+  echo "build_ref: $OUT/tmg_ref_gpupc"
+  $CXX $FLAGS -I"$HERE/../include" "$HERE/ref_glue/tmg_ref_gpupc.cpp" "$OUT"/obj/*.o -L"$LIB" -l:libtmgx_parity.so \
+    -Wl,-rpath,'$ORIGIN/../../paper_1604_07163_b200' -ldl -lrt -o "$OUT/tmg_ref_gpupc_parity"
+  echo "build_ref: $OUT/tmg_ref_gpupc_parity"
+fi

@@ -242,6 +242,7 @@ double now() {
 
 }  // namespace
 
+#ifndef TMG_REF_NO_MAIN
 int main(int argc, char** argv) {
   if (argc < 7) {
     std::fprintf(stderr, "usage: %s N nlevels m steps warmup seed [est] [galerkin] [kind] [dump]\n", argv[0]);
@@ -324,3 +325,4 @@ int main(int argc, char** argv) {
   std::printf("%s\n", res[0].c_str());
   return 0;
 }
+#endif  // TMG_REF_NO_MAIN

@@ -294,7 +294,10 @@ struct MarchMinBlocks<FSpmvDotP> {
   static constexpr int v = TMGX_PSPMV_MINB;
 };
 
-template <bool VAR, class F, class U = ULoad>
+// KV (variable coefficients): rows evaluated from the vertex coefficient k in registers (six
+// harmonic faces and 1/D per vertex, the same expressions k_fill_faces stores)
+// instead of streaming the four precomputed row planes: 8 B/pt of coefficients instead of 32.
+template <bool VAR, class F, class U = ULoad, bool KV = false>
 __global__ void __launch_bounds__(kBX* kBY, MarchMinBlocks<F>::v)
     k_march(BoxGeo g, OpParams op, U u, F f, const double* __restrict__ scal, int beta_slot) {
   if constexpr (!std::is_same<U, ULoad>::value) u.beta = scal[beta_slot];
@@ -310,20 +313,35 @@ __global__ void __launch_bounds__(kBX* kBY, MarchMinBlocks<F>::v)
     const double *fD = op.fc, *fX = op.fc + op.fc_stride, *fY = op.fc + 2 * op.fc_stride,
                  *fZ = op.fc + 3 * op.fc_stride;
     double2 fzm{0.0, 0.0};
-    if (VAR) fzm = ld2(fZ + v - g.pxy);
+    if (VAR && !KV) fzm = ld2(fZ + v - g.pxy);
+    const double* K = op.k;
+    double2 kzm{0.0, 0.0}, kzc{0.0, 0.0}, kzn{0.0, 0.0};
+    if (KV) {
+      kzm = ld2(K + v - g.pxy);
+      kzc = ld2(K + v);
+      kzn = ld2(K + v + g.pxy);
+    }
     typename F::In in = f.load(v);
     for (int k = k0; k < k1; ++k, v += g.pxy) {
-      double2 unn{0.0, 0.0};
+      double2 unn{0.0, 0.0}, knn{0.0, 0.0};
       typename F::In inn{};
       if (k + 1 < k1) {  // prefetch the next plane
         unn = u.two(v + 2 * g.pxy);
         inn = f.load(v + g.pxy);
+        if (KV) knn = ld2(K + v + 2 * g.pxy);
       }
       const double2 uym = u.two(v - g.px), uyp = u.two(v + g.px);
       const double uxl = u.one(v - 1), uxr = u.one(v + 2);
       double2 dd{0.0, 0.0}, fx{0.0, 0.0}, fy{0.0, 0.0}, fym{0.0, 0.0}, fz{0.0, 0.0};
       double fxl = 0.0;
-      if (VAR) {
+      double2 kym{0.0, 0.0}, kyp{0.0, 0.0};
+      double kxl = 0.0, kxr = 0.0;
+      if (KV) {
+        kym = ld2(K + v - g.px);
+        kyp = ld2(K + v + g.px);
+        kxl = __ldg(K + v - 1);
+        kxr = __ldg(K + v + 2);
+      } else if (VAR) {
         dd = ld2(fD + v);
         fx = ld2(fX + v);
         fy = ld2(fY + v);
@@ -337,7 +355,10 @@ __global__ void __launch_bounds__(kBX* kBY, MarchMinBlocks<F>::v)
         if (q == 1 && !two) break;
         const Pt p = make_pt(g, i0 + q, j, k);
         Coef c;
-        if (VAR) {
+        if (KV) {
+          c = coef_at<true>(op, p, get(kzc, q), q ? kzc.x : kxl, q ? kxr : kzc.y, get(kym, q), get(kyp, q),
+                            get(kzm, q), get(kzn, q));
+        } else if (VAR) {
           c.dg = get(dd, q);
           c.invd = 1.0 / c.dg;
           c.azm = -get(fzm, q);
@@ -357,7 +378,12 @@ __global__ void __launch_bounds__(kBX* kBY, MarchMinBlocks<F>::v)
       um = uc;
       uc = un;
       un = unn;
-      if (VAR) fzm = fz;
+      if (VAR && !KV) fzm = fz;
+      if (KV) {
+        kzm = kzc;
+        kzc = kzn;
+        kzn = knn;
+      }
       in = inn;
     }
   }
@@ -382,8 +408,11 @@ __device__ __forceinline__ double row27(const BoxGeo& g, const double* __restric
   return acc;
 }
 
-template <class F>
-__global__ void __launch_bounds__(kBX* kBY) k_march27(BoxGeo g, OpParams op, const double* __restrict__ u, F f) {
+// Register-capped variants (TMGX_M27 = 1..3: 4 or 6 blocks/SM, rows of a pair loaded apart) for
+// the 161-register kernel (3 blocks/SM, long_scoreboard 81% under ncu): measured no faster live
+// (the Galerkin Chebyshev step streams ~272 B/pt at ~6.1 TB/s, profiles/README.md r03).
+template <class F, int MINB = 1, bool SERIAL = false>
+__global__ void __launch_bounds__(kBX* kBY, MINB) k_march27(BoxGeo g, OpParams op, const double* __restrict__ u, F f) {
   __shared__ double sh[32];
   double acc0 = 0.0, acc1 = 0.0;
   const int i0 = 2 * (blockIdx.x * kBX + threadIdx.x), j = blockIdx.y * kBY + threadIdx.y;
@@ -397,6 +426,7 @@ __global__ void __launch_bounds__(kBX* kBY) k_march27(BoxGeo g, OpParams op, con
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
         if (q == 1 && !two) break;
+        if (SERIAL) asm volatile("" ::: "memory");  // keep the two rows' loads apart (register cap)
         const double au = row27(g, op.S, op.S_stride, u, v + q);
         const double invd = 1.0 / __ldg(op.S + 13 * op.S_stride + v + q);
         f.point(q, au, invd, __ldg(u + v + q), in, out, acc0, acc1);
@@ -1111,7 +1141,32 @@ struct alignas(128) T3VSmem {
   unsigned long long bar[NS];
 };
 
-template <bool PRE, int NR, int TY, bool DOTS>
+// Row of the coupling-plane operator: -z,-y,-x,c,+x,+y,+z in the reference's column order
+// (parity), or (TREE, performance build only) as a depth-4 tree of FMAs for the blocked kernel's
+// dependency chains.
+template <bool TREE>
+__device__ __forceinline__ double row7v(double fzm, double fym, double fxm, double dg, double fxp, double fyp,
+                                        double fzp, double uzm, double uym, double uxm, double uc, double uxp,
+                                        double uyp, double uzp) {
+#ifndef TMGX_PARITY
+  if (TREE) {
+    const double a = fma(-fzm, uzm, -fym * uym), b = fma(-fxm, uxm, dg * uc);
+    const double c = fma(-fxp, uxp, -fyp * uyp);
+    return (a + b) + fma(-fzp, uzp, c);
+  }
+#endif
+  double acc = 0.0;
+  acc += (-fzm) * uzm;
+  acc += (-fym) * uym;
+  acc += (-fxm) * uxm;
+  acc += dg * uc;
+  acc += (-fxp) * uxp;
+  acc += (-fyp) * uyp;
+  acc += (-fzp) * uzp;
+  return acc;
+}
+
+template <bool PRE, int NR, int TY, bool DOTS, bool TREE = false>
 __global__ void __launch_bounds__(kTBX* TY, 1)
     k_cheb3_var(const __grid_constant__ T3Maps maps, BoxGeo g, OpParams, double* __restrict__ xout, double s_theta, double c1a,
                 double c2a, double c1b, double c2b, double* __restrict__ dpart, long long dstride) {
@@ -1229,14 +1284,8 @@ __global__ void __launch_bounds__(kTBX* TY, 1)
         const double xs_ = r == 0 ? Xp[-kT3SX] : XQ[P1][r > 0 ? r - 1 : 0];
         const double xn_ = r == NR - 1 ? Xp[NR * kT3SX] : XQ[P1][r < NR - 1 ? r + 1 : 0];
         XQ[P3][r] = xn1;
-        double acc = 0.0;
-        acc += (-fzm) * XQ[P2][r];
-        acc += (-fym) * xs_;
-        acc += (-fxm) * xw;
-        acc += dg * xc;
-        acc += (-fxp) * xe;
-        acc += (-fyp) * xn_;
-        acc += (-fzp) * xn1;
+        const double acc = row7v<TREE>(fzm, fym, fxm, dg, fxp, fyp, fzp,
+                                       XQ[P2][r], xs_, xw, xc, xe, xn_, xn1);
         rr = bb - acc;
         d0 = (rr * invd) * s_theta;
       }
@@ -1258,14 +1307,8 @@ __global__ void __launch_bounds__(kTBX* TY, 1)
       const double d0 = D0[P2][r];
       const double ds = r == 0 ? ds0 : D0[P2][r > 0 ? r - 1 : 0];
       const double dn = r == NR - 1 ? dnN : D0[P2][r < NR - 1 ? r + 1 : 0];
-      double acc = 0.0;
-      acc += (-fzm) * D0[P3][r];
-      acc += (-fym) * ds;
-      acc += (-fxm) * dwv[r];
-      acc += DG[P2][r] * d0;
-      acc += (-fxp) * dev[r];
-      acc += (-fyp) * dn;
-      acc += (-fzp) * D0[P1][r];
+      const double acc = row7v<TREE>(fzm, fym, fxm, DG[P2][r], fxp, fyp, fzp,
+                                     D0[P3][r], ds, dwv[r], d0, dev[r], dn, D0[P1][r]);
       const double r1 = R0[P2][r] - acc;
       const double z = r1 * IV[P2][r];
       const double d1 = c1a * d0 + c2a * z;
@@ -1288,14 +1331,9 @@ __global__ void __launch_bounds__(kTBX* TY, 1)
       const double d1 = D1[P3][r];
       const double es = r == 0 ? es0 : D1[P3][r > 0 ? r - 1 : 0];
       const double en = r == NR - 1 ? enN : D1[P3][r < NR - 1 ? r + 1 : 0];
-      double acc = 0.0;
-      acc += (-fzm) * D1[P1][r];  // d1(p3 - 1): written when pass 2 ran on p1 - 3 (slot P1)
-      acc += (-fym) * es;
-      acc += (-fxm) * ewv[r];
-      acc += DG[P3][r] * d1;
-      acc += (-fxp) * eev[r];
-      acc += (-fyp) * en;
-      acc += (-fzp) * D1[P2][r];
+      // d1(p3 - 1) is D1[P1]: written when pass 2 ran on p1 - 3
+      const double acc = row7v<TREE>(fzm, fym, fxm, DG[P3][r], fxp, fyp, fzp,
+                                     D1[P1][r], es, ewv[r], d1, eev[r], en, D1[P2][r]);
       const double r2 = R1[P3][r] - acc;
       const double z = r2 * IV[P3][r];
       const double dn = c1b * d1 + c2b * z;
@@ -2813,10 +2851,36 @@ int launch_cheb_start_zero(const BoxGeo& g, const OpParams& op, const double* b,
   return 1;
 }
 
+// Variable-coefficient stencil passes stream the precomputed row planes (default) or evaluate
+// their rows from k (TMGX_VAR_K=1). Measured at 513^3 (profiles/README.md r03): the six
+// divisions per vertex cost more than the 24 B/pt they save (last Chebyshev pass 1.78 -> 2.76 ms,
+// residual 1.41 -> 1.97 ms, p-update + SpMV 1.31 -> 2.48 ms), so the planes stay.
+static bool var_k_rows() {
+  static const bool on = [] {
+    const char* e = std::getenv("TMGX_VAR_K");
+    return e ? std::atoi(e) != 0 : false;
+  }();
+  return on;
+}
+
 template <class F>
 static void march(const BoxGeo& g, const OpParams& op, const double* u, const F& f, cudaStream_t s) {
-  if (op.S)
-    k_march27<F><<<tile_grid(g), kBlock, 0, s>>>(g, op, u, f);
+  if (op.S) {
+    static const int v27 = [] {
+      const char* e = std::getenv("TMGX_M27");
+      return e ? std::atoi(e) : 0;
+    }();
+    if (v27 == 1)
+      k_march27<F, 4, false><<<tile_grid(g), kBlock, 0, s>>>(g, op, u, f);
+    else if (v27 == 2)
+      k_march27<F, 4, true><<<tile_grid(g), kBlock, 0, s>>>(g, op, u, f);
+    else if (v27 == 3)
+      k_march27<F, 6, true><<<tile_grid(g), kBlock, 0, s>>>(g, op, u, f);
+    else
+      k_march27<F><<<tile_grid(g), kBlock, 0, s>>>(g, op, u, f);
+  }
+  else if (op.fc && op.k && var_k_rows())
+    k_march<true, F, ULoad, true><<<tile_grid(g), kBlock, 0, s>>>(g, op, ULoad{u}, f, nullptr, 0);
   else if (op.fc)
     k_march<true, F><<<tile_grid(g), kBlock, 0, s>>>(g, op, ULoad{u}, f, nullptr, 0);
   else
@@ -2831,7 +2895,9 @@ int launch_pspmv_dot(const BoxGeo& g, const OpParams& op, const double* z, const
                      double* w, double* part, const double* scal, int beta_slot, cudaStream_t s) {
   const UPDir u{z, p_old, 0.0};
   const FSpmvDotP f{w, p_new, part};
-  if (op.fc)
+  if (op.fc && op.k && var_k_rows())
+    k_march<true, FSpmvDotP, UPDir, true><<<tile_grid(g), kBlock, 0, s>>>(g, op, u, f, scal, beta_slot);
+  else if (op.fc)
     k_march<true, FSpmvDotP, UPDir><<<tile_grid(g), kBlock, 0, s>>>(g, op, u, f, scal, beta_slot);
   else
     k_march<false, FSpmvDotP, UPDir><<<tile_grid(g), kBlock, 0, s>>>(g, op, u, f, scal, beta_slot);
@@ -3164,7 +3230,19 @@ static int launch_t3_rows(const BoxGeo& g, const OpParams& op, const double* b, 
     return true;
   };
   bool ok;
-  if (op.fc && t3_env("TMGX_T3_LEAN", 1)) {
+#ifdef TMGX_PARITY
+  const bool tree = false;
+#else
+  const bool tree = t3_env("TMGX_T3_TREE", 0) != 0;
+#endif
+  if (op.fc && t3_env("TMGX_T3_LEAN", 1) && tree) {
+    if (pre)
+      ok = run(k_cheb3_var<true, NR, TY, false, true>, sizeof(T3VSmem<NR, TY, true>), slots[0]);
+    else if (dots)
+      ok = run(k_cheb3_var<false, NR, TY, true, true>, sizeof(T3VSmem<NR, TY, false>), slots[1]);
+    else
+      ok = run(k_cheb3_var<false, NR, TY, false, true>, sizeof(T3VSmem<NR, TY, false>), slots[2]);
+  } else if (op.fc && t3_env("TMGX_T3_LEAN", 1)) {
     if (pre)
       ok = run(k_cheb3_var<true, NR, TY, false>, sizeof(T3VSmem<NR, TY, true>), slots[0]);
     else if (dots)

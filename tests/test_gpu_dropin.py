@@ -1,0 +1,69 @@
+"""The drop-in proved from the reference side: oracle/_ref/tmg_ref_gpupc links
+the reference's own translation units with libtmgx.so and runs the reference's krylov_solve(cg)
+three ways -- with its own V-cycle (ref), with GpuMGPC (the tmgx V-cycle behind the reference's
+Preconditioner interface, preconditioner.hpp:17-32), and as one tmgx_solve (gpu).
+
+Bar (BASELINE.json north_star): iterations equal or within +-1; solutions within 1e-9 relative
+(max-norm) at equal iteration counts. Built by oracle/build_ref.sh in the CPU container (skipped
+where the reference sources were absent at build time)."""
+import json
+import os
+import subprocess
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+BIN = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref", "tmg_ref_gpupc")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def need():
+    try:
+        import torch
+
+        if not torch.cuda.is_available():
+            pytest.skip("no CUDA device")
+    except ImportError:
+        pytest.skip("torch missing")
+    if not os.path.exists(BIN):
+        pytest.skip("oracle/_ref/tmg_ref_gpupc not built (reference sources absent at build time)")
+
+
+CASES = [(33, 4, 2, 0, 0), (65, 5, 2, 0, 0), (65, 5, 3, 0, 0), (33, 4, 3, 1, 0), (65, 5, 3, 1, 1)]
+
+
+def run(binary, n, nl, m, kind, galerkin):
+    if not os.path.exists(binary):
+        pytest.skip(f"{binary} not built")
+    out = subprocess.run([binary, str(n), str(nl), str(m), str(kind), str(galerkin), "42"], capture_output=True,
+                         text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    r = json.loads(out.stdout.strip().splitlines()[-1])
+    assert r["pc_kind"] == "mg(gpu)"
+    assert r["ref_reason"] == "rtol" and r["pc_reason"] == "rtol"
+    return r
+
+
+@pytest.mark.parametrize("n,nl,m,kind,galerkin", CASES)
+def test_reference_cg_with_gpu_vcycle(n, nl, m, kind, galerkin):
+    """Performance build: +-1 iteration, ||x - x_ref||_2 / ||x_ref||_2 < 1e-9 at equal counts."""
+    r = run(BIN, n, nl, m, kind, galerkin)
+    assert r["parity_build"] == 0
+    for key in ("pc", "gpu"):
+        assert abs(r[f"{key}_its"] - r["ref_its"]) <= 1, r
+        if r[f"{key}_its"] == r["ref_its"]:
+            assert r[f"{key}_vs_ref"] < 1e-9, (key, r[f"{key}_vs_ref"])
+
+
+@pytest.mark.parametrize("n,nl,m,kind,galerkin", [c for c in CASES if not (c[3] == 1 and c[4] == 1)])
+def test_reference_cg_with_gpu_vcycle_bitwise(n, nl, m, kind, galerkin):
+    """Parity build behind the same binding: the reference's CG with the GPU V-cycle, and the
+    whole GPU solve, reproduce the reference's own solve bit for bit (iterations, residual
+    history, solution) on every operator the reference assembles directly. (Variable-coefficient
+    Galerkin levels are excluded: the reference's ptap sums the same products in spgemm order,
+    tests/test_oracle_vs_reference.py.)"""
+    r = run(BIN + "_parity", n, nl, m, kind, galerkin)
+    assert r["parity_build"] == 1
+    assert r["pc_its"] == r["ref_its"] and r["gpu_its"] == r["ref_its"]
+    assert r["pc_history_bitwise"] and r["pc_x_bitwise"], r
+    assert r["gpu_history_bitwise"] and r["gpu_x_bitwise"], r
