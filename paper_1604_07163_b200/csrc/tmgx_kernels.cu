@@ -397,13 +397,19 @@ __global__ void __launch_bounds__(kBX* kBY, MarchMinBlocks<F>::v)
 // 27-point (Galerkin) rows: columns ascending = slots (dz, dy, dx) lexicographic; every slot
 // is multiplied (out-of-grid slots hold exact zeros and read zero ghosts), which equals the
 // reference CSR row loop over the stored entries. Same functors and tiles as k_march.
+// SYM (performance build): slots above the diagonal read the mirrored lower slot of the
+// neighbour's row, A(v, v+o) = A(v+o, v), so only the 14 lower planes stream from HBM. Exact for
+// constant coefficients; variable-coefficient Galerkin rows are symmetric to ~1e-12 relative (the
+// triple products are summed in row order), so the parity build always reads all 27 planes.
+template <bool SYM = false>
 __device__ __forceinline__ double row27(const BoxGeo& g, const double* __restrict__ S, long long st,
                                         const double* __restrict__ u, long long v) {
   double acc = 0.0;
 #pragma unroll
   for (int s = 0; s < 27; ++s) {
     const long long o = (long long)(s / 9 - 1) * g.pxy + (long long)((s / 3) % 3 - 1) * g.px + (s % 3 - 1);
-    acc += __ldg(S + s * st + v) * __ldg(u + v + o);
+    const double a = (SYM && s > 13) ? __ldg(S + (26 - s) * st + v + o) : __ldg(S + s * st + v);
+    acc += a * __ldg(u + v + o);
   }
   return acc;
 }
@@ -411,7 +417,7 @@ __device__ __forceinline__ double row27(const BoxGeo& g, const double* __restric
 // Register-capped variants (TMGX_M27 = 1..3: 4 or 6 blocks/SM, rows of a pair loaded apart) for
 // the 161-register kernel (3 blocks/SM, long_scoreboard 81% under ncu): measured no faster live
 // (the Galerkin Chebyshev step streams ~272 B/pt at ~6.1 TB/s, profiles/README.md r03).
-template <class F, int MINB = 1, bool SERIAL = false>
+template <class F, int MINB = 1, bool SERIAL = false, bool SYM = false>
 __global__ void __launch_bounds__(kBX* kBY, MINB) k_march27(BoxGeo g, OpParams op, const double* __restrict__ u, F f) {
   __shared__ double sh[32];
   double acc0 = 0.0, acc1 = 0.0;
@@ -427,7 +433,7 @@ __global__ void __launch_bounds__(kBX* kBY, MINB) k_march27(BoxGeo g, OpParams o
       for (int q = 0; q < 2; ++q) {
         if (q == 1 && !two) break;
         if (SERIAL) asm volatile("" ::: "memory");  // keep the two rows' loads apart (register cap)
-        const double au = row27(g, op.S, op.S_stride, u, v + q);
+        const double au = row27<SYM>(g, op.S, op.S_stride, u, v + q);
         const double invd = 1.0 / __ldg(op.S + 13 * op.S_stride + v + q);
         f.point(q, au, invd, __ldg(u + v + q), in, out, acc0, acc1);
       }
@@ -2870,6 +2876,18 @@ static void march(const BoxGeo& g, const OpParams& op, const double* u, const F&
       const char* e = std::getenv("TMGX_M27");
       return e ? std::atoi(e) : 0;
     }();
+#ifndef TMGX_PARITY
+    static const bool sym = [] {
+      const char* e = std::getenv("TMGX_G27_SYM");
+      return e ? std::atoi(e) != 0 : true;
+    }();
+    // single-box levels only: the mirrored slot of a vertex on a box face lives in the
+    // neighbouring box (coefficient planes have no halo); out-of-grid ghosts hold zeros
+    if (sym && v27 == 0 && g.ex == g.Nx && g.ey == g.Ny && g.ez == g.Nz) {
+      k_march27<F, 1, false, true><<<tile_grid(g), kBlock, 0, s>>>(g, op, u, f);
+      return;
+    }
+#endif
     if (v27 == 1)
       k_march27<F, 4, false><<<tile_grid(g), kBlock, 0, s>>>(g, op, u, f);
     else if (v27 == 2)
