@@ -242,7 +242,25 @@ def run_elast(args, world, rank, np3, nlevels, m, rtol, dist):
         s.solve_ptr(b_host.data_ptr(), x_host.data_ptr(), cfg)
         e2e_t += time.perf_counter() - t1
     ms, by, fl = s.bench_apply(20)
-    peak, peak_kind = read_peaks()
+    # k_el_apply is fp64-FMA bound (576 FMAs per vertex): the roofline is the B200 fp64 vector
+    # peak. MEASURED_PEAKS.json has none, so the nominal figure: 148 SMs x 64 DFMA/clk x 2 flop x
+    # 1.965 GHz = 37.2 TFLOP/s.
+    fp64_peak = 148 * 64 * 2 * 1.965e9 / 1e12
+    cpu = None
+    if not args.no_cpu_baseline:
+        # the elasticity oracle (C, OpenMP over the host cores) on a bounded sample: the same
+        # algorithm at 65^3 x 3 dofs, 5 levels (the 129^3 problem takes ~1 min per solve there)
+        from oracle import oracle as O
+
+        mg = O.ElastMG((65, 65, 65), nlevels - 1, smooth_its=m)
+        bo = O.el_rhs((65, 65, 65))
+        t1 = time.perf_counter()
+        _, orep = mg.solve(bo, rtol=rtol)
+        t_cpu = time.perf_counter() - t1
+        cpu = {"value": bo.size / t_cpu, "unit": "DOF/s", "cores": int(os.environ.get("OMP_NUM_THREADS", os.cpu_count())),
+               "kind": "port", "sample": f"elasticity oracle (oracle/tmg_elast_oracle.c, OpenMP) on 65^3 x 3 dofs, "
+                                         f"{nlevels - 1} levels, V({m},{m}), rtol {rtol:g}: {orep['iterations']} its, "
+                                         f"{t_cpu:.2f} s"}
     line = {
         "metric": "MG-CG DOF/s (time-to-solution)", "value": n_dof * args.steps / dev_t, "unit": "DOF/s",
         "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_t / args.steps * 1e3,
@@ -255,11 +273,13 @@ def run_elast(args, world, rank, np3, nlevels, m, rtol, dist):
         "e2e": {"value": n_dof * args.steps / e2e_t, "unit": "DOF/s", "h2d_bytes_per_step": 8 * n_dof,
                 "d2h_bytes_per_step": 8 * n_dof},
         "gpu_launches": rep.kernel_launches * args.steps,
-        "roofline": {"bound": "hbm", "achieved": by / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
-                     "frac": by / (ms * 1e-3) / 1e9 / peak, "traffic": None, "peak_kind": peak_kind,
+        "roofline": {"bound": "fp64", "achieved": fl / (ms * 1e-3) / 1e12, "peak": fp64_peak, "unit": "TFLOP/s",
+                     "frac": fl / (ms * 1e-3) / 1e12 / fp64_peak, "traffic": None,
+                     "peak_kind": "nominal (148 SMs x 64 DFMA/clk x 1.965 GHz; no measured fp64 peak)",
                      "kernel": "k_el_apply (Q1 elasticity operator, fine level)", "ms_per_launch": ms,
-                     "bytes_per_launch": by, "fp64_tflops": fl / (ms * 1e-3) / 1e12},
-        "cpu_baseline": None,
+                     "flops_per_launch": fl, "bytes_per_launch": by,
+                     "hbm_GBs": by / (ms * 1e-3) / 1e9},
+        "cpu_baseline": cpu,
         "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)

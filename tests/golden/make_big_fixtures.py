@@ -29,7 +29,7 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
-OUT = os.path.dirname(os.path.abspath(__file__))
+OUT = os.environ.get("TMGX_FIXTURE_OUT", os.path.dirname(os.path.abspath(__file__)))  # e.g. gpurun_out/ on a big host
 SEED_F, SEED_K = 1234, 7
 
 CASES = {
