@@ -32,7 +32,26 @@ CONFIGS = {
     "cfg4w": ((257, 257, 257), 7, 2, 0, 4, 1e-8),
     # Q1 elasticity, 3 dof/vertex (kind 2): one GPU, no telescope on this path yet
     "cfg5": ((129, 129, 129), 6, 2, 2, None, 1e-6),
+    # weak scaling, 257^3 per GPU (true-weak series): the global grid and the
+    # nested telescope stages depend on N (resolve())
+    "cfg4": ((257, 257, 257), 7, 2, 0, "nested", 1e-8),
 }
+CFG4_GRID = {1: (257, 257, 257), 2: (513, 257, 257), 4: (513, 513, 257), 8: (513, 513, 513)}
+
+
+def resolve(config, world):
+    """(np3, nlevels, m, kind, telescope stages [(level, r)], rtol, scaling) of a config at N."""
+    np3, nlevels, m, kind, tele_level, rtol = CONFIGS[config]
+    if config != "cfg4":
+        stages = [(tele_level, world)] if (world > 1 and tele_level is not None) else []
+        return np3, nlevels, m, kind, stages, rtol, "strong"
+    if world not in CFG4_GRID:
+        raise SystemExit(f"cfg4 is defined for 1, 2, 4, 8 GPUs (got {world})")
+    np3 = CFG4_GRID[world]
+    nlevels = 7 if world == 1 else 8
+    # nested telescoping (BASELINE configs[3]): N -> 2 at level 4, 2 -> 1 at level 2
+    stages = ([(4, world // 2)] if world > 2 else []) + ([(2, 2)] if world > 1 else [])
+    return np3, nlevels, m, kind, stages, rtol, "weak"
 # Coarse operators: rediscretised (reference default, SURVEY App. A-C7) for constant k;
 # Galerkin 2^-3 P^T A P for the 1e4-contrast problem (with rediscretisation the reference
 # algorithm needs ~500 CG iterations at 513^3; see DESIGN.md §9).
@@ -115,19 +134,19 @@ class ClockSampler:
 
 def workload_config(config, world, tele_level, galerkin, est):
     """The `config` object of both arms' JSON lines (identical for the same --config / N)."""
-    np3, nlevels, m, kind, _, rtol = CONFIGS[config]
+    np3, nlevels, m, kind, stages, rtol, _ = resolve(config, world)
     n_dof = np3[0] * np3[1] * np3[2]
-    tele = world > 1 and tele_level is not None
+    tele = bool(stages)
     return {"workload": f"{config}: {np3[0]}x{np3[1]}x{np3[2]} {'var-coef' if kind else 'Poisson'} {nlevels}-level "
                         f"MG V({m},{m}) Cheb-Jacobi CG rtol {rtol:g}, est={est}, "
                         f"coarse={'galerkin' if galerkin else 'rediscretised'}",
             "global_batch": 1, "seq_len": np3[0],
-            "parallelism": f"box{world}" + (f"+telescope(L{tele_level},r{world})" if tele else ""),
+            "parallelism": f"box{world}" + "".join(f"+telescope(L{lv},r{r})" for lv, r in stages),
             "l2": ("inputs larger than L2 (one fine vector = %.0f MB)" % (n_dof * 8 / 1e6) if n_dof * 8 > 126e6 else
                    "L2-resident problem (one fine vector = %.1f MB): a latency benchmark" % (n_dof * 8 / 1e6))}
 
 
-def cpu_reference_sample(config="cfg2", steps=1, warmup=0, galerkin=False, budget_s=0.0):
+def cpu_reference_sample(config="cfg2", steps=1, warmup=0, galerkin=False, budget_s=0.0, world=1):
     """The reference algorithm on the host, on the SAME problem as the GPU arm (BASELINE config,
     full size): oracle/_ref (the reference's own translation units + the SPEC-following V-cycle
     glue) when it was built, else the C restatement in oracle/. One rank = one core (the
@@ -135,7 +154,7 @@ def cpu_reference_sample(config="cfg2", steps=1, warmup=0, galerkin=False, budge
     Setup (assembly, hierarchy, estimates) is excluded; `warmup` untimed solves first, then the
     mean over `steps` complete solves. Returns (dof_per_s, seconds_per_solve, kind, description,
     iterations)."""
-    np3, nlevels, m, kind_p, _, rtol = CONFIGS[config]
+    np3, nlevels, m, kind_p, _, rtol, _ = resolve(config, world)
     ref_bin = os.path.join(ROOT, "oracle", "_ref", "tmg_ref_bench")
     n = np3[0] * np3[1] * np3[2]
     if os.path.exists(ref_bin) and np3[0] == np3[1] == np3[2]:
@@ -180,18 +199,19 @@ def run_reference(args, rank, world):
     GPU arm's config (same problem, same size). One complete 257^3 solve takes ~50 s on one
     core, so K steps are capped by a time budget (TMGX_REF_BUDGET_S, default 150 s of timed
     solves after one untimed solve); `steps` reports the solves actually timed."""
-    np3, nlevels, m, kind, tele_level, rtol = CONFIGS[args.config]
+    np3, nlevels, m, kind, _, rtol, scaling = resolve(args.config, world)
     if rank != 0:
         return
     galerkin = GALERKIN.get(args.config, False) if args.galerkin is None else args.galerkin == "on"
     budget = float(os.environ.get("TMGX_REF_BUDGET_S", "150"))
     W = 1 if args.warmup > 0 else 0  # the reference protocol: time the second of identical solves
     rate, t, kind_s, desc, its, K = cpu_reference_sample(args.config, steps=max(args.steps, 1), warmup=W,
-                                                         galerkin=galerkin, budget_s=budget if W else 0.0)
+                                                         galerkin=galerkin, budget_s=budget if W else 0.0,
+                                                         world=world)
     line = {
         "impl": "reference", "metric": "MG-CG DOF/s (time-to-solution)", "value": rate, "unit": "DOF/s",
         "n_gpus": args.gpus, "steps": K, "warmup": W, "steps_requested": args.steps,
-        "warmup_requested": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
+        "warmup_requested": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": scaling,
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded RHS, natural-index hash; BASELINE configs are synthetic)",
         "config": workload_config(args.config, world, tele_level, galerkin, args.est),
@@ -321,7 +341,8 @@ def main():
     from paper_1604_07163_b200 import tmgx as T
 
     torch.cuda.set_device(local)
-    np3, nlevels, m, kind, tele_level, rtol = CONFIGS[args.config]
+    np3, nlevels, m, kind, stages, rtol, scaling = resolve(args.config, world)
+    tele_level = stages[0][0] if stages else None
     if kind == 2:
         run_elast(args, world, rank, np3, nlevels, m, rtol, dist)
         return
@@ -333,7 +354,7 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         job = obj[0]
     w = T.World(n_ranks=world, nproc=world, proc=rank, device=local, job=job)
-    tele = [T.TelescopeStage(tele_level, world)] if (world > 1 and tele_level is not None) else []
+    tele = [T.TelescopeStage(lv, r) for lv, r in stages]
     t0 = time.perf_counter()
     galerkin = GALERKIN.get(args.config, False) if args.galerkin is None else args.galerkin == "on"
     s = T.SolverNode(w, T.Problem(np3, kind, seed_k=SEED_K),
@@ -431,6 +452,19 @@ def main():
         except Exception:  # noqa: BLE001 (kernel not applicable to this level)
             pass
 
+    # per-level V-cycle profile (device time per node, max over ranks; peer bytes, summed over
+    # ranks): BASELINE configs[3] asks for per-level time and NVLink bytes
+    levels = s.level_profile(reps=10)
+    if dist:
+        t = torch.tensor([lv["us"] for lv in levels], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        bsum = torch.tensor([float(lv["peer_bytes"]) for lv in levels], dtype=torch.float64)
+        dist.all_reduce(bsum, op=dist.ReduceOp.SUM)
+        for lv, u, by in zip(levels, t.tolist(), bsum.tolist()):
+            lv["us"], lv["peer_bytes"] = u, int(by)
+    for lv in levels:
+        lv["us"] = round(lv["us"], 2)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, t_cpu, ckind, desc, _, _ = cpu_reference_sample(args.config, steps=1, warmup=0, galerkin=galerkin)
@@ -440,7 +474,7 @@ def main():
         line = {
             "metric": "MG-CG DOF/s (time-to-solution)", "value": value, "unit": "DOF/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_dev / args.steps * 1e3,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded RHS, natural-index hash; BASELINE configs are synthetic)",
             "config": workload_config(args.config, world, tele_level, galerkin, args.est),
             "solve": {"iterations": its[-1] if its else None, "t_setup_s": t_setup,
@@ -457,6 +491,7 @@ def main():
                                         else "algorithmic bytes (SURVEY §8(d))")},
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
+            "levels": levels,
         }
         print(json.dumps(line), flush=True)
     if dist:

@@ -253,6 +253,14 @@ typedef struct {
   int64_t allreduces;
 } tmgx_counters;
 int tmgx_get_counters(tmgx_solver s, tmgx_counters *c);
+/* Per-level V-cycle profile (the reference's per-level MsgCounters, comm.hpp:37-47, plus device
+ * time): runs `reps` V-cycles with CUDA events around every node of the hierarchy and returns,
+ * per node (0 = finest; kinds 0 smooth / 1 telescope / 2 coarse LU), the global grid, the number
+ * of ranks of its communicator, the node's own mean device microseconds per V-cycle (its
+ * coarser part excluded; a telescope node's time is its gather + scatter) and the bytes this
+ * process sent to peers for it (halos, telescope transfers). Collective. */
+int tmgx_level_profile(tmgx_solver s, int reps, int max_nodes, int *n_nodes, int *kind, int64_t *npoints,
+                       int *n_ranks, double *us, int64_t *bytes);
 
 /* Telescope timing in the paper's Table 1/2 schema: T_setup = host time of
  * the stage's plan construction (P-hat / ScatterPlan analogue) + upload during solver setup;

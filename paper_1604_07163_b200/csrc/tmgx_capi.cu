@@ -804,6 +804,29 @@ int tmgx_exchange_timing(tmgx_solver s, int level, int reps, double* us, int64_t
   });
 }
 
+int tmgx_level_profile(tmgx_solver s, int reps, int max_nodes, int* n_nodes, int* kind, int64_t* npoints,
+                       int* n_ranks, double* us, int64_t* bytes) {
+  return guard([&] {
+    auto& S = *s->s;
+    if (reps < 1) throw tmg::ConfigError("reps must be >= 1");
+    const int n = (int)S.nodes.size();
+    *n_nodes = n;
+    if (n > max_nodes) throw tmg::ConfigError("level_profile: need room for " + std::to_string(n) + " nodes");
+    std::vector<double> u;
+    std::vector<long long> by;
+    S.level_profile(reps, u, by);
+    for (int i = 0; i < n; ++i) {
+      const auto& nd = S.nodes[(size_t)i];
+      kind[i] = (int)nd.kind;
+      for (int a = 0; a < 3; ++a) npoints[3 * i + a] = nd.dist->h.npoints[(size_t)a];
+      n_ranks[i] = nd.dist->h.n_ranks();
+      us[i] = u[(size_t)i];
+      bytes[i] = by[(size_t)i];
+    }
+    return 0;
+  });
+}
+
 int tmgx_get_counters(tmgx_solver s, tmgx_counters* c) {
   const auto& k = s->s->W.cnt;
   c->kernel_launches = k.launches;

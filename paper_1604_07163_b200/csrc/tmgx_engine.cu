@@ -957,6 +957,75 @@ void Solver::coarse_cycle(int i0) {
 // mg_apply (Alg. 1) over the node list; TELESCOPE nodes realise
 // TelescopePC::apply: gather, inner V-cycle on the members, scatter back.
 void Solver::vcycle(int i) {
+  if (!prof) {
+    vcycle_body(i);
+    return;
+  }
+  LevelProf& P = (*prof)[(size_t)i];
+  P.descended = false;
+  P.bytes_in = W.cnt.halo_bytes + W.cnt.tele_bytes;
+  cuda_check(cudaEventRecord(P.e[0], W.stream), "record");
+  vcycle_body(i);
+  cuda_check(cudaEventRecord(P.e[3], W.stream), "record");
+  P.bytes_out = W.cnt.halo_bytes + W.cnt.tele_bytes;
+}
+
+// the coarser part of the cycle below node i (events around it when profiling)
+void Solver::descend(int i) {
+  if (!prof) {
+    vcycle(i + 1);
+    return;
+  }
+  LevelProf& P = (*prof)[(size_t)i];
+  P.descended = true;
+  P.bytes_down = W.cnt.halo_bytes + W.cnt.tele_bytes;
+  cuda_check(cudaEventRecord(P.e[1], W.stream), "record");
+  vcycle(i + 1);
+  cuda_check(cudaEventRecord(P.e[2], W.stream), "record");
+  P.bytes_up = W.cnt.halo_bytes + W.cnt.tele_bytes;
+}
+
+// Per-node exclusive device time and peer bytes of `reps` V-cycles (events on the library
+// stream; the node's own kernels and exchanges, its coarser part excluded).
+void Solver::level_profile(int reps, std::vector<double>& us, std::vector<long long>& bytes) {
+  std::vector<LevelProf> lp(nodes.size());
+  for (auto& P : lp)
+    for (auto& e : P.e) cuda_check(cudaEventCreate(&e), "event");
+  us.assign(nodes.size(), 0.0);
+  bytes.assign(nodes.size(), 0);
+  prof = &lp;
+  try {
+    for (int r = 0; r < reps; ++r) {
+      vcycle(0);
+      cuda_check(cudaStreamSynchronize(W.stream), "sync");
+      for (size_t i = 0; i < nodes.size(); ++i) {
+        LevelProf& P = lp[i];
+        float a = 0.f, b = 0.f;
+        if (P.descended) {
+          cuda_check(cudaEventElapsedTime(&a, P.e[0], P.e[1]), "elapsed");
+          cuda_check(cudaEventElapsedTime(&b, P.e[2], P.e[3]), "elapsed");
+          bytes[i] += (P.bytes_down - P.bytes_in) + (P.bytes_out - P.bytes_up);
+        } else {
+          cuda_check(cudaEventElapsedTime(&a, P.e[0], P.e[3]), "elapsed");
+          bytes[i] += P.bytes_out - P.bytes_in;
+        }
+        us[i] += 1e3 * (double)(a + b);
+      }
+    }
+  } catch (...) {
+    prof = nullptr;
+    throw;
+  }
+  prof = nullptr;
+  for (auto& P : lp)
+    for (auto& e : P.e) cudaEventDestroy(e);
+  for (size_t i = 0; i < nodes.size(); ++i) {
+    us[i] /= reps;
+    bytes[i] /= reps;
+  }
+}
+
+void Solver::vcycle_body(int i) {
   Node& nd = nodes[i];
   if (i == 0) dots_nblk = 0;
   if (nd.kind == COARSE) {
@@ -969,7 +1038,7 @@ void Solver::vcycle(int i) {
   }
   if (nd.kind == TELESCOPE) {
     run_plan(W, nd.gather, nd.b, nodes[i + 1].b, true);
-    vcycle(i + 1);
+    descend(i);
     run_plan(W, nd.scatter, nodes[i + 1].x, nd.x, true);
     return;
   }
@@ -980,7 +1049,7 @@ void Solver::vcycle(int i) {
     // correction x~ = d + P x_c into r (free after the restriction), blocked post-smooth r -> x
     for (size_t q = 0; q < D.local.size(); ++q) tb_side(nd, q, nullptr, nd.d.p[q], true);
     residual_restrict(i, nd.d);
-    vcycle(i + 1);
+    descend(i);
     halo(i + 1, cn.x);
     for (size_t q = 0; q < D.local.size(); ++q)
       W.cnt.launches += launch_prolong_to(D.geo[q], cn.dist->geo[q], cn.x.p[q], nd.d.p[q], nd.r.p[q], W.stream);
@@ -992,7 +1061,7 @@ void Solver::vcycle(int i) {
   }
   smooth(i, true);
   residual_restrict(i, nd.x);
-  vcycle(i + 1);
+  descend(i);
   halo(i + 1, cn.x);
   for (size_t q = 0; q < D.local.size(); ++q)
     W.cnt.launches += launch_prolong_add(D.geo[q], cn.dist->geo[q], cn.x.p[q], nd.x.p[q], W.stream);

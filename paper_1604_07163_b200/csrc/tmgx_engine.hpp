@@ -243,6 +243,16 @@ class Solver {
 
   // primitives
   void vcycle(int i);  // nodes[i].b -> nodes[i].x
+  void vcycle_body(int i);
+  void descend(int i);
+  // per-node exclusive device time (us) and peer bytes sent of one V-cycle, mean of `reps`
+  void level_profile(int reps, std::vector<double>& us, std::vector<long long>& bytes);
+  struct LevelProf {
+    cudaEvent_t e[4]{};
+    bool descended = false;
+    long long bytes_in = 0, bytes_down = 0, bytes_up = 0, bytes_out = 0;
+  };
+  std::vector<LevelProf>* prof = nullptr;
   void smooth(int i, bool zero_x);
   void residual_restrict(int i, const Field& x);  // nodes[i+1].b = R (nodes[i].b - A x)
   void halo(int i, const Field& f);

@@ -86,7 +86,7 @@ EXPORTS = [
     "tmgx_pc_apply", "tmgx_level_apply", "tmgx_level_smooth", "tmgx_level_residual_restrict",
     "tmgx_level_prolong_add", "tmgx_coarse_solve", "tmgx_telescope_gather", "tmgx_telescope_scatter",
     "tmgx_get_counters", "tmgx_parity_build", "tmgx_last_error", "tmgx_bench_kernel", "tmgx_plan_summary",
-    "tmgx_node_selftest", "tmgx_exchange_timing",
+    "tmgx_node_selftest", "tmgx_exchange_timing", "tmgx_level_profile",
     "tmgx_options_create", "tmgx_options_destroy", "tmgx_options_parse", "tmgx_options_parse_file_text",
     "tmgx_options_set", "tmgx_options_get", "tmgx_options_serialize", "tmgx_options_unused",
     "tmgx_options_resolve", "tmgx_solver_from_options", "tmgx_telescope_timing",
@@ -145,6 +145,8 @@ def load(parity: bool = False):
         "tmgx_telescope_gather": [C.c_void_p, C.c_int, D, D],
         "tmgx_telescope_scatter": [C.c_void_p, C.c_int, D, D],
         "tmgx_get_counters": [C.c_void_p, P(_Counters)],
+        "tmgx_level_profile": [C.c_void_p, C.c_int, C.c_int, P(C.c_int), P(C.c_int), P(C.c_int64), P(C.c_int),
+                               P(C.c_double), P(C.c_int64)],
         "tmgx_bench_kernel": [C.c_void_p, C.c_int, C.c_int, C.c_int, D, D],
         "tmgx_plan_summary": [C.c_int, C.c_int, C.c_int, P(_Problem), P(_MG), I64, C.c_int, P(C.c_int)],
         "tmgx_node_selftest": [C.c_char_p, C.c_int, C.c_int, C.c_int, I64],
@@ -723,6 +725,19 @@ class SolverNode:
         x = np.zeros_like(b)
         _check(self.L, self.L.tmgx_coarse_solve(self.h, _dp(b), _dp(x)))
         return x
+
+    def level_profile(self, reps=10):
+        """Per-node V-cycle profile (tmgx_level_profile): list of dicts {node, kind, npoints,
+        ranks, us, peer_bytes}, node 0 = finest."""
+        mx = 64
+        n = C.c_int()
+        kind, ranks = (C.c_int * mx)(), (C.c_int * mx)()
+        npts = (C.c_int64 * (3 * mx))()
+        us, by = (C.c_double * mx)(), (C.c_int64 * mx)()
+        _check(self.L, self.L.tmgx_level_profile(self.h, reps, mx, C.byref(n), kind, npts, ranks, us, by))
+        names = {0: "smooth", 1: "telescope", 2: "coarse"}
+        return [{"node": i, "kind": names.get(kind[i], str(kind[i])), "npoints": list(npts[3 * i:3 * i + 3]),
+                 "ranks": ranks[i], "us": us[i], "peer_bytes": by[i]} for i in range(n.value)]
 
     def bench_kernel(self, which, level, iters=20):
         """(ms per launch, algorithmic bytes per launch) for kernel `which` on `level`."""
