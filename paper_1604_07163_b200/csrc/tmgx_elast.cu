@@ -43,16 +43,27 @@ __device__ __forceinline__ long long vx(const BoxGeo& g, int i, int j, int k) {
   return g.base + i + g.px * (long long)j + g.pxy * (long long)k;
 }
 
-// y = A x (MODE 0) or y = b - A x (MODE 1); x, y, b: three component planes of g.total
+// y = A x (MODE 0) or y = b - A x (MODE 1); x, y, b: three component planes of g.total.
+// One thread per vertex over a flattened (i, j) index, so every warp is full (a 128-wide x tile
+// left a 1-thread warp per row of the 129^3 level: a fifth of the issued instructions); neighbour
+// offsets are 32-bit and constant per (element, vertex) after the unroll; the couplings to a
+// clamped -x neighbour are dropped by multiplying its values by exact zeros (a row's partial sum
+// is never -0, so acc + (+-0) == acc: bitwise the skipped terms) instead of a divergent branch.
 template <int MODE>
 __global__ void __launch_bounds__(128) k_el_apply(BoxGeo g, const double* __restrict__ E, double h,
                                                   const double* __restrict__ x, const double* __restrict__ b,
                                                   double* __restrict__ y) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y, k = blockIdx.z;
-  if (i >= g.ex || j >= g.ey) return;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x, k = blockIdx.y;
+  if (idx >= g.ex * g.ey) return;
+  const int j = idx / g.ex, i = idx - j * g.ex;
   const long long T = g.total;
   const int nx = g.Nx, ny = g.Ny, nz = g.Nz;
+  const int px = (int)g.px, pxy = (int)g.pxy;
+  const long long v = vx(g, i, j, k);
+  const double* __restrict__ xv = x + v;
+  const double* __restrict__ Ev = E + v;
   const bool cl = g.gx + i == 0;
+  const double keep_m1 = g.gx + i - 1 == 0 ? 0.0 : 1.0;  // -x neighbour clamped: coupling dropped
   double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
 #pragma unroll
   for (int ez = -1; ez <= 0; ++ez)
@@ -62,22 +73,25 @@ __global__ void __launch_bounds__(128) k_el_apply(BoxGeo g, const double* __rest
       for (int ex = -1; ex <= 0; ++ex) {
         const int ei = i + ex, ej = j + ey, ek = k + ez;
         if (ei < 0 || ej < 0 || ek < 0 || ei >= nx - 1 || ej >= ny - 1 || ek >= nz - 1) continue;
-        const double eh = __ldg(E + vx(g, ei, ej, ek)) * h;
+        const double eh = __ldg(Ev + ex + ey * px + ez * pxy) * h;
         const int l = -ex + 2 * (-ey) + 4 * (-ez);
         // element contribution: K_ref row block times the element's x, then scaled by E h
         double ea0 = 0.0, ea1 = 0.0, ea2 = 0.0;
         if (cl) {
-          const long long w = vx(g, i, j, k);
-          ea0 += c_K[(3 * l + 0) * 24 + 3 * l + 0] * __ldg(x + w);
-          ea1 += c_K[(3 * l + 1) * 24 + 3 * l + 1] * __ldg(x + T + w);
-          ea2 += c_K[(3 * l + 2) * 24 + 3 * l + 2] * __ldg(x + 2 * T + w);
+          ea0 += c_K[(3 * l + 0) * 24 + 3 * l + 0] * __ldg(xv);
+          ea1 += c_K[(3 * l + 1) * 24 + 3 * l + 1] * __ldg(xv + T);
+          ea2 += c_K[(3 * l + 2) * 24 + 3 * l + 2] * __ldg(xv + 2 * T);
         } else {
 #pragma unroll
           for (int lp = 0; lp < 8; ++lp) {
-            const int vi = ei + (lp & 1), vj = ej + ((lp >> 1) & 1), vk = ek + (lp >> 2);
-            if (g.gx + vi == 0) continue;  // coupling to a clamped dof dropped
-            const long long w = vx(g, vi, vj, vk);
-            const double x0 = __ldg(x + w), x1 = __ldg(x + T + w), x2 = __ldg(x + 2 * T + w);
+            const int dx = ex + (lp & 1), dy = ey + ((lp >> 1) & 1), dz = ez + (lp >> 2);
+            const int o = dx + dy * px + dz * pxy;
+            double x0 = __ldg(xv + o), x1 = __ldg(xv + T + o), x2 = __ldg(xv + 2 * T + o);
+            if (dx == -1) {
+              x0 *= keep_m1;
+              x1 *= keep_m1;
+              x2 *= keep_m1;
+            }
             const double xb[3] = {x0, x1, x2};
 #pragma unroll
             for (int bb = 0; bb < 3; ++bb) {
@@ -91,7 +105,6 @@ __global__ void __launch_bounds__(128) k_el_apply(BoxGeo g, const double* __rest
         acc1 += eh * ea1;
         acc2 += eh * ea2;
       }
-  const long long v = vx(g, i, j, k);
   if (MODE == 0) {
     y[v] = acc0;
     y[T + v] = acc1;
@@ -216,11 +229,19 @@ __global__ void k_el_dot_part(BoxGeo g, const double* __restrict__ a, const doub
   }
   if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
 }
-__global__ void k_el_dot_sum(const double* part, int n, double* out) {
-  if (threadIdx.x || blockIdx.x) return;
+// sum of the block partials: fixed strided order per thread, then a fixed shared-memory tree
+// (deterministic; a single-thread serial loop over 1184 partials took 43 us per dot)
+__global__ void __launch_bounds__(256) k_el_dot_sum(const double* __restrict__ part, int n, double* out) {
+  __shared__ double sh[256];
   double acc = 0.0;
-  for (int q = 0; q < n; ++q) acc += part[q];
-  *out = acc;
+  for (int q = threadIdx.x; q < n; q += 256) acc += part[q];
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = sh[0];
 }
 
 // natural interleaved (3 v + c) <-> component planes
@@ -237,6 +258,7 @@ __global__ void k_el_pack(BoxGeo g, const double* __restrict__ src, double* __re
 }
 
 dim3 vgrid(const BoxGeo& g) { return dim3((g.ex + 127) / 128, g.ey, g.ez); }
+dim3 fgrid(const BoxGeo& g) { return dim3((g.ex * g.ey + 127) / 128, g.ez); }  // flattened (i, j)
 
 }  // namespace
 
@@ -295,11 +317,11 @@ void q1_kref(double nu, double* K) {
 // hierarchy
 // ------------------------------------------------------------------------------------------
 void ElastSolver::apply(int l, const double* x, double* y) {
-  k_el_apply<0><<<vgrid(L[l].g), 128, 0, W.stream>>>(L[l].g, L[l].E, L[l].h, x, nullptr, y);
+  k_el_apply<0><<<fgrid(L[l].g), 128, 0, W.stream>>>(L[l].g, L[l].E, L[l].h, x, nullptr, y);
   ++launches;
 }
 void ElastSolver::residual(int l, const double* b, const double* x, double* r) {
-  k_el_apply<1><<<vgrid(L[l].g), 128, 0, W.stream>>>(L[l].g, L[l].E, L[l].h, x, b, r);
+  k_el_apply<1><<<fgrid(L[l].g), 128, 0, W.stream>>>(L[l].g, L[l].E, L[l].h, x, b, r);
   ++launches;
 }
 void ElastSolver::jacobi(int l, const double* x, double* y) {
@@ -318,7 +340,7 @@ double ElastSolver::dot(int l, const double* a, const double* b) {
     ++launches;
   } else {
     k_el_dot_part<<<1184, 256, 0, W.stream>>>(L[l].g, a, b, dot_part);
-    k_el_dot_sum<<<1, 1, 0, W.stream>>>(dot_part, 1184, dot_out);
+    k_el_dot_sum<<<1, 256, 0, W.stream>>>(dot_part, 1184, dot_out);
     launches += 2;
   }
   double h = 0.0;

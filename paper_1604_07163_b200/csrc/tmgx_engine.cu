@@ -963,6 +963,7 @@ void Solver::vcycle(int i) {
   }
   LevelProf& P = (*prof)[(size_t)i];
   P.descended = false;
+  P.recorded = true;
   P.bytes_in = W.cnt.halo_bytes + W.cnt.tele_bytes;
   cuda_check(cudaEventRecord(P.e[0], W.stream), "record");
   vcycle_body(i);
@@ -996,10 +997,12 @@ void Solver::level_profile(int reps, std::vector<double>& us, std::vector<long l
   prof = &lp;
   try {
     for (int r = 0; r < reps; ++r) {
+      for (auto& P : lp) P.recorded = false;
       vcycle(0);
       cuda_check(cudaStreamSynchronize(W.stream), "sync");
       for (size_t i = 0; i < nodes.size(); ++i) {
         LevelProf& P = lp[i];
+        if (!P.recorded) continue;  // inside the fused coarse cycle: counted by its first node
         float a = 0.f, b = 0.f;
         if (P.descended) {
           cuda_check(cudaEventElapsedTime(&a, P.e[0], P.e[1]), "elapsed");

@@ -249,7 +249,7 @@ class Solver {
   void level_profile(int reps, std::vector<double>& us, std::vector<long long>& bytes);
   struct LevelProf {
     cudaEvent_t e[4]{};
-    bool descended = false;
+    bool descended = false, recorded = false;
     long long bytes_in = 0, bytes_down = 0, bytes_up = 0, bytes_out = 0;
   };
   std::vector<LevelProf>* prof = nullptr;
