@@ -28,6 +28,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <tuple>
@@ -2993,10 +2994,16 @@ static CUtensorMap tensor_map(const BoxGeo& g, const double* base_ptr, int bx, i
       return std::tie(p, px, ey, ez, bx, by) < std::tie(o.p, o.px, o.ey, o.ez, o.bx, o.by);
     }
   };
+  // guarded: solvers on different host threads share it; bounded: a freed buffer's address can
+  // come back with another shape, so stale entries only cost memory, and the cache is dropped
+  // wholesale when it grows past a few thousand descriptors (128 B each)
+  static std::mutex mu;
   static std::map<Key, CUtensorMap> cache;
+  std::lock_guard<std::mutex> lock(mu);
   const Key key{base_ptr, g.px, g.ey, g.ez, bx, by};
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
+  if (cache.size() > 4096) cache.clear();
   CUtensorMap m;
   const cuuint64_t dims[3] = {(cuuint64_t)g.px, (cuuint64_t)(g.ey + 2), (cuuint64_t)(g.ez + 2)};
   const cuuint64_t strides[2] = {(cuuint64_t)g.px * 8, (cuuint64_t)g.pxy * 8};
