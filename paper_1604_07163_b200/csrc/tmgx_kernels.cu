@@ -298,8 +298,10 @@ struct MarchMinBlocks<FSpmvDotP> {
 // KV (variable coefficients): rows evaluated from the vertex coefficient k in registers (six
 // harmonic faces and 1/D per vertex, the same expressions k_fill_faces stores)
 // instead of streaming the four precomputed row planes: 8 B/pt of coefficients instead of 32.
-template <bool VAR, class F, class U = ULoad, bool KV = false>
-__global__ void __launch_bounds__(kBX* kBY, MarchMinBlocks<F>::v)
+// PF2: the input planes are prefetched two planes ahead instead of one (twice the bytes in
+// flight per thread for the latency-bound passes).
+template <bool VAR, class F, class U = ULoad, bool KV = false, bool PF2 = false, int MB = 0>
+__global__ void __launch_bounds__(kBX* kBY, MB ? MB : MarchMinBlocks<F>::v)
     k_march(BoxGeo g, OpParams op, U u, F f, const double* __restrict__ scal, int beta_slot) {
   if constexpr (!std::is_same<U, ULoad>::value) u.beta = scal[beta_slot];
   __shared__ double sh[32];
@@ -323,10 +325,24 @@ __global__ void __launch_bounds__(kBX* kBY, MarchMinBlocks<F>::v)
       kzn = ld2(K + v + g.pxy);
     }
     typename F::In in = f.load(v);
+    double2 un2{0.0, 0.0};
+    typename F::In in2{};
+    if (PF2 && k0 + 1 < k1) {
+      un2 = u.two(v + 2 * g.pxy);
+      in2 = f.load(v + g.pxy);
+    }
     for (int k = k0; k < k1; ++k, v += g.pxy) {
       double2 unn{0.0, 0.0}, knn{0.0, 0.0};
       typename F::In inn{};
-      if (k + 1 < k1) {  // prefetch the next plane
+      if (PF2) {  // planes k + 2 (u) / k + 1 (inputs) arrived during the previous plane
+        unn = un2;
+        inn = in2;
+        if (k + 2 < k1) {
+          un2 = u.two(v + 3 * g.pxy);
+          in2 = f.load(v + 2 * g.pxy);
+        }
+        if (KV && k + 1 < k1) knn = ld2(K + v + 2 * g.pxy);
+      } else if (k + 1 < k1) {  // prefetch the next plane
         unn = u.two(v + 2 * g.pxy);
         inn = f.load(v + g.pxy);
         if (KV) knn = ld2(K + v + 2 * g.pxy);
@@ -2870,6 +2886,25 @@ static bool var_k_rows() {
   return on;
 }
 
+// resident-block request for the constant-coefficient fused p-update / SpMV (TMGX_PSPMV_MB:
+// 0 = unconstrained, 106 registers, 4 blocks/SM; 5 or 6 = register caps)
+static int pspmv_minb() {
+  static const int v = [] {
+    const char* e = std::getenv("TMGX_PSPMV_MB");
+    return e ? std::atoi(e) : (kBY == 4 ? 5 : 0);  // measured: 5 blocks/SM (92 registers) 153 -> 146 us
+  }();
+  return v;
+}
+
+// two-plane-deep input prefetch in the z-marching passes (TMGX_MARCH_PF2)
+static bool march_pf2() {
+  static const bool on = [] {
+    const char* e = std::getenv("TMGX_MARCH_PF2");
+    return e ? std::atoi(e) != 0 : false;
+  }();
+  return on;
+}
+
 template <class F>
 static void march(const BoxGeo& g, const OpParams& op, const double* u, const F& f, cudaStream_t s) {
   if (op.S) {
@@ -2900,8 +2935,12 @@ static void march(const BoxGeo& g, const OpParams& op, const double* u, const F&
   }
   else if (op.fc && op.k && var_k_rows())
     k_march<true, F, ULoad, true><<<tile_grid(g), kBlock, 0, s>>>(g, op, ULoad{u}, f, nullptr, 0);
+  else if (op.fc && march_pf2())
+    k_march<true, F, ULoad, false, true><<<tile_grid(g), kBlock, 0, s>>>(g, op, ULoad{u}, f, nullptr, 0);
   else if (op.fc)
     k_march<true, F><<<tile_grid(g), kBlock, 0, s>>>(g, op, ULoad{u}, f, nullptr, 0);
+  else if (march_pf2())
+    k_march<false, F, ULoad, false, true><<<tile_grid(g), kBlock, 0, s>>>(g, op, ULoad{u}, f, nullptr, 0);
   else
     k_march<false, F><<<tile_grid(g), kBlock, 0, s>>>(g, op, ULoad{u}, f, nullptr, 0);
 }
@@ -2916,8 +2955,16 @@ int launch_pspmv_dot(const BoxGeo& g, const OpParams& op, const double* z, const
   const FSpmvDotP f{w, p_new, part};
   if (op.fc && op.k && var_k_rows())
     k_march<true, FSpmvDotP, UPDir, true><<<tile_grid(g), kBlock, 0, s>>>(g, op, u, f, scal, beta_slot);
+  else if (op.fc && march_pf2())
+    k_march<true, FSpmvDotP, UPDir, false, true><<<tile_grid(g), kBlock, 0, s>>>(g, op, u, f, scal, beta_slot);
   else if (op.fc)
     k_march<true, FSpmvDotP, UPDir><<<tile_grid(g), kBlock, 0, s>>>(g, op, u, f, scal, beta_slot);
+  else if (march_pf2())
+    k_march<false, FSpmvDotP, UPDir, false, true><<<tile_grid(g), kBlock, 0, s>>>(g, op, u, f, scal, beta_slot);
+  else if (pspmv_minb() == 5)
+    k_march<false, FSpmvDotP, UPDir, false, false, 5><<<tile_grid(g), kBlock, 0, s>>>(g, op, u, f, scal, beta_slot);
+  else if (pspmv_minb() == 6)
+    k_march<false, FSpmvDotP, UPDir, false, false, 6><<<tile_grid(g), kBlock, 0, s>>>(g, op, u, f, scal, beta_slot);
   else
     k_march<false, FSpmvDotP, UPDir><<<tile_grid(g), kBlock, 0, s>>>(g, op, u, f, scal, beta_slot);
   return 1;

@@ -15,7 +15,10 @@ namespace tmgx {
 
 constexpr int kXO = 4;         // padding so that i = 0 is sector aligned
 constexpr int kBX = 32;        // threads along x per block
-constexpr int kBY = 4;         // threads along y per block
+#ifndef TMGX_KBY
+#define TMGX_KBY 4
+#endif
+constexpr int kBY = TMGX_KBY;  // threads along y per block
 constexpr int kZC = 16;        // z planes marched per block
 constexpr int kMaxLocal = 64;  // local boxes per process
 
