@@ -2919,8 +2919,17 @@ static void march(const BoxGeo& g, const OpParams& op, const double* u, const F&
     }();
     // single-box levels only: the mirrored slot of a vertex on a box face lives in the
     // neighbouring box (coefficient planes have no halo); out-of-grid ghosts hold zeros
+    static const int sym_mb = [] {  // resident blocks requested for the symmetric variant
+      const char* e = std::getenv("TMGX_M27_SYM_MB");
+      return e ? std::atoi(e) : 3;  // measured at 257^3: step 645 -> 632 us, residual 534 -> 521 us
+    }();
     if (sym && v27 == 0 && g.ex == g.Nx && g.ey == g.Ny && g.ez == g.Nz) {
-      k_march27<F, 1, false, true><<<tile_grid(g), kBlock, 0, s>>>(g, op, u, f);
+      if (sym_mb == 3)
+        k_march27<F, 3, false, true><<<tile_grid(g), kBlock, 0, s>>>(g, op, u, f);
+      else if (sym_mb == 4)
+        k_march27<F, 4, false, true><<<tile_grid(g), kBlock, 0, s>>>(g, op, u, f);
+      else
+        k_march27<F, 1, false, true><<<tile_grid(g), kBlock, 0, s>>>(g, op, u, f);
       return;
     }
 #endif
@@ -2953,8 +2962,16 @@ int launch_pspmv_dot(const BoxGeo& g, const OpParams& op, const double* z, const
                      double* w, double* part, const double* scal, int beta_slot, cudaStream_t s) {
   const UPDir u{z, p_old, 0.0};
   const FSpmvDotP f{w, p_new, part};
+  static const int var_mb = [] {
+    const char* e = std::getenv("TMGX_PSPMV_VAR_MB");
+    return e ? std::atoi(e) : 5;  // measured at 513^3: 1838 -> 1659 us (4 blocks: 1916 us)
+  }();
   if (op.fc && op.k && var_k_rows())
     k_march<true, FSpmvDotP, UPDir, true><<<tile_grid(g), kBlock, 0, s>>>(g, op, u, f, scal, beta_slot);
+  else if (op.fc && var_mb == 4)
+    k_march<true, FSpmvDotP, UPDir, false, false, 4><<<tile_grid(g), kBlock, 0, s>>>(g, op, u, f, scal, beta_slot);
+  else if (op.fc && var_mb == 5)
+    k_march<true, FSpmvDotP, UPDir, false, false, 5><<<tile_grid(g), kBlock, 0, s>>>(g, op, u, f, scal, beta_slot);
   else if (op.fc && march_pf2())
     k_march<true, FSpmvDotP, UPDir, false, true><<<tile_grid(g), kBlock, 0, s>>>(g, op, u, f, scal, beta_slot);
   else if (op.fc)
