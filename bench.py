@@ -199,7 +199,8 @@ def run_reference(args, rank, world):
     GPU arm's config (same problem, same size). One complete 257^3 solve takes ~50 s on one
     core, so K steps are capped by a time budget (TMGX_REF_BUDGET_S, default 150 s of timed
     solves after one untimed solve); `steps` reports the solves actually timed."""
-    np3, nlevels, m, kind, _, rtol, scaling = resolve(args.config, world)
+    np3, nlevels, m, kind, stages, rtol, scaling = resolve(args.config, world)
+    tele_level = stages[0][0] if stages else None
     if rank != 0:
         return
     galerkin = GALERKIN.get(args.config, False) if args.galerkin is None else args.galerkin == "on"

@@ -693,9 +693,15 @@ void Solver::build_galerkin() {
         W.cnt.launches += launch_galerkin(up.dist->geo[q], up.op[q], D.geo[q], nd.S.p[q], D.geo[q].total,
                                           spheres_dev, (int)spheres.size(), prob.k_in, W.stream);
     }
+    static const bool sym_env = [] {  // TMGX_G27_SYM=0: read all 27 planes in the perf build too
+      const char* e = std::getenv("TMGX_G27_SYM");
+      return e ? std::atoi(e) != 0 : true;
+    }();
     for (size_t q = 0; q < D.local.size(); ++q) {
+      const BoxGeo& g = D.geo[q];
       nd.op[q].S = nd.S.p[q];
-      nd.op[q].S_stride = D.geo[q].total;
+      nd.op[q].S_stride = g.total;
+      nd.op[q].sym27 = !parity_build() && sym_env && g.ex == g.Nx && g.ey == g.Ny && g.ez == g.Nz ? 1 : 0;
     }
   }
   sync();

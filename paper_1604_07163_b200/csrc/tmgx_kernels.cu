@@ -2619,7 +2619,8 @@ __device__ __forceinline__ double cc_row(const BoxGeo& g, const OpParams& op, co
 #pragma unroll
     for (int s = 0; s < 27; ++s) {
       const long long o = (long long)(s / 9 - 1) * g.pxy + (long long)((s / 3) % 3 - 1) * g.px + (s % 3 - 1);
-      acc += op.S[s * op.S_stride + v] * u[v + o];
+      const double a = (op.sym27 && s > 13) ? op.S[(26 - s) * op.S_stride + v + o] : op.S[s * op.S_stride + v];
+      acc += a * u[v + o];  // the same values as k_march27<SYM>
     }
     invd = 1.0 / op.S[13 * op.S_stride + v];
     return acc;
@@ -2913,17 +2914,13 @@ static void march(const BoxGeo& g, const OpParams& op, const double* u, const F&
       return e ? std::atoi(e) : 0;
     }();
 #ifndef TMGX_PARITY
-    static const bool sym = [] {
-      const char* e = std::getenv("TMGX_G27_SYM");
-      return e ? std::atoi(e) != 0 : true;
-    }();
-    // single-box levels only: the mirrored slot of a vertex on a box face lives in the
-    // neighbouring box (coefficient planes have no halo); out-of-grid ghosts hold zeros
+    // op.sym27 (set by the engine): single-box levels only -- the mirrored slot of a vertex on a
+    // box face lives in the neighbouring box (coefficient planes have no halo)
     static const int sym_mb = [] {  // resident blocks requested for the symmetric variant
       const char* e = std::getenv("TMGX_M27_SYM_MB");
       return e ? std::atoi(e) : 3;  // measured at 257^3: step 645 -> 632 us, residual 534 -> 521 us
     }();
-    if (sym && v27 == 0 && g.ex == g.Nx && g.ey == g.Ny && g.ez == g.Nz) {
+    if (op.sym27 && v27 == 0) {
       if (sym_mb == 3)
         k_march27<F, 3, false, true><<<tile_grid(g), kBlock, 0, s>>>(g, op, u, f);
       else if (sym_mb == 4)

@@ -48,6 +48,9 @@ struct OpParams {
   const double* k;          // vertex coefficient (padded layout, ghosts filled); nullptr = k == 1
   const double* S;          // Galerkin level: 27 row-coefficient planes (slot s at S + s*S_stride)
   long long S_stride;
+  // performance build, single box covering the grid: read the 13 upper slots as the mirrored
+  // lower slots of the neighbour's row (14 planes from HBM; tmgx_kernels.cu row27)
+  int sym27;
   // Variable k, precomputed rows: planes D (diagonal), FX, FY, FZ (+x/+y/+z face terms
   // harm(k_v, k_nb)/h^2) at fc + {0,1,2,3}*fc_stride; the -x/-y/-z faces are the neighbours'
   // +faces. Same values as evaluating from k, without the six divisions per row.
