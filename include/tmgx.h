@@ -226,11 +226,19 @@ int tmgx_solver_from_options(tmgx_world w, const tmgx_problem *prob, tmgx_option
 /* Q1 hexahedral linear elasticity MG-CG (BASELINE configs[4]; no reference implementation,
  * discretisation defined in tmgx_elast.cu / oracle/tmg_elast_oracle.c): N^3 vertices x 3 dofs,
  * E_e = 10^(3 u(seed_e, e)) per element, nu, clamped x = 0 face, body force (0, 0, -1),
- * point-block Jacobi Chebyshev V(m,m), rediscretised coarse levels, LU on level 0. One box
- * on one GPU. Vectors: natural vertex order, 3 interleaved dofs (host or device memory). */
+ * point-block Jacobi Chebyshev V(m,m), rediscretised coarse levels, LU on level 0. The levels
+ * are split into the world's boxes exactly like the scalar path (GridHeader of R ranks over P
+ * processes, box halos, rank-ordered dot sums) and may be telescoped onto fewer boxes
+ * (tmgx_elast_create_mg; cfg5: 8 boxes, reduction factor 8 at level 3). Vectors: the level's
+ * global natural vertex order, 3 interleaved dofs (host or device memory); each process reads
+ * and writes the entries of its own boxes. Collective over the processes. */
 typedef struct tmgx_elast_s *tmgx_elast;
 int tmgx_elast_create(tmgx_world w, const int64_t np[3], int nlevels, int smooth_its, int est_mode, uint64_t seed_e,
                       double nu, tmgx_elast *out);
+/* Same with the full MG description: nlevels, smooth_its, est_mode, optional cheb_bounds
+ * [2*nlevels], telescope stages (TelescopePC); galerkin must be 0. */
+int tmgx_elast_create_mg(tmgx_world w, const int64_t np[3], const tmgx_mg_cfg *mg, uint64_t seed_e, double nu,
+                         tmgx_elast *out);
 int tmgx_elast_destroy(tmgx_elast e);
 int tmgx_elast_kref(double nu, double *k576);      /* 24x24 reference stiffness (E = 1, unit cube) */
 int tmgx_elast_level_info(tmgx_elast e, int level, int64_t np[3], double *lo, double *hi);

@@ -577,20 +577,32 @@ int tmgx_telescope_timing(tmgx_solver s, int stage, int reps, double* t_setup_s,
 }
 
 // ---- Q1 elasticity (tmgx_elast.cu)
+static int elast_create(tmgx_world w, const int64_t np[3], const tmgx::MGDesc& md, uint64_t seed_e, double nu,
+                        tmgx_elast* out) {
+  auto e = new tmgx_elast_s;
+  e->world = w;
+  try {
+    e->s = std::make_unique<tmgx::ElastSolver>(*w->w, np, md, seed_e, nu);
+  } catch (...) {
+    delete e;
+    throw;
+  }
+  *out = e;
+  return 0;
+}
 int tmgx_elast_create(tmgx_world w, const int64_t np[3], int nlevels, int smooth_its, int est_mode, uint64_t seed_e,
                       double nu, tmgx_elast* out) {
   return guard([&] {
-    auto e = new tmgx_elast_s;
-    e->world = w;
-    try {
-      e->s = std::make_unique<tmgx::ElastSolver>(*w->w, np, nlevels, smooth_its, est_mode, seed_e, nu);
-    } catch (...) {
-      delete e;
-      throw;
-    }
-    *out = e;
-    return 0;
+    tmgx::MGDesc md;
+    md.nlevels = nlevels;
+    md.m = smooth_its;
+    md.est_mode = est_mode;
+    return elast_create(w, np, md, seed_e, nu, out);
   });
+}
+int tmgx_elast_create_mg(tmgx_world w, const int64_t np[3], const tmgx_mg_cfg* mg, uint64_t seed_e, double nu,
+                         tmgx_elast* out) {
+  return guard([&] { return elast_create(w, np, to_mg(mg), seed_e, nu, out); });
 }
 int tmgx_elast_destroy(tmgx_elast e) {
   return guard([&] {
@@ -604,36 +616,33 @@ int tmgx_elast_kref(double nu, double* k576) {
     return 0;
   });
 }
-static int el_check(tmgx_elast e, int level) {
-  if (level < 0 || level >= (int)e->s->L.size()) throw tmg::ConfigError("elasticity: no such level");
-  return level;
-}
 int tmgx_elast_level_info(tmgx_elast e, int level, int64_t np[3], double* lo, double* hi) {
   return guard([&] {
-    const auto& L = e->s->L[el_check(e, level)];
-    if (np) np[0] = L.g.ex, np[1] = L.g.ey, np[2] = L.g.ez;
-    if (lo) *lo = L.lo;
-    if (hi) *hi = L.hi;
+    const auto& nd = e->s->nodes[(size_t)e->s->node_for_level(level)];
+    if (np) np[0] = nd.dist->h.npoints[0], np[1] = nd.dist->h.npoints[1], np[2] = nd.dist->h.npoints[2];
+    if (lo) *lo = nd.lo;
+    if (hi) *hi = nd.hi;
     return 0;
   });
 }
 int tmgx_elast_rhs(tmgx_elast e, double* b) {
   return guard([&] {
     // b_z(v) = sum over incident elements of -h^3/8 (exact: powers of two), 0 on clamped dofs
-    const auto& g = e->s->L.back().g;
-    const double h = e->s->L.back().h, q = -(h * h * h) / 8.0;
-    for (int k = 0; k < g.ez; ++k)
-      for (int j = 0; j < g.ey; ++j)
-        for (int i = 0; i < g.ex; ++i) {
+    const auto& nd = e->s->nodes[0];
+    const long long nx = nd.dist->h.npoints[0], ny = nd.dist->h.npoints[1], nz = nd.dist->h.npoints[2];
+    const double h = nd.h, q = -(h * h * h) / 8.0;
+    for (long long k = 0; k < nz; ++k)
+      for (long long j = 0; j < ny; ++j)
+        for (long long i = 0; i < nx; ++i) {
           double acc = 0.0;
           for (int ez = -1; ez <= 0; ++ez)
             for (int ey = -1; ey <= 0; ++ey)
               for (int ex = -1; ex <= 0; ++ex) {
-                const int ei = i + ex, ej = j + ey, ek = k + ez;
-                if (ei < 0 || ej < 0 || ek < 0 || ei >= g.ex - 1 || ej >= g.ey - 1 || ek >= g.ez - 1) continue;
+                const long long ei = i + ex, ej = j + ey, ek = k + ez;
+                if (ei < 0 || ej < 0 || ek < 0 || ei >= nx - 1 || ej >= ny - 1 || ek >= nz - 1) continue;
                 acc += q;
               }
-          const long long v = i + (long long)g.ex * (j + (long long)g.ey * k);
+          const long long v = i + nx * (j + ny * k);
           b[3 * v + 0] = 0.0;
           b[3 * v + 1] = 0.0;
           b[3 * v + 2] = i == 0 ? 0.0 : acc;
@@ -644,32 +653,33 @@ int tmgx_elast_rhs(tmgx_elast e, double* b) {
 int tmgx_elast_level_apply(tmgx_elast e, int level, const double* x, double* y) {
   return guard([&] {
     auto& S = *e->s;
-    auto& L = S.L[el_check(e, level)];
-    S.upload(level, x, L.x);
-    S.apply(level, L.x, L.ad);
-    S.download(level, L.ad, y);
+    const int i = S.node_for_level(level);
+    auto& nd = S.nodes[(size_t)i];
+    S.upload(i, x, nd.x);
+    S.apply(i, nd.x, nd.ad);
+    S.download(i, nd.ad, y);
     return 0;
   });
 }
 int tmgx_elast_level_smooth(tmgx_elast e, int level, const double* b, double* x) {
   return guard([&] {
     auto& S = *e->s;
-    auto& L = S.L[el_check(e, level)];
-    if (level == 0) throw tmg::ConfigError("elasticity: level 0 is the LU level");
-    S.upload(level, b, L.b);
-    S.upload(level, x, L.x);
-    S.smooth(level, L.b, L.x);
-    S.download(level, L.x, x);
+    const int i = S.node_for_level(level);
+    auto& nd = S.nodes[(size_t)i];
+    if (nd.kind != tmgx::SMOOTH) throw tmg::ConfigError("elasticity: level 0 is the LU level");
+    S.upload(i, b, nd.b);
+    S.upload(i, x, nd.x);
+    S.smooth(i, nd.b, nd.x);
+    S.download(i, nd.x, x);
     return 0;
   });
 }
 int tmgx_elast_pc_apply(tmgx_elast e, const double* x, double* y) {
   return guard([&] {
     auto& S = *e->s;
-    const int top = (int)S.L.size() - 1;
-    S.upload(top, x, S.cr);
-    S.vcycle(top, S.cr, S.cz);
-    S.download(top, S.cz, y);
+    S.upload(0, x, S.cr);
+    S.vcycle(0);
+    S.download(0, S.cz, y);
     return 0;
   });
 }
@@ -698,21 +708,22 @@ int tmgx_elast_bench_apply(tmgx_elast e, int iters, double* ms_per_launch, doubl
                             double* flops_per_launch) {
   return guard([&] {
     auto& S = *e->s;
-    const int top = (int)S.L.size() - 1;
-    auto& L = S.L[top];
-    for (int w = 0; w < 3; ++w) S.apply(top, L.x, L.ad);
+    auto& nd = S.nodes[0];
+    if (nd.dist->geo.empty()) throw tmg::ConfigError("elasticity: no local box on the finest level");
+    for (int w = 0; w < 3; ++w) S.apply(0, nd.x, nd.ad);
     cudaEvent_t e0, e1;
     tmgx::cuda_check(cudaEventCreate(&e0), "event");
     tmgx::cuda_check(cudaEventCreate(&e1), "event");
     tmgx::cuda_check(cudaEventRecord(e0, S.W.stream), "record");
-    for (int it = 0; it < iters; ++it) S.apply(top, L.x, L.ad);
+    for (int it = 0; it < iters; ++it) S.apply(0, nd.x, nd.ad);
     tmgx::cuda_check(cudaEventRecord(e1, S.W.stream), "record");
     tmgx::cuda_check(cudaEventSynchronize(e1), "sync");
     float ms = 0.f;
     cudaEventElapsedTime(&ms, e0, e1);
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
-    const double nv = (double)L.g.ex * L.g.ey * L.g.ez;
+    double nv = 0.0;
+    for (const auto& g : nd.dist->geo) nv += (double)g.ex * g.ey * g.ez;
     *ms_per_launch = ms / iters;
     *bytes_per_launch = nv * (24.0 + 24.0 + 8.0);     // x in, y out, one modulus per element
     *flops_per_launch = nv * 576.0 * 2.0;               // 8 elements x 8 vertices x 3 x 3 FMAs

@@ -11,9 +11,15 @@
 //   solve_cg (solver.cpp:214-266), solve_fixed (solver.cpp:79-110) and estimator
 //   (solver.cpp:520-581) drive it.
 //
-// B200 layout: each level is one box (single GPU) in the padded layout of tmgx_kernels.cuh;
-// a 3-dof vector is three consecutive component planes of that layout (component c at
-// p + c * total), elements (ei, ej, ek) live at the vertex slot of their lower corner. The
+// B200 layout: each level is split into the boxes of the scalar path's GridHeader (one box per
+// reference rank, boxes over processes / GPUs as the World says) in the padded layout of
+// tmgx_kernels.cuh; a 3-dof vector is three consecutive component planes of that layout
+// (component c at p + c * total), elements (ei, ej, ek) live at the vertex slot of their lower
+// corner, each box holding its elements and the ring of the lower neighbours' elements. Box
+// halos, telescope gathers / scatters and the rank-ordered dot sums reuse the scalar path's
+// region plans and peer-mailbox transport (per component), so the same node list (SMOOTH /
+// TELESCOPE / COARSE, build_node_specs) drives the V-cycle: cfg5's 8 boxes telescoped r = 8
+// at level 3 onto one box. The
 // operator is matrix-free and vertex-centric: a thread gathers its row from the 8 incident
 // elements (576 fused multiply-adds with K_ref in constant memory, one E h scaling per
 // element); everything else reuses the
@@ -71,7 +77,7 @@ __global__ void __launch_bounds__(128) k_el_apply(BoxGeo g, const double* __rest
     for (int ey = -1; ey <= 0; ++ey)
 #pragma unroll
       for (int ex = -1; ex <= 0; ++ex) {
-        const int ei = i + ex, ej = j + ey, ek = k + ez;
+        const int ei = g.gx + i + ex, ej = g.gy + j + ey, ek = g.gz + k + ez;  // global element
         if (ei < 0 || ej < 0 || ek < 0 || ei >= nx - 1 || ej >= ny - 1 || ek >= nz - 1) continue;
         const double eh = __ldg(Ev + ex + ey * px + ez * pxy) * h;
         const int l = -ex + 2 * (-ey) + 4 * (-ez);
@@ -127,7 +133,9 @@ __global__ void k_el_binv(BoxGeo g, const double* __restrict__ E, double h, doub
     for (int ey = -1; ey <= 0; ++ey)
       for (int ex = -1; ex <= 0; ++ex) {
         const int ei = i + ex, ej = j + ey, ek = k + ez;
-        if (ei < 0 || ej < 0 || ek < 0 || ei >= nx - 1 || ej >= ny - 1 || ek >= nz - 1) continue;
+        if (g.gx + ei < 0 || g.gy + ej < 0 || g.gz + ek < 0 || g.gx + ei >= nx - 1 || g.gy + ej >= ny - 1 ||
+            g.gz + ek >= nz - 1)
+          continue;
         const double eh = E[vx(g, ei, ej, ek)] * h;
         const int l = -ex + 2 * (-ey) + 4 * (-ez);
         for (int bb = 0; bb < 3; ++bb)
@@ -244,11 +252,12 @@ __global__ void __launch_bounds__(256) k_el_dot_sum(const double* __restrict__ p
   if (threadIdx.x == 0) *out = sh[0];
 }
 
-// natural interleaved (3 v + c) <-> component planes
+// global natural interleaved (3 v + c, v the level's natural vertex index) <-> the box's planes
 __global__ void k_el_pack(BoxGeo g, const double* __restrict__ src, double* __restrict__ dst, int to_compact) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y, k = blockIdx.z;
   if (i >= g.ex || j >= g.ey) return;
-  const long long v = vx(g, i, j, k), n = i + (long long)g.ex * (j + (long long)g.ey * k);
+  const long long v = vx(g, i, j, k),
+                  n = (g.gx + i) + (long long)g.Nx * ((g.gy + j) + (long long)g.Ny * (g.gz + k));
   for (int c = 0; c < 3; ++c) {
     if (to_compact)
       dst[3 * n + c] = src[c * g.total + v];
@@ -313,216 +322,360 @@ void q1_kref(double nu, double* K) {
   }
 }
 
+
 // ------------------------------------------------------------------------------------------
 // hierarchy
 // ------------------------------------------------------------------------------------------
-void ElastSolver::apply(int l, const double* x, double* y) {
-  k_el_apply<0><<<fgrid(L[l].g), 128, 0, W.stream>>>(L[l].g, L[l].E, L[l].h, x, nullptr, y);
-  ++launches;
+Field ElastSolver::make3(const Dist& D) {
+  Field f;
+  for (const auto& g : D.geo) f.p.push_back(arena.alloc(3 * g.total));
+  return f;
 }
-void ElastSolver::residual(int l, const double* b, const double* x, double* r) {
-  k_el_apply<1><<<fgrid(L[l].g), 128, 0, W.stream>>>(L[l].g, L[l].E, L[l].h, x, b, r);
-  ++launches;
+Field ElastSolver::comp(int i, const Field& f, int c) const {
+  Field o;
+  const Dist& D = *nodes[(size_t)i].dist;
+  for (size_t q = 0; q < f.p.size(); ++q) o.p.push_back(f.p[q] + c * D.geo[q].total);
+  return o;
 }
-void ElastSolver::jacobi(int l, const double* x, double* y) {
-  k_el_jacobi<<<vgrid(L[l].g), 128, 0, W.stream>>>(L[l].g, L[l].binv, x, y);
-  ++launches;
-}
-void ElastSolver::vec(int l, int op, double s, double t, const double* x, double* y) {
-  const long long n = L[l].n3();
-  const int blocks = (int)std::min<long long>((n + 255) / 256, 4 * 148 * 8);
-  k_el_vec<<<blocks, 256, 0, W.stream>>>(n, op, s, t, x, y);
-  ++launches;
-}
-double ElastSolver::dot(int l, const double* a, const double* b) {
-  if (parity_build()) {
-    k_el_fold_dot<<<1, 1, 0, W.stream>>>(L[l].g, a, b, dot_out);
-    ++launches;
-  } else {
-    k_el_dot_part<<<1184, 256, 0, W.stream>>>(L[l].g, a, b, dot_part);
-    k_el_dot_sum<<<1, 256, 0, W.stream>>>(dot_part, 1184, dot_out);
-    launches += 2;
-  }
-  double h = 0.0;
-  CK(cudaMemcpyAsync(&h, dot_out, sizeof(double), cudaMemcpyDeviceToHost, W.stream));
+void ElastSolver::sync() {
   CK(cudaStreamSynchronize(W.stream));
-  return h;
+  W.check();
 }
-void ElastSolver::coarse_solve(const double* b, double* x) {
-  if (parity_build())
-    launches += launch_lu_solve(A_dev, piv_dev, nc, map_dev, b, x, W.stream);
-  else
-    launches += launch_dense_matvec(A_dev, nc, map_dev, b, x, W.stream);
-}
-void ElastSolver::upload(int l, const double* host, double* dev) {
-  const long long n = 3LL * L[l].g.ex * L[l].g.ey * L[l].g.ez;
-  CK(cudaMemcpyAsync(staging, host, sizeof(double) * n, cudaMemcpyDefault, W.stream));
-  k_el_pack<<<vgrid(L[l].g), 128, 0, W.stream>>>(L[l].g, staging, dev, 0);
-  ++launches;
-}
-void ElastSolver::download(int l, const double* dev, double* host) {
-  const long long n = 3LL * L[l].g.ex * L[l].g.ey * L[l].g.ez;
-  k_el_pack<<<vgrid(L[l].g), 128, 0, W.stream>>>(L[l].g, dev, staging, 1);
-  ++launches;
-  CK(cudaMemcpyAsync(host, staging, sizeof(double) * n, cudaMemcpyDefault, W.stream));
-  CK(cudaStreamSynchronize(W.stream));
+int ElastSolver::node_for_level(int level) const {
+  int best = -1;
+  for (size_t i = 0; i < nodes.size(); ++i)
+    if (nodes[i].level == level) best = (int)i;
+  if (best < 0) throw tmg::ConfigError("elasticity: no such level");
+  return best;
 }
 
-ElastSolver::ElastSolver(World& W_, const int64_t np[3], int nlevels, int m_, int est_mode, uint64_t seed_e, double nu)
-    : W(W_), m(m_) {
+void ElastSolver::halo(int i, const Field& f) {
+  for (int c = 0; c < 3; ++c) {
+    const Field fc = comp(i, f, c);
+    run_plan(W, nodes[(size_t)i].halo, fc, fc, false);
+  }
+}
+void ElastSolver::apply(int i, const Field& x, const Field& y) {
+  ElNode& nd = nodes[(size_t)i];
+  halo(i, x);
+  for (size_t q = 0; q < nd.dist->geo.size(); ++q) {
+    const BoxGeo& g = nd.dist->geo[q];
+    k_el_apply<0><<<fgrid(g), 128, 0, W.stream>>>(g, nd.E[q], nd.h, x.p[q], nullptr, y.p[q]);
+    ++launches;
+  }
+}
+void ElastSolver::residual(int i, const Field& b, const Field& x, const Field& r) {
+  ElNode& nd = nodes[(size_t)i];
+  halo(i, x);
+  for (size_t q = 0; q < nd.dist->geo.size(); ++q) {
+    const BoxGeo& g = nd.dist->geo[q];
+    k_el_apply<1><<<fgrid(g), 128, 0, W.stream>>>(g, nd.E[q], nd.h, x.p[q], b.p[q], r.p[q]);
+    ++launches;
+  }
+}
+void ElastSolver::jacobi(int i, const Field& x, const Field& y) {
+  ElNode& nd = nodes[(size_t)i];
+  for (size_t q = 0; q < nd.dist->geo.size(); ++q) {
+    k_el_jacobi<<<vgrid(nd.dist->geo[q]), 128, 0, W.stream>>>(nd.dist->geo[q], nd.binv[q], x.p[q], y.p[q]);
+    ++launches;
+  }
+}
+void ElastSolver::vec(int i, int op, double s, double t, const Field& x, const Field& y) {
+  const Dist& D = *nodes[(size_t)i].dist;
+  for (size_t q = 0; q < D.geo.size(); ++q) {
+    const long long n = 3 * D.geo[q].total;
+    const int blocks = (int)std::min<long long>((n + 255) / 256, 4 * 148 * 8);
+    k_el_vec<<<blocks, 256, 0, W.stream>>>(n, op, s, t, x.p[q], y.p[q]);
+    ++launches;
+  }
+}
+void ElastSolver::zero(int i, const Field& f) {
+  const Dist& D = *nodes[(size_t)i].dist;
+  for (size_t q = 0; q < D.geo.size(); ++q)
+    CK(cudaMemsetAsync(f.p[q], 0, sizeof(double) * 3 * D.geo[q].total, W.stream));
+}
+// a.b over the node's communicator: per box a fixed tree (performance build) or the serial fold
+// in natural dof order (parity build; the reference's dot on one rank), then the rank-ordered
+// sum of the box values (ordered_fold_sum, comm.cpp:338-351). One box: the box's value itself.
+double ElastSolver::dot(int i, const Field& a, const Field& b) {
+  const Dist& D = *nodes[(size_t)i].dist;
+  for (size_t q = 0; q < D.geo.size(); ++q) {
+    double* out = rank_sums + D.wr[(size_t)D.local[q]];
+    if (parity_build()) {
+      k_el_fold_dot<<<1, 1, 0, W.stream>>>(D.geo[q], a.p[q], b.p[q], out);
+      ++launches;
+    } else {
+      k_el_dot_part<<<1184, 256, 0, W.stream>>>(D.geo[q], a.p[q], b.p[q], dot_part);
+      k_el_dot_sum<<<1, 256, 0, W.stream>>>(dot_part, 1184, out);
+      launches += 2;
+    }
+  }
+  push_ranksums(W, rank_sums, 1, peer_mail, rs_last_bar);
+  CK(cudaMemcpyAsync(host_sums, rank_sums, sizeof(double) * W.R, cudaMemcpyDeviceToHost, W.stream));
+  sync();
+  double s = host_sums[D.wr[0]];
+  for (int r = 1; r < D.h.n_ranks(); ++r) s += host_sums[D.wr[(size_t)r]];
+  return s;
+}
+void ElastSolver::coarse_solve(int i) {
+  ElNode& nd = nodes[(size_t)i];
+  if (nd.dist->local.empty()) return;
+  if (parity_build())
+    launches += launch_lu_solve(nd.A_dev, nd.piv_dev, nd.nc, nd.map_dev, nd.b.p[0], nd.x.p[0], W.stream);
+  else
+    launches += launch_dense_matvec(nd.A_dev, nd.nc, nd.map_dev, nd.b.p[0], nd.x.p[0], W.stream);
+}
+void ElastSolver::upload(int i, const double* src, const Field& f) {
+  const ElNode& nd = nodes[(size_t)i];
+  const Dist& D = *nd.dist;
+  if (D.geo.empty()) return;
+  CK(cudaMemcpyAsync(staging, src, sizeof(double) * nd.n_global(), cudaMemcpyDefault, W.stream));
+  for (size_t q = 0; q < D.geo.size(); ++q) {
+    k_el_pack<<<vgrid(D.geo[q]), 128, 0, W.stream>>>(D.geo[q], staging, f.p[q], 0);
+    ++launches;
+  }
+}
+void ElastSolver::download(int i, const Field& f, double* dst) {
+  const ElNode& nd = nodes[(size_t)i];
+  const Dist& D = *nd.dist;
+  if (D.geo.empty()) return;
+  const auto& N = D.h.npoints;
+  for (size_t q = 0; q < D.geo.size(); ++q) {
+    k_el_pack<<<vgrid(D.geo[q]), 128, 0, W.stream>>>(D.geo[q], f.p[q], staging, 1);
+    ++launches;
+  }
+  if (D.h.n_ranks() == (int)D.geo.size()) {  // every box here: one linear copy
+    CK(cudaMemcpyAsync(dst, staging, sizeof(double) * nd.n_global(), cudaMemcpyDefault, W.stream));
+  } else {  // this process's boxes only: one pitched 3D copy per box
+    for (const BoxGeo& g : D.geo) {
+      cudaMemcpy3DParms pr{};
+      pr.srcPtr = make_cudaPitchedPtr(staging, sizeof(double) * 3 * N[0], 3 * N[0], N[1]);
+      pr.dstPtr = make_cudaPitchedPtr(dst, sizeof(double) * 3 * N[0], 3 * N[0], N[1]);
+      pr.srcPos = pr.dstPos = make_cudaPos(sizeof(double) * 3 * g.gx, g.gy, g.gz);
+      pr.extent = make_cudaExtent(sizeof(double) * 3 * g.ex, g.ey, g.ez);
+      pr.kind = cudaMemcpyDefault;
+      CK(cudaMemcpy3DAsync(&pr, W.stream));
+    }
+  }
+  sync();
+}
+
+ElastSolver::ElastSolver(World& W_, const int64_t np[3], const MGDesc& M, uint64_t seed_e, double nu)
+    : W(W_), mgd(M), m(M.m) {
   CK(cudaSetDevice(W.device));
   arena.set_stream(W.stream);
-  if (W.R != 1 || W.P != 1)
-    throw tmg::ConfigError("elasticity path: one box on one GPU (box split + telescope not implemented)");
-  if (nlevels < 1 || m < 1) throw tmg::ConfigError("elasticity: nlevels and smooth_its must be >= 1");
+  const int nlev = mgd.nlevels;
+  if (nlev < 1 || m < 1) throw tmg::ConfigError("elasticity: nlevels and smooth_its must be >= 1");
+  if (mgd.galerkin) throw tmg::ConfigError("elasticity: rediscretised coarse levels only (no -pc_mg_galerkin)");
+  if (!mgd.bounds.empty() && (int)mgd.bounds.size() != 2 * nlev)
+    throw tmg::ConfigError("elasticity: cheb_bounds needs 2 * nlevels values");
+  if (np[0] != np[1] || np[1] != np[2]) throw tmg::ConfigError("elasticity: cubic grids only (h uniform)");
   double K[576];
   q1_kref(nu, K);
   CK(cudaMemcpyToSymbolAsync(c_K, K, sizeof K, 0, cudaMemcpyHostToDevice, W.stream));
   CK(cudaStreamSynchronize(W.stream));
-  // level ladder (coarsest first)
-  std::vector<std::array<int64_t, 3>> dims(nlevels);
-  std::array<int64_t, 3> n = {np[0], np[1], np[2]};
-  if (n[0] != n[1] || n[1] != n[2]) throw tmg::ConfigError("elasticity: cubic grids only (h uniform)");
-  for (int l = nlevels - 1; l >= 0; --l) {
-    dims[l] = n;
-    if (l > 0) {
-      for (int a = 0; a < 3; ++a) {
-        if (n[a] < 3 || n[a] % 2 == 0) throw tmg::ConfigError("elasticity: cannot coarsen (need 2M+1 vertices)");
-        n[a] = (n[a] + 1) / 2;
+  ProblemDesc P;
+  P.np = {np[0], np[1], np[2]};
+  const std::vector<NodeSpec> specs = build_node_specs(W, P, mgd);  // ConfigError: cannot coarsen / split
+  // element moduli per level on the host, global (the oracle's pow / mean sequence)
+  std::vector<std::vector<double>> Eg((size_t)nlev);
+  std::vector<long long> Ng((size_t)nlev);
+  {
+    long long n = np[0];
+    for (int l = nlev - 1; l >= 0; --l) {
+      Ng[(size_t)l] = n;
+      if (l > 0) n = (n + 1) / 2;
+    }
+    for (int l = nlev - 1; l >= 0; --l) {
+      const long long mx = std::max(Ng[(size_t)l] - 1, 0LL);
+      std::vector<double>& Eh = Eg[(size_t)l];
+      Eh.assign((size_t)(mx * mx * mx), 0.0);
+      if (l == nlev - 1) {
+        for (size_t e = 0; e < Eh.size(); ++e) Eh[e] = std::pow(10.0, 3.0 * hashed_uniform_h(seed_e, (uint64_t)e));
+      } else {
+        const auto& F = Eg[(size_t)l + 1];
+        const long long fx = 2 * mx;
+        for (long long K2 = 0; K2 < mx; ++K2)
+          for (long long J = 0; J < mx; ++J)
+            for (long long I = 0; I < mx; ++I) {
+              double acc = 0.0;
+              for (int c = 0; c < 8; ++c)
+                acc += F[(size_t)((2 * I + (c & 1)) + fx * ((2 * J + ((c >> 1) & 1)) + fx * (2 * K2 + (c >> 2))))];
+              Eh[(size_t)(I + mx * (J + mx * K2))] = 0.125 * acc;
+            }
       }
     }
   }
-  L.resize(nlevels);
-  double h = 1.0 / (double)(np[0] - 1);
-  std::vector<std::vector<double>> Ehost(nlevels);
-  for (int l = nlevels - 1; l >= 0; --l, h *= 2.0) {
-    ElLevel& lv = L[l];
-    BoxGeo g{};
-    g.ex = (int)dims[l][0];
-    g.ey = (int)dims[l][1];
-    g.ez = (int)dims[l][2];
-    g.gx = g.gy = g.gz = 0;
-    g.Nx = g.ex;
-    g.Ny = g.ey;
-    g.Nz = g.ez;
-    g.zc = choose_zc(g.ex, g.ey, g.ez);
-    g.px = ((kXO + g.ex + 1) + 3) / 4 * 4;
-    g.pxy = g.px * (g.ey + 2);
-    g.base = kXO + g.px + g.pxy;
-    g.total = g.pxy * (g.ez + 2) + 8;
-    lv.g = g;
-    lv.h = h;
-    // element moduli on the host (the oracle's pow / mean sequence), padded upload
-    const int mx = g.ex - 1, my = g.ey - 1, mz = g.ez - 1;
-    std::vector<double>& Eh = Ehost[l];
-    Eh.assign((size_t)std::max(mx, 0) * std::max(my, 0) * std::max(mz, 0), 0.0);
-    if (l == nlevels - 1) {
-      for (size_t e = 0; e < Eh.size(); ++e) Eh[e] = std::pow(10.0, 3.0 * hashed_uniform_h(seed_e, (uint64_t)e));
-    } else {
-      const auto& F = Ehost[l + 1];
-      const int fx = 2 * mx, fy = 2 * my;
-      for (int K2 = 0; K2 < mz; ++K2)
-        for (int J = 0; J < my; ++J)
-          for (int I = 0; I < mx; ++I) {
-            double acc = 0.0;
-            for (int c = 0; c < 8; ++c)
-              acc += F[(size_t)(2 * I + (c & 1)) + (size_t)fx * ((2 * J + ((c >> 1) & 1)) + (size_t)fy * (2 * K2 + (c >> 2)))];
-            Eh[(size_t)I + (size_t)mx * (J + (size_t)my * K2)] = 0.125 * acc;
+  long long stage_n = 1;
+  for (const NodeSpec& sp : specs) {
+    ElNode nd;
+    nd.kind = sp.kind;
+    nd.level = sp.level;
+    nd.dist = sp.dist;
+    const Dist& D = *nd.dist;
+    if (D.h.npoints[0] != Ng[(size_t)nd.level]) throw tmg::Error("elasticity: level ladder mismatch");
+    nd.h = 1.0 / (double)(D.h.npoints[0] - 1);
+    const long long mx = D.h.npoints[0] - 1;
+    const std::vector<double>& Eh = Eg[(size_t)nd.level];
+    for (const BoxGeo& g : D.geo) {
+      // the box's elements plus the ring of the lower neighbours' (slot -1 on each axis)
+      std::vector<double> Epad((size_t)g.total, 0.0);
+      for (int k = -1; k < g.ez; ++k)
+        for (int j = -1; j < g.ey; ++j)
+          for (int i = -1; i < g.ex; ++i) {
+            const long long ei = g.gx + i, ej = g.gy + j, ek = g.gz + k;
+            if (ei < 0 || ej < 0 || ek < 0 || ei >= mx || ej >= mx || ek >= mx) continue;
+            Epad[(size_t)(g.base + i + g.px * j + g.pxy * k)] = Eh[(size_t)(ei + mx * (ej + mx * ek))];
           }
+      double* E = arena.alloc(g.total);
+      arena.upload(E, Epad.data(), sizeof(double) * g.total);
+      double* binv = arena.alloc(9 * g.total);
+      k_el_binv<<<vgrid(g), 128, 0, W.stream>>>(g, E, nd.h, binv);
+      nd.E.push_back(E);
+      nd.binv.push_back(binv);
     }
-    std::vector<double> Epad((size_t)g.total, 0.0);
-    for (int k = 0; k < mz; ++k)
-      for (int j = 0; j < my; ++j)
-        for (int i = 0; i < mx; ++i)
-          Epad[(size_t)(g.base + i + g.px * j + g.pxy * k)] = Eh[(size_t)i + (size_t)mx * (j + (size_t)my * k)];
-    lv.E = arena.alloc(g.total);
-    arena.upload(lv.E, Epad.data(), sizeof(double) * g.total);
-    lv.binv = arena.alloc(9 * g.total);
-    k_el_binv<<<vgrid(g), 128, 0, W.stream>>>(g, lv.E, lv.h, lv.binv);
-    for (double** f : {&lv.b, &lv.x, &lv.r, &lv.z, &lv.d, &lv.ad}) *f = arena.alloc(3 * g.total);
+    stage_n = std::max(stage_n, nd.n_global());
+    nd.halo = upload_plan(arena, halo_plan_host(W, D));
+    nodes.push_back(std::move(nd));
   }
-  const BoxGeo& gt = L.back().g;
-  for (double** f : {&cr, &cz, &cp, &cw, &cx}) *f = arena.alloc(3 * gt.total);
+  for (size_t i = 0; i < nodes.size(); ++i) {
+    ElNode& nd = nodes[i];
+    const Dist& D = *nd.dist;
+    if (i == 0) {
+      cr = make3(D);
+      cz = make3(D);
+      cp = make3(D);
+      cw = make3(D);
+      cx = make3(D);
+      nd.b = cr;
+      nd.x = cz;
+    } else {
+      nd.b = make3(D);
+      nd.x = make3(D);
+    }
+    for (Field* f : {&nd.r, &nd.z, &nd.d, &nd.ad}) *f = make3(D);
+    if (nd.kind == TELESCOPE) {  // TelescopePC setup: the P-hat^T / ScatterPlan data movement
+      nd.gather = upload_plan(arena, transfer_plan_host(W, D, *nodes[i + 1].dist));
+      nd.scatter = upload_plan(arena, transfer_plan_host(W, *nodes[i + 1].dist, D));
+    }
+  }
+  std::vector<RegionPlan*> plans;  // creation order, identical on every process
+  for (ElNode& nd : nodes) {
+    plans.push_back(&nd.halo);
+    if (nd.kind == TELESCOPE) {
+      plans.push_back(&nd.gather);
+      plans.push_back(&nd.scatter);
+    }
+  }
+  if (W.P == 1)
+    rank_sums = arena.alloc(W.R);
+  else
+    rank_sums = wire_plans(W, arena, plans, W.R, peer_mail);
+  CK(cudaMallocHost(&host_sums, sizeof(double) * W.R));
   dot_part = arena.alloc(1184);
-  dot_out = arena.alloc(1);
-  staging = arena.alloc(3 * gt.total);
-  CK(cudaStreamSynchronize(W.stream));
-  // Chebyshev intervals (SolverNode::create, solver.cpp:591-592)
-  est_lanczos = est_mode == 1;
-  for (int l = 1; l < nlevels; ++l) {
-    auto lh = estimate(l);
-    L[l].lo = lh.first;
-    L[l].hi = lh.second;
-  }
-  // coarse DenseLU: rows from the device operator applied to unit vectors (identical values)
-  {
-    const ElLevel& c = L[0];
-    const int nv = c.g.ex * c.g.ey * c.g.ez;
-    nc = 3 * nv;
-    std::vector<double> a((size_t)nc * nc), col((size_t)nc), e((size_t)nc, 0.0);
-    for (int q = 0; q < nc; ++q) {
-      e[(size_t)q] = 1.0;
-      upload(0, e.data(), c.x);
-      apply(0, c.x, c.r);
-      download(0, c.r, col.data());
-      for (int r = 0; r < nc; ++r) a[(size_t)r * nc + q] = col[(size_t)r];
-      e[(size_t)q] = 0.0;
+  staging = arena.alloc(stage_n);
+  sync();
+  // Chebyshev intervals: given, or estimated (SolverNode::create, solver.cpp:591-592)
+  est_lanczos = mgd.est_mode == 1;
+  for (size_t i = 0; i < nodes.size(); ++i) {
+    ElNode& nd = nodes[i];
+    if (nd.kind != SMOOTH) continue;
+    if (!mgd.bounds.empty()) {
+      nd.lo = mgd.bounds[(size_t)(2 * nd.level)];
+      nd.hi = mgd.bounds[(size_t)(2 * nd.level + 1)];
+    } else {
+      auto lh = estimate((int)i);
+      nd.lo = lh.first;
+      nd.hi = lh.second;
     }
-    std::vector<long long> map((size_t)nc);
-    for (int k = 0; k < c.g.ez; ++k)
-      for (int j = 0; j < c.g.ey; ++j)
-        for (int i = 0; i < c.g.ex; ++i) {
-          const int v = i + c.g.ex * (j + c.g.ey * k);
-          for (int comp = 0; comp < 3; ++comp)
-            map[(size_t)(3 * v + comp)] = comp * c.g.total + c.g.base + i + c.g.px * j + c.g.pxy * k;
-        }
-    dense_lu_setup(arena, a, nc, map, &A_dev, &piv_dev, &map_dev);
   }
+  // coarse DenseLU on its single rank: rows from the device operator applied to unit vectors
+  {
+    const int ic = (int)nodes.size() - 1;
+    ElNode& c = nodes[(size_t)ic];
+    if (!c.dist->geo.empty()) {
+      const BoxGeo& g = c.dist->geo[0];
+      const int nv = g.ex * g.ey * g.ez;
+      c.nc = 3 * nv;
+      const int nc = c.nc;
+      std::vector<double> a((size_t)nc * nc), col((size_t)nc), e((size_t)nc, 0.0);
+      for (int q = 0; q < nc; ++q) {
+        e[(size_t)q] = 1.0;
+        upload(ic, e.data(), c.x);
+        apply(ic, c.x, c.r);
+        download(ic, c.r, col.data());
+        for (int r = 0; r < nc; ++r) a[(size_t)r * nc + q] = col[(size_t)r];
+        e[(size_t)q] = 0.0;
+      }
+      std::vector<long long> map((size_t)nc);
+      for (int k = 0; k < g.ez; ++k)
+        for (int j = 0; j < g.ey; ++j)
+          for (int i = 0; i < g.ex; ++i) {
+            const int v = i + g.ex * (j + g.ey * k);
+            for (int cc = 0; cc < 3; ++cc)
+              map[(size_t)(3 * v + cc)] = cc * g.total + g.base + i + g.px * j + g.pxy * k;
+          }
+      dense_lu_setup(arena, a, nc, map, &c.A_dev, &c.piv_dev, &c.map_dev);
+    }
+  }
+  sync();
+}
+
+ElastSolver::~ElastSolver() {
+  if (W.grp) {  // collective teardown: no peer may still store into our mailbox
+    cudaStreamSynchronize(W.stream);
+    try {
+      W.grp->barrier(30.0);
+    } catch (...) {
+    }
+    for (double* p : peer_mail)
+      if (p) cudaIpcCloseMemHandle(p);
+  }
+  if (host_sums) cudaFreeHost(host_sums);
 }
 
 // chebyshev_bounds_estimate (solver.cpp:520-581) with point-block Jacobi; fill_random keyed by
-// the natural dof index 3 v + c
-std::pair<double, double> ElastSolver::estimate(int l) {
-  ElLevel& lv = L[l];
-  const BoxGeo& g = lv.g;
-  const long long nd = 3LL * g.ex * g.ey * g.ez;
-  std::vector<double> b0((size_t)nd);
-  for (long long q = 0; q < nd; ++q) b0[(size_t)q] = 2.0 * hashed_uniform_h(0x5eedbeefULL, (uint64_t)q) - 1.0;
-  double *r = lv.r, *z = lv.z, *p = lv.d, *w = lv.ad, *x = lv.x;
-  upload(l, b0.data(), r);
-  vec(l, 0, 0.0, 0.0, r, x);  // x = 0
-  jacobi(l, r, z);
-  vec(l, 0, 1.0, 0.0, z, p);  // p = z
-  double rz = dot(l, r, z);
+// the natural dof index 3 v + c of the level
+std::pair<double, double> ElastSolver::estimate(int i) {
+  ElNode& nd = nodes[(size_t)i];
+  const long long n = nd.n_global();
+  std::vector<double> b0((size_t)n);
+  for (long long q = 0; q < n; ++q) b0[(size_t)q] = 2.0 * hashed_uniform_h(0x5eedbeefULL, (uint64_t)q) - 1.0;
+  const Field &r = nd.r, &z = nd.z, &p = nd.d, &w = nd.ad, &x = nd.x;
+  upload(i, b0.data(), r);
+  zero(i, x);
+  jacobi(i, r, z);
+  vec(i, 0, 1.0, 0.0, z, p);  // p = z
+  double rz = dot(i, r, z);
   std::vector<double> alphas, betas;
   bool broke = false;
   for (int it = 0; it < 10; ++it) {
     if (rz == 0.0 || !std::isfinite(rz)) break;
-    apply(l, p, w);
-    const double pw = dot(l, p, w);
+    apply(i, p, w);
+    const double pw = dot(i, p, w);
     if (pw <= 0.0 || !std::isfinite(pw)) {
       if (alphas.empty()) broke = true;
       break;
     }
     const double alpha = rz / pw;
-    vec(l, 1, alpha, 0.0, p, x);
-    vec(l, 1, -alpha, 0.0, w, r);
-    jacobi(l, r, z);
-    const double rz_new = dot(l, r, z);
+    vec(i, 1, alpha, 0.0, p, x);
+    vec(i, 1, -alpha, 0.0, w, r);
+    jacobi(i, r, z);
+    const double rz_new = dot(i, r, z);
     alphas.push_back(alpha);
     if (rz_new <= 0.0 || !std::isfinite(rz_new)) break;
     const double beta = rz_new / rz;
     betas.push_back(beta);
     rz = rz_new;
-    if (est_lanczos) vec(l, 4, beta, 0.0, z, p);  // p = z + beta p
+    if (est_lanczos) vec(i, 4, beta, 0.0, z, p);  // p = z + beta p
   }
   if (broke || alphas.empty()) return {0.1, 1.1};
   const int na = (int)alphas.size();
   std::vector<double> d((size_t)na), e((size_t)na);
-  for (int i = 0; i < na; ++i) {
-    d[(size_t)i] = 1.0 / alphas[(size_t)i];
-    if (i > 0) d[(size_t)i] += betas[(size_t)i - 1] / alphas[(size_t)i - 1];
-    if (i + 1 < na) e[(size_t)i] = std::sqrt(betas[(size_t)i]) / alphas[(size_t)i];
+  for (int k = 0; k < na; ++k) {
+    d[(size_t)k] = 1.0 / alphas[(size_t)k];
+    if (k > 0) d[(size_t)k] += betas[(size_t)k - 1] / alphas[(size_t)k - 1];
+    if (k + 1 < na) e[(size_t)k] = std::sqrt(betas[(size_t)k]) / alphas[(size_t)k];
   }
   const double lam = tridiag_eig_max(d, e);
   if (!(lam > 0.0) || !std::isfinite(lam)) return {0.1, 1.1};
@@ -530,48 +683,62 @@ std::pair<double, double> ElastSolver::estimate(int l) {
 }
 
 // solve_fixed, Chebyshev branch (solver.cpp:79-110), the oracle's operation sequence
-void ElastSolver::smooth(int l, const double* b, double* x) {
-  ElLevel& lv = L[l];
-  const double theta = 0.5 * (lv.hi + lv.lo);
-  const double delta = 0.5 * (lv.hi - lv.lo);
+void ElastSolver::smooth(int i, const Field& b, const Field& x) {
+  ElNode& nd = nodes[(size_t)i];
+  const double theta = 0.5 * (nd.hi + nd.lo);
+  const double delta = 0.5 * (nd.hi - nd.lo);
   const double sigma = theta / delta;
   double rho = 1.0 / sigma;
-  residual(l, b, x, lv.r);  // r = b - A x
-  jacobi(l, lv.r, lv.z);
-  vec(l, 0, 1.0 / theta, 0.0, lv.z, lv.d);  // d = z * (1/theta)
+  residual(i, b, x, nd.r);  // r = b - A x
+  jacobi(i, nd.r, nd.z);
+  vec(i, 0, 1.0 / theta, 0.0, nd.z, nd.d);  // d = z * (1/theta)
   for (int it = 0; it < m; ++it) {
-    vec(l, 1, 1.0, 0.0, lv.d, x);  // x += 1.0 d
+    vec(i, 1, 1.0, 0.0, nd.d, x);  // x += 1.0 d
     if (it + 1 == m) break;
-    apply(l, lv.d, lv.ad);
-    vec(l, 1, -1.0, 0.0, lv.ad, lv.r);  // r += -1.0 ad
-    jacobi(l, lv.r, lv.z);
+    apply(i, nd.d, nd.ad);
+    vec(i, 1, -1.0, 0.0, nd.ad, nd.r);  // r += -1.0 ad
+    jacobi(i, nd.r, nd.z);
     const double rho_new = 1.0 / (2.0 * sigma - rho);
-    vec(l, 2, rho_new * rho, 2.0 * rho_new / delta, lv.z, lv.d);  // d = c1 d + c2 z
+    vec(i, 2, rho_new * rho, 2.0 * rho_new / delta, nd.z, nd.d);  // d = c1 d + c2 z
     rho = rho_new;
   }
 }
 
-void ElastSolver::vcycle(int l, const double* b, double* x) {
-  ElLevel& lv = L[l];
-  CK(cudaMemsetAsync(x, 0, sizeof(double) * lv.n3(), W.stream));
-  if (l == 0) {
-    coarse_solve(b, x);
+// mg_apply over the node list; TELESCOPE nodes gather b onto the members (per component), run
+// the members' V-cycle and scatter x back (TelescopePC::apply)
+void ElastSolver::vcycle(int i) {
+  ElNode& nd = nodes[(size_t)i];
+  zero(i, nd.x);
+  if (nd.kind == COARSE) {
+    coarse_solve(i);
     return;
   }
-  ElLevel& c = L[l - 1];
-  smooth(l, b, x);
-  residual(l, b, x, lv.r);
-  for (int comp = 0; comp < 3; ++comp)  // R = P^T per component (finite-element scaling)
-    launches += launch_restrict_scaled(lv.g, c.g, lv.r + comp * lv.g.total, c.b + comp * c.g.total, 1.0, W.stream);
-  vcycle(l - 1, c.b, c.x);
-  for (int comp = 0; comp < 3; ++comp)
-    launches += launch_prolong_add(lv.g, c.g, c.x + comp * c.g.total, x + comp * lv.g.total, W.stream);
-  smooth(l, b, x);
+  ElNode& cn = nodes[(size_t)i + 1];
+  if (nd.kind == TELESCOPE) {
+    for (int c = 0; c < 3; ++c) run_plan(W, nd.gather, comp(i, nd.b, c), comp(i + 1, cn.b, c), true);
+    vcycle(i + 1);
+    for (int c = 0; c < 3; ++c) run_plan(W, nd.scatter, comp(i + 1, cn.x, c), comp(i, nd.x, c), true);
+    return;
+  }
+  const Dist& D = *nd.dist;
+  smooth(i, nd.b, nd.x);
+  residual(i, nd.b, nd.x, nd.r);
+  halo(i, nd.r);
+  for (size_t q = 0; q < D.geo.size(); ++q)  // R = P^T per component (finite-element scaling)
+    for (int c = 0; c < 3; ++c)
+      launches += launch_restrict_scaled(D.geo[q], cn.dist->geo[q], nd.r.p[q] + c * D.geo[q].total,
+                                         cn.b.p[q] + c * cn.dist->geo[q].total, 1.0, W.stream);
+  vcycle(i + 1);
+  halo(i + 1, cn.x);
+  for (size_t q = 0; q < D.geo.size(); ++q)
+    for (int c = 0; c < 3; ++c)
+      launches += launch_prolong_add(D.geo[q], cn.dist->geo[q], cn.x.p[q] + c * cn.dist->geo[q].total,
+                                     nd.x.p[q] + c * D.geo[q].total, W.stream);
+  smooth(i, nd.b, nd.x);
 }
 
 int ElastSolver::solve(const double* b, double* x, double rtol, double atol, int max_its, bool x0_nonzero,
                        double* hist, int* reason, int* its, double* n0, double* nf, double* t_ms) {
-  const int top = (int)L.size() - 1;
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
@@ -583,14 +750,14 @@ int ElastSolver::solve(const double* b, double* x, double rtol, double atol, int
     CK(cudaEventDestroy(ev));
   }
   CK(cudaEventRecord(e0, W.stream));
-  upload(top, b, cw);  // b -> cw
+  upload(0, b, cw);  // b -> cw
   if (x && x0_nonzero)
-    upload(top, x, cx);
+    upload(0, x, cx);
   else
-    CK(cudaMemsetAsync(cx, 0, sizeof(double) * L[top].n3(), W.stream));
-  residual(top, cw, cx, cr);
-  vcycle(top, cr, cz);
-  double nrm = std::sqrt(dot(top, cz, cz));
+    zero(0, cx);
+  residual(0, cw, cx, cr);
+  vcycle(0);  // cr -> cz
+  double nrm = std::sqrt(dot(0, cz, cz));
   *n0 = *nf = nrm;
   if (hist) hist[0] = nrm;
   *its = 0;
@@ -600,22 +767,22 @@ int ElastSolver::solve(const double* b, double* x, double rtol, double atol, int
   if (nrm <= tol) {
     *reason = nrm <= atol ? 1 : 0;
   } else {
-    vec(top, 0, 1.0, 0.0, cz, cp);
-    double rz = dot(top, cr, cz);
+    vec(0, 0, 1.0, 0.0, cz, cp);
+    double rz = dot(0, cr, cz);
     for (int it = 1; it <= max_its; ++it) {
-      apply(top, cp, cw);
-      const double pw = dot(top, cp, cw);
+      apply(0, cp, cw);
+      const double pw = dot(0, cp, cw);
       if (pw <= 0.0 || !std::isfinite(pw)) {
         *reason = 4;
         rc = 2;
         break;
       }
       const double alpha = rz / pw;
-      vec(top, 1, alpha, 0.0, cp, cx);
-      vec(top, 1, -alpha, 0.0, cw, cr);
-      vcycle(top, cr, cz);
-      const double rz_new = dot(top, cr, cz);
-      nrm = std::sqrt(dot(top, cz, cz));
+      vec(0, 1, alpha, 0.0, cp, cx);
+      vec(0, 1, -alpha, 0.0, cw, cr);
+      vcycle(0);
+      const double rz_new = dot(0, cr, cz);
+      nrm = std::sqrt(dot(0, cz, cz));
       *its = it;
       *nf = nrm;
       if (hist) hist[it] = nrm;
@@ -630,10 +797,10 @@ int ElastSolver::solve(const double* b, double* x, double rtol, double atol, int
       }
       const double beta = rz_new / rz;
       rz = rz_new;
-      vec(top, 4, beta, 0.0, cz, cp);  // p = z + beta p
+      vec(0, 4, beta, 0.0, cz, cp);  // p = z + beta p
     }
   }
-  if (x) download(top, cx, x);
+  if (x) download(0, cx, x);
   CK(cudaEventRecord(e1, W.stream));
   CK(cudaEventSynchronize(e1));
   float ms = 0.f;

@@ -598,14 +598,20 @@ void Solver::wire_transport() {
     rank_sums = arena.alloc(2LL * W.R);
     return;
   }
-  long long off = 2LL * W.R;
+  mailbox = wire_plans(W, arena, plans, 2LL * W.R, peer_mail);
+  rank_sums = mailbox;
+}
+
+double* wire_plans(World& W, DeviceArena& arena, const std::vector<RegionPlan*>& plans, long long head,
+                   std::vector<double*>& peer_mail) {
+  long long off = head;
   for (RegionPlan* p : plans) {
     p->mb_off = off;
     off += p->recv_total;
   }
-  mailbox = arena.alloc(off);
-  sync();
-  rank_sums = mailbox;
+  double* mailbox = arena.alloc(off);
+  CK(cudaStreamSynchronize(W.stream));
+  W.check();
   for (RegionPlan* p : plans) p->recvbuf = p->recv_total ? mailbox + p->mb_off : nullptr;
   // publication: handle, then per plan {send_total, nrecvs, (src proc, segment offset)...}
   std::string mine;
@@ -665,6 +671,7 @@ void Solver::wire_transport() {
     arena.upload(p.d_pack, p.pack_h.data(), sizeof(CopyDesc) * p.pack_h.size());
   }
   W.grp->barrier();
+  return mailbox;
 }
 
 // Galerkin coarse operators (mg_setup with galerkin; ptap dist_matrix.cpp:462-468):
@@ -1143,16 +1150,18 @@ void Solver::tb_side(Node& nd, size_t q, const double* xin, double* xout, bool p
 // Cross-process scalar reduction: every process stores its rank slots into every peer's
 // rank_sums, then one stream barrier; each process then sums the slots in rank order itself
 // (identical on all processes, and identical to the single-process sum).
-void Solver::device_allreduce_ranksums(int nslots) {
+void Solver::device_allreduce_ranksums(int nslots) { push_ranksums(W, rank_sums, nslots, peer_mail, rs_last_bar); }
+
+void push_ranksums(World& W, double* rank_sums, int nslots, const std::vector<double*>& peer_mail, long long& last_bar) {
   if (W.P == 1) return;
-  if (rs_last_bar == W.nbar) W.stream_barrier();  // peers done reading the previous values
+  if (last_bar == W.nbar) W.stream_barrier();  // peers done reading the previous values
   PtrTable peers{};
   int np = 0;
   for (int q = 0; q < W.P; ++q)
     if (q != W.me) peers.p[np++] = peer_mail[(size_t)q];
   W.cnt.launches += launch_push_ranksums(rank_sums, W.R, nslots, W.first, W.end, peers, np, W.stream);
   W.stream_barrier();
-  rs_last_bar = W.nbar;
+  last_bar = W.nbar;
   W.cnt.allreduces++;
 }
 

@@ -148,6 +148,14 @@ PlanHost halo_plan_host(const Owners& W, const Dist& D);
 PlanHost transfer_plan_host(const Owners& W, const Dist& S, const Dist& T);
 RegionPlan upload_plan(DeviceArena& A, const PlanHost& h);
 void run_plan(World& W, RegionPlan& plan, const Field& src, const Field& dst, bool telescope);
+// Cross-process wiring (P > 1): one CUDA-IPC mailbox per process holding `head` doubles (the
+// rank-sum slots) followed by every plan's receive area; pack descriptors are rewired to the
+// peers' mailboxes. Collective; returns this process's mailbox.
+double* wire_plans(World& W, DeviceArena& A, const std::vector<RegionPlan*>& plans, long long head,
+                   std::vector<double*>& peer_mail);
+// Rank-ordered allreduce of [2][R] rank-sum slots: this process's slots stored into every peer's
+// mailbox head, then a stream barrier (no-op when P == 1).
+void push_ranksums(World& W, double* rank_sums, int nslots, const std::vector<double*>& peer_mail, long long& last_bar);
 
 struct ProblemDesc {
   int kind = 0;  // 0 POISSON7, 1 VARCOEF7_HARMONIC

@@ -90,7 +90,7 @@ EXPORTS = [
     "tmgx_options_create", "tmgx_options_destroy", "tmgx_options_parse", "tmgx_options_parse_file_text",
     "tmgx_options_set", "tmgx_options_get", "tmgx_options_serialize", "tmgx_options_unused",
     "tmgx_options_resolve", "tmgx_solver_from_options", "tmgx_telescope_timing",
-    "tmgx_elast_create", "tmgx_elast_destroy", "tmgx_elast_kref", "tmgx_elast_level_info", "tmgx_elast_rhs",
+    "tmgx_elast_create", "tmgx_elast_create_mg", "tmgx_elast_destroy", "tmgx_elast_kref", "tmgx_elast_level_info", "tmgx_elast_rhs",
     "tmgx_elast_level_apply", "tmgx_elast_level_smooth", "tmgx_elast_pc_apply", "tmgx_elast_solve",
     "tmgx_elast_bench_apply",
 ]
@@ -162,6 +162,7 @@ def load(parity: bool = False):
         "tmgx_options_resolve": [C.c_void_p, C.c_char_p, C.c_char_p, P(_MG), P(_Ksp), C.c_char_p, C.c_int],
         "tmgx_telescope_timing": [C.c_void_p, C.c_int, C.c_int, D, D, I64],
         "tmgx_elast_create": [C.c_void_p, I64, C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_double, P(C.c_void_p)],
+        "tmgx_elast_create_mg": [C.c_void_p, I64, P(_MG), C.c_uint64, C.c_double, P(C.c_void_p)],
         "tmgx_elast_destroy": [C.c_void_p],
         "tmgx_elast_kref": [C.c_double, D],
         "tmgx_elast_level_info": [C.c_void_p, C.c_int, I64, D, D],
@@ -783,18 +784,25 @@ def elast_kref(nu=0.3, parity=False):
 
 
 class ElastSolver:
-    """Q1 hexahedral elasticity MG-CG on one GPU (tmgx_elast.cu): N^3 vertices x 3 dofs,
-    log-uniform E per element, clamped x = 0, body force (0, 0, -1), point-block Jacobi
-    Chebyshev V(m,m), rediscretised coarse levels, LU on level 0. Vectors in natural vertex
-    order with 3 interleaved dofs."""
+    """Q1 hexahedral elasticity MG-CG (tmgx_elast.cu): N^3 vertices x 3 dofs, log-uniform E per
+    element, clamped x = 0, body force (0, 0, -1), point-block Jacobi Chebyshev V(m,m),
+    rediscretised coarse levels, LU on level 0. The levels are split into the world's boxes
+    like the scalar path and may be telescoped (`telescope`: TelescopeStage list; cfg5 is 8
+    boxes with reduction factor 8 at level 3). Vectors in the level's global natural vertex
+    order with 3 interleaved dofs; each process reads / writes its own boxes' entries."""
 
-    def __init__(self, world: World, npoints, nlevels, smooth_its=2, est_mode=EST_LANCZOS, seed_e=11, nu=0.3):
+    def __init__(self, world: World, npoints, nlevels, smooth_its=2, est_mode=EST_LANCZOS, seed_e=11, nu=0.3,
+                 telescope: Optional[Sequence[TelescopeStage]] = None, cheb_bounds=None):
         self.world, self.L = world, world.L
         self.nlevels = nlevels
         npa = np.array(npoints, dtype=np.int64)
         h = C.c_void_p()
-        _check(self.L, self.L.tmgx_elast_create(world.h, _i64(npa), nlevels, smooth_its, est_mode, seed_e, nu,
-                                                C.byref(h)))
+        if cheb_bounds is not None and len(cheb_bounds) != 2 * nlevels:
+            raise ConfigError(f"elasticity: cheb_bounds needs 2 * nlevels = {2 * nlevels} values")
+        mg = MGConfig(nlevels=nlevels, smooth_its=smooth_its, est_mode=est_mode, cheb_bounds=cheb_bounds,
+                      telescope=list(telescope or []))
+        m, _keep = _c_mg(mg)
+        _check(self.L, self.L.tmgx_elast_create_mg(world.h, _i64(npa), C.byref(m), seed_e, nu, C.byref(h)))
         self.h = h
 
     def __del__(self):

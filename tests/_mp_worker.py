@@ -40,3 +40,25 @@ def solve_slice(job, n_ranks, nproc, proc, case, q):
         w.close()
     except Exception as e:  # noqa: BLE001
         q.put((proc, repr(e)))
+
+
+def elast_slice(job, n_ranks, nproc, proc, case, q):
+    """One process of a multi-process World running the Q1 elasticity MG-CG: V-cycle and solve;
+    returns the global-order vectors with this process's boxes filled (zeros elsewhere)."""
+    import numpy as np
+
+    from paper_1604_07163_b200 import tmgx as T
+
+    try:
+        n, nl, tele, parity = case
+        w = T.World(n_ranks=n_ranks, nproc=nproc, proc=proc, device=0, job=job, parity=parity)
+        s = T.ElastSolver(w, (n,) * 3, nl, smooth_its=2, telescope=[T.TelescopeStage(*t) for t in tele])
+        b = s.rhs()
+        y = s.pc_apply(b)
+        x, rep = s.solve(b, cfg=T.KrylovConfig("cg", rtol=1e-6, initial_guess_nonzero=False))
+        bnds = [s.bounds(l) for l in range(1, nl)]
+        q.put((proc, dict(y=y, x=x, its=rep.iterations, hist=np.asarray(rep.residual_history), bounds=bnds)))
+        del s
+        w.close()
+    except Exception as e:  # noqa: BLE001
+        q.put((proc, repr(e)))

@@ -116,6 +116,25 @@ def test_cfg5_perf():
     compare(fx, x, rep)
 
 
+def test_cfg5_boxes_telescoped():
+    """cfg5's own layout (BASELINE configs[4]): 8 boxes, telescope reduction factor 8 at level 3,
+    on one GPU; against the one-box elasticity oracle fixture (iterations +-1, 1e-9)."""
+    fx = fixture("cfg5")
+    w = T.World(8)
+    s = T.ElastSolver(w, tuple(fx["np"]), fx["nlevels"], smooth_its=fx["m"], telescope=[T.TelescopeStage(3, 8)])
+    b = s.rhs()
+    x, rep = s.solve(b, cfg=T.KrylovConfig("cg", rtol=fx["rtol"], initial_guess_nonzero=False))
+    assert rep.converged()
+    its = fx["iterations"]
+    assert abs(rep.iterations - its) <= 1, (rep.iterations, its)
+    if rep.iterations != its:
+        x, rep = s.solve(b, cfg=T.KrylovConfig("cg", rtol=0.0, max_its=its, initial_guess_nonzero=False))
+    xn = float(np.linalg.norm(x))
+    assert abs(xn - fx["xnorm"]) / fx["xnorm"] < TOL, (xn, fx["xnorm"])
+    samp = np.asarray(fx["x_sample"])
+    assert np.linalg.norm(x[:: fx["sample_stride"]] - samp) / np.linalg.norm(samp) < TOL
+
+
 def test_cfg5_parity_bitwise():
     fx = fixture("cfg5")
     x, rep = run(fx, parity=True)

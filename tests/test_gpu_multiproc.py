@@ -83,3 +83,43 @@ def test_multiprocess_equals_single_process(case, parity):
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     with open(os.path.join(ROOT, "gpurun_out", "multiproc_exchange.jsonl"), "a") as f:
         f.write(json.dumps(rec) + "\n")
+
+
+# Q1 elasticity (cfg5's layout, scaled): (name, n, nlevels, telescope stages, R, P)
+ELAST_CASES = [
+    ("elast cfg5@8: r=8 at L2", 65, 5, [(2, 8)], 8, 8),
+    ("elast 8 boxes on 2 processes", 33, 4, [(1, 8)], 8, 2),
+]
+
+
+@pytest.mark.parametrize("parity", [False, True])
+@pytest.mark.parametrize("case", ELAST_CASES, ids=[c[0] for c in ELAST_CASES])
+def test_elast_multiprocess_equals_single_process(case, parity):
+    """The elasticity V-cycle and solve over P processes equal the one-process run with the same
+    R boxes bit for bit (halos and telescope transfers per component through the mailboxes,
+    rank-ordered dot sums)."""
+    name, n, nl, tele, R, P = case
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    job = "e" + secrets.token_hex(8)
+    ps = [ctx.Process(target=W.elast_slice, args=(job, R, P, p, (n, nl, tele, parity), q)) for p in range(P)]
+    for p in ps:
+        p.start()
+    out = dict(q.get(timeout=900) for _ in ps)
+    for p in ps:
+        p.join(timeout=120)
+    for p in range(P):
+        assert not isinstance(out[p], str), f"process {p}: {out[p]}"
+    w = T.World(n_ranks=R, parity=parity)
+    s = T.ElastSolver(w, (n,) * 3, nl, smooth_its=2, telescope=[T.TelescopeStage(*t) for t in tele])
+    b = s.rhs()
+    y1 = s.pc_apply(b)
+    x1, r1 = s.solve(b, cfg=T.KrylovConfig("cg", rtol=1e-6, initial_guess_nonzero=False))
+    for lv in range(1, nl):
+        assert all(out[p]["bounds"][lv - 1] == s.bounds(lv) for p in range(P))
+    y = sum(out[p]["y"] for p in range(P))
+    x = sum(out[p]["x"] for p in range(P))
+    assert np.array_equal(y, y1), "V-cycle differs from the single-process run"
+    assert all(out[p]["its"] == r1.iterations for p in range(P))
+    assert np.array_equal(out[0]["hist"], r1.residual_history)
+    assert np.array_equal(x, x1), "solve differs from the single-process run"
