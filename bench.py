@@ -30,8 +30,8 @@ CONFIGS = {
     "cfg2": ((257, 257, 257), 7, 2, 0, 3, 1e-8),
     "cfg3": ((513, 513, 513), 8, 3, 1, 4, 1e-8),
     "cfg4w": ((257, 257, 257), 7, 2, 0, 4, 1e-8),
-    # Q1 elasticity, 3 dof/vertex (kind 2): one GPU, no telescope on this path yet
-    "cfg5": ((129, 129, 129), 6, 2, 2, None, 1e-6),
+    # Q1 elasticity, 3 dof/vertex (kind 2): N boxes, telescoped r = N at level 3 (BASELINE configs[4])
+    "cfg5": ((129, 129, 129), 6, 2, 2, 3, 1e-6),
     # weak scaling, 257^3 per GPU (true-weak series): the global grid and the
     # nested telescope stages depend on N (resolve())
     "cfg4": ((257, 257, 257), 7, 2, 0, "nested", 1e-8),
@@ -223,21 +223,35 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def run_elast(args, world, rank, np3, nlevels, m, rtol, dist):
-    """BASELINE configs[4]: Q1 elasticity MG-CG, one GPU (ElastSolver). value = DOF/s with b, x
-    resident in HBM; e2e through tmgx_elast_solve with pinned host b / x."""
+def run_elast(args, world, rank, local, np3, nlevels, m, rtol, stages, dist):
+    """BASELINE configs[4]: Q1 elasticity MG-CG (ElastSolver). One box per GPU; with N > 1 the
+    levels <= 3 are telescoped onto GPU 0 (reduction factor N). value = DOF/s with b, x resident in
+    HBM; e2e through tmgx_elast_solve with pinned host b / x. Device times: max over ranks."""
     import torch
 
     from paper_1604_07163_b200 import tmgx as T
 
-    if world > 1:
-        if rank == 0:
-            print(json.dumps({"metric": "MG-CG DOF/s (time-to-solution)", "unavailable":
-                              "elasticity path runs on one GPU (no box split / telescope yet)"}))
-        return
-    w = T.World(1)
+    job = None
+    if world > 1:  # node-local rendezvous name for the peer-memory transport
+        obj = [T.job_token() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        job = obj[0]
+
+    def max_over_ranks(v):
+        if not dist:
+            return v
+        t = torch.tensor([v], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+
+    w = T.World(n_ranks=world, nproc=world, proc=rank, device=local, job=job)
     t0 = time.perf_counter()
-    s = T.ElastSolver(w, np3, nlevels, smooth_its=m)
+    s = T.ElastSolver(w, np3, nlevels, smooth_its=m, telescope=[T.TelescopeStage(lv, r) for lv, r in stages])
     t_setup = time.perf_counter() - t0
     b_np = s.rhs()
     n_dof = b_np.size
@@ -246,29 +260,43 @@ def run_elast(args, world, rank, np3, nlevels, m, rtol, dist):
     x_dev = torch.zeros_like(b_dev)
     for _ in range(max(args.warmup, 0)):
         rep = s.solve_ptr(b_dev.data_ptr(), x_dev.data_ptr(), cfg)
-    torch.cuda.synchronize()
+    barrier()
     dev_t, its = 0.0, 0
-    with ClockSampler(0) as clk:
+    with ClockSampler(local) as clk:
         for _ in range(args.steps):
             rep = s.solve_ptr(b_dev.data_ptr(), x_dev.data_ptr(), cfg)
             dev_t += rep.t_solve_s
             its = rep.iterations
-        torch.cuda.synchronize()
+        barrier()
+    dev_t = max_over_ranks(dev_t)
     b_host = torch.from_numpy(b_np).pin_memory()
     x_host = torch.zeros(n_dof, dtype=torch.float64).pin_memory()
     s.solve_ptr(b_host.data_ptr(), x_host.data_ptr(), cfg)
+    barrier()
     e2e_t = 0.0
     for _ in range(args.steps):
         t1 = time.perf_counter()
         s.solve_ptr(b_host.data_ptr(), x_host.data_ptr(), cfg)
         e2e_t += time.perf_counter() - t1
+    barrier()
+    e2e_t = max_over_ranks(e2e_t)
     ms, by, fl = s.bench_apply(20)
+    ms = max_over_ranks(ms)
+    if rank != 0:
+        return
     # k_el_apply is fp64-FMA bound (576 FMAs per vertex): the roofline is the B200 fp64 vector
-    # peak. MEASURED_PEAKS.json has none, so the nominal figure: 148 SMs x 64 DFMA/clk x 2 flop x
-    # 1.965 GHz = 37.2 TFLOP/s.
-    fp64_peak = 148 * 64 * 2 * 1.965e9 / 1e12
+    # peak. MEASURED_PEAKS.json has none; profiles/r04_fp64_peak.json holds the one measured on
+    # this pool's B200 (tools/fp64_peak: 8 independent DFMA chains per thread, full occupancy),
+    # else the nominal 148 SMs x 64 DFMA/clk x 2 flop x 1.965 GHz = 37.2 TFLOP/s.
+    fp64_peak, fp64_kind = 148 * 64 * 2 * 1.965e9 / 1e12, "nominal (148 SMs x 64 DFMA/clk x 1.965 GHz)"
+    try:
+        with open(os.path.join(ROOT, "profiles", "r04_fp64_peak.json")) as f:
+            fp64_peak = float(json.load(f)["fp64_tflops"])
+        fp64_kind = "measured (tools/fp64_peak on a B200 of this pool, profiles/r04_fp64_peak.json)"
+    except Exception:
+        pass
     cpu = None
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:
         # the elasticity oracle (C, OpenMP over the host cores) on a bounded sample: the same
         # algorithm at 65^3 x 3 dofs, 5 levels (the 129^3 problem takes ~1 min per solve there)
         from oracle import oracle as O
@@ -284,19 +312,21 @@ def run_elast(args, world, rank, np3, nlevels, m, rtol, dist):
                                          f"{t_cpu:.2f} s"}
     line = {
         "metric": "MG-CG DOF/s (time-to-solution)", "value": n_dof * args.steps / dev_t, "unit": "DOF/s",
-        "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_t / args.steps * 1e3,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_t / args.steps * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded log-uniform element moduli, body force)",
         "config": {"workload": f"cfg5: {np3[0]}^3 Q1 elasticity x3 dof {nlevels}-level MG V({m},{m}) "
                                f"Cheb-point-block-Jacobi CG rtol {rtol:g}", "global_batch": 1,
-                   "seq_len": np3[0], "parallelism": "box1", "iterations": its, "t_setup_s": t_setup,
+                   "seq_len": np3[0], "parallelism": f"box{world}" + (f", telescope r={world} at L{stages[0][0]}"
+                                                                      if stages else ""),
+                   "iterations": its, "t_setup_s": t_setup,
                    "l2": "inputs larger than L2 (b, x 155 MB each)"},
         "e2e": {"value": n_dof * args.steps / e2e_t, "unit": "DOF/s", "h2d_bytes_per_step": 8 * n_dof,
                 "d2h_bytes_per_step": 8 * n_dof},
         "gpu_launches": rep.kernel_launches * args.steps,
         "roofline": {"bound": "fp64", "achieved": fl / (ms * 1e-3) / 1e12, "peak": fp64_peak, "unit": "TFLOP/s",
                      "frac": fl / (ms * 1e-3) / 1e12 / fp64_peak, "traffic": None,
-                     "peak_kind": "nominal (148 SMs x 64 DFMA/clk x 1.965 GHz; no measured fp64 peak)",
+                     "peak_kind": fp64_kind,
                      "kernel": "k_el_apply (Q1 elasticity operator, fine level)", "ms_per_launch": ms,
                      "flops_per_launch": fl, "bytes_per_launch": by,
                      "hbm_GBs": by / (ms * 1e-3) / 1e9},
@@ -345,7 +375,7 @@ def main():
     np3, nlevels, m, kind, stages, rtol, scaling = resolve(args.config, world)
     tele_level = stages[0][0] if stages else None
     if kind == 2:
-        run_elast(args, world, rank, np3, nlevels, m, rtol, dist)
+        run_elast(args, world, rank, local, np3, nlevels, m, rtol, stages, dist)
         return
     est = T.EST_LANCZOS if args.est == "lanczos" else T.EST_REFERENCE
 
