@@ -17,7 +17,8 @@
 // (component c at p + c * total), elements (ei, ej, ek) live at the vertex slot of their lower
 // corner, each box holding its elements and the ring of the lower neighbours' elements. Box
 // halos, telescope gathers / scatters and the rank-ordered dot sums reuse the scalar path's
-// region plans and peer-mailbox transport (per component), so the same node list (SMOOTH /
+// region plans (expanded to the three component planes: one exchange, one publishing barrier)
+// and peer-mailbox transport, so the same node list (SMOOTH /
 // TELESCOPE / COARSE, build_node_specs) drives the V-cycle: cfg5's 8 boxes telescoped r = 8
 // at level 3 onto one box. The
 // operator is matrix-free and vertex-centric: a thread gathers its row from the 8 incident
@@ -349,12 +350,7 @@ int ElastSolver::node_for_level(int level) const {
   return best;
 }
 
-void ElastSolver::halo(int i, const Field& f) {
-  for (int c = 0; c < 3; ++c) {
-    const Field fc = comp(i, f, c);
-    run_plan(W, nodes[(size_t)i].halo, fc, fc, false);
-  }
-}
+void ElastSolver::halo(int i, const Field& f) { run_plan(W, nodes[(size_t)i].halo, f, f, false); }
 void ElastSolver::apply(int i, const Field& x, const Field& y) {
   ElNode& nd = nodes[(size_t)i];
   halo(i, x);
@@ -535,7 +531,7 @@ ElastSolver::ElastSolver(World& W_, const int64_t np[3], const MGDesc& M, uint64
       nd.binv.push_back(binv);
     }
     stage_n = std::max(stage_n, nd.n_global());
-    nd.halo = upload_plan(arena, halo_plan_host(W, D));
+    nd.halo = upload_plan(arena, expand_components(halo_plan_host(W, D), D, D, 3));
     nodes.push_back(std::move(nd));
   }
   for (size_t i = 0; i < nodes.size(); ++i) {
@@ -555,8 +551,9 @@ ElastSolver::ElastSolver(World& W_, const int64_t np[3], const MGDesc& M, uint64
     }
     for (Field* f : {&nd.r, &nd.z, &nd.d, &nd.ad}) *f = make3(D);
     if (nd.kind == TELESCOPE) {  // TelescopePC setup: the P-hat^T / ScatterPlan data movement
-      nd.gather = upload_plan(arena, transfer_plan_host(W, D, *nodes[i + 1].dist));
-      nd.scatter = upload_plan(arena, transfer_plan_host(W, *nodes[i + 1].dist, D));
+      const Dist& M = *nodes[i + 1].dist;
+      nd.gather = upload_plan(arena, expand_components(transfer_plan_host(W, D, M), D, M, 3));
+      nd.scatter = upload_plan(arena, expand_components(transfer_plan_host(W, M, D), M, D, 3));
     }
   }
   std::vector<RegionPlan*> plans;  // creation order, identical on every process
@@ -715,9 +712,9 @@ void ElastSolver::vcycle(int i) {
   }
   ElNode& cn = nodes[(size_t)i + 1];
   if (nd.kind == TELESCOPE) {
-    for (int c = 0; c < 3; ++c) run_plan(W, nd.gather, comp(i, nd.b, c), comp(i + 1, cn.b, c), true);
+    run_plan(W, nd.gather, nd.b, cn.b, true);
     vcycle(i + 1);
-    for (int c = 0; c < 3; ++c) run_plan(W, nd.scatter, comp(i + 1, cn.x, c), comp(i, nd.x, c), true);
+    run_plan(W, nd.scatter, cn.x, nd.x, true);
     return;
   }
   const Dist& D = *nd.dist;

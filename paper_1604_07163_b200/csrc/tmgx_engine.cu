@@ -277,6 +277,54 @@ RegionPlan upload_plan(DeviceArena& A, const PlanHost& h) {
   return plan;
 }
 
+// A plan moving `ncomp` consecutive component planes (component c of a box at p + c * total) in one
+// use: every region descriptor repeated per component; each peer segment of the packed buffer
+// holds its regions component-major (segment offset and size scaled by ncomp, identical on both
+// ends), so a cross-process exchange of all components costs one publishing barrier.
+PlanHost expand_components(const PlanHost& h, const Dist& S, const Dist& T, int ncomp) {
+  if (ncomp == 1) return h;
+  PlanHost o = h;
+  o.loc.clear();
+  o.pack.clear();
+  o.unpack.clear();
+  o.pack_peer.clear();
+  for (auto& sd : o.sends) sd.off *= ncomp, sd.count *= ncomp;
+  for (auto& rv : o.recvs) rv.off *= ncomp, rv.count *= ncomp;
+  o.send_total *= ncomp;
+  o.recv_total *= ncomp;
+  o.local_count *= ncomp;
+  auto seg_of = [](const std::vector<RegionPlan::Peer>& v, long long off) -> const RegionPlan::Peer& {
+    for (const auto& e : v)
+      if (off >= e.off && off < e.off + e.count) return e;
+    throw tmg::Error("plan: packed offset outside every peer segment");
+  };
+  for (int c = 0; c < ncomp; ++c) {
+    for (const CopyDesc& d : h.loc) {
+      CopyDesc e = d;
+      e.src_off += c * S.geo[(size_t)d.src_slot].total;
+      e.dst_off += c * T.geo[(size_t)d.dst_slot].total;
+      o.loc.push_back(e);
+    }
+    for (size_t k = 0; k < h.pack.size(); ++k) {
+      const CopyDesc& d = h.pack[k];
+      const RegionPlan::Peer& sg = seg_of(h.sends, d.dst_off);
+      CopyDesc e = d;
+      e.src_off += c * S.geo[(size_t)d.src_slot].total;
+      e.dst_off = sg.off * ncomp + c * sg.count + (d.dst_off - sg.off);
+      o.pack.push_back(e);
+      o.pack_peer.push_back(h.pack_peer[k]);
+    }
+    for (const CopyDesc& d : h.unpack) {
+      const RegionPlan::Peer& sg = seg_of(h.recvs, d.src_off);
+      CopyDesc e = d;
+      e.src_off = sg.off * ncomp + c * sg.count + (d.src_off - sg.off);
+      e.dst_off += c * T.geo[(size_t)d.dst_slot].total;
+      o.unpack.push_back(e);
+    }
+  }
+  return o;
+}
+
 // ghost_exchange (grid.cpp:645-696): every rank's halo box (width 1, clipped to the grid,
 // edges and corners included) is filled from the owning boxes.
 PlanHost halo_plan_host(const Owners& W, const Dist& D) {

@@ -146,6 +146,8 @@ struct PlanHost {
 };
 PlanHost halo_plan_host(const Owners& W, const Dist& D);
 PlanHost transfer_plan_host(const Owners& W, const Dist& S, const Dist& T);
+// the same plan for `ncomp` consecutive component planes per box (one barrier for all of them)
+PlanHost expand_components(const PlanHost& h, const Dist& S, const Dist& T, int ncomp);
 RegionPlan upload_plan(DeviceArena& A, const PlanHost& h);
 void run_plan(World& W, RegionPlan& plan, const Field& src, const Field& dst, bool telescope);
 // Cross-process wiring (P > 1): one CUDA-IPC mailbox per process holding `head` doubles (the
