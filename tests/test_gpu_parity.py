@@ -211,7 +211,11 @@ def test_mgcg_varcoef(parity, np3, nl, m):
     the reference algorithm needs hundreds of CG iterations here (SURVEY §7 'Var-coef with 1e4
     contrast'). The parity build reproduces the oracle solve bit for bit (iterations, history,
     solution); the FMA/tree-reduction build drifts by a few iterations over such long Krylov
-    runs, so its bar is iterations within 2% and 1e-8 at equal iteration counts."""
+    runs, so its bar is iterations within 2% and 1e-8 at equal iteration counts. Measured
+    (tools/varcoef_drift.py, profiles/r04_varcoef_perf_drift.jsonl): 33^3 V(3,3) 362 vs 367
+    iterations, 7.6e-10 max-rel at equal counts; 65x65x33 V(2,2) 1037 vs 1050, 7.2e-9 -- the
+    north_star +-1 / 1e-9 bar holds for the Galerkin north-star problem (cfg3g, 49 its), not for
+    these ~10^3-iteration rediscretised runs."""
     om = oracle_mg(np3, nl, O.VARCOEF7, m=m)
     b = O.rhs(np3, 1234)
     xo, orep = om.solve(b, rtol=1e-8)
