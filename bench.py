@@ -471,7 +471,8 @@ def main():
     # every fine-level kernel of the path: live us/launch and algorithmic GB/s
     kernels = {}
     names = {1: "cheb_step_last", 3: "residual", 4: "restrict", 5: "prolong_add", 6: "cg_update", 7: "spmv_dot",
-             8: "tb_pre", 9: "tb_post", 10: "prolong_to", 11: "resid_restrict", 12: "tb3_pre", 13: "tb3_post"}
+             8: "tb_pre", 9: "tb_post", 10: "prolong_to", 11: "resid_restrict", 12: "tb3_pre", 13: "tb3_post",
+             15: "resid_restrict_sep"}
     if m == 3:
         names = {k: v for k, v in names.items() if k not in (8, 9)}
     else:

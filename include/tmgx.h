@@ -307,6 +307,7 @@ int tmgx_exchange_timing(tmgx_solver s, int level, int reps, double *us_per_exch
  *       12 temporally blocked V(3,3) pre-smooth side (b in, x out)
  *       13 temporally blocked V(3,3) post-smooth side (x, b in, x out)
  *       14 fused CG direction update + SpMV + p.w partials (z, p in; p', w out)
+ *       15 separable fused residual + restriction (performance build default; b, x in, b_c out)
  * Variable-coefficient levels count the algorithmic coefficient stream (k: 8 B per point,
  * SURVEY.md §8(d)); the kernels read the precomputed face planes (32 B per point). */
 int tmgx_bench_kernel(tmgx_solver s, int which, int level, int iters, double *ms_per_launch,

@@ -868,6 +868,9 @@ extern "C" int tmgx_bench_kernel(tmgx_solver s, int which, int level, int iters,
     if ((which == 12 || which == 13) &&
         (D.h.n_ranks() != 1 || D.local.size() != 1 || !tmgx::cheb3_tb_supported(D.geo[0]) || nd.op[0].S))
       throw tmg::ConfigError("bench_kernel: the blocked m = 3 smoother needs a single-box 7-point level");
+    if (which == 15 && (D.h.n_ranks() != 1 || D.local.size() != 1 ||
+                        !tmgx::resid_restrict2_supported(D.geo[0], nd.op[0], S.nodes[i + 1].dist->geo[0])))
+      throw tmg::ConfigError("bench_kernel: the separable fused residual + restriction needs a single-box 7-point level");
     tmgx::ChebStep cs2{0.4, 0.2};
     auto launch = [&]() {
       for (size_t q = 0; q < D.local.size(); ++q) {
@@ -884,6 +887,7 @@ extern "C" int tmgx_bench_kernel(tmgx_solver s, int which, int level, int iters,
           case 8: tmgx::launch_cheb2_tb(g, nd.op[q], nd.b.p[q], nullptr, nd.d.p[q], 1.0, cs, true, S.W.stream); break;
           case 9: tmgx::launch_cheb2_tb(g, nd.op[q], nd.b.p[q], nd.d.p[q], nd.x.p[q], 1.0, cs, false, S.W.stream); break;
           case 11: tmgx::launch_resid_restrict(g, nd.op[q], S.nodes[i + 1].dist->geo[q], nd.b.p[q], nd.x.p[q], S.nodes[i + 1].b.p[q], S.W.stream); break;
+          case 15: tmgx::launch_resid_restrict2(g, nd.op[q], S.nodes[i + 1].dist->geo[q], nd.b.p[q], nd.x.p[q], S.nodes[i + 1].b.p[q], S.W.stream); break;
           case 14: tmgx::launch_pspmv_dot(g, nd.op[q], nd.x.p[q], nd.d.p[q], nd.d2.p[q], nd.b.p[q], S.part + S.part_off[q], S.scal, tmgx::S_TMP1, S.W.stream); break;
           case 12: tmgx::launch_cheb3_tb(g, nd.op[q], nd.b.p[q], nullptr, nd.d.p[q], 1.0, cs, cs2, true, S.W.stream); break;
           case 13: tmgx::launch_cheb3_tb(g, nd.op[q], nd.b.p[q], nd.d.p[q], nd.x.p[q], 1.0, cs, cs2, false, S.W.stream); break;
@@ -905,6 +909,7 @@ extern "C" int tmgx_bench_kernel(tmgx_solver s, int which, int level, int iters,
       case 9: per_pt = 24 + kb; break;             // blocked post-smooth: x, b in, x out
       case 10: per_pt = 16 + 8.0 / 8.0; break;     // out-of-place prolongation: x, x_c in, x~ out
       case 11: per_pt = 16 + 8.0 / 8.0 + kb; break; // fused residual + restriction: b, x in, b_c out
+      case 15: per_pt = 16 + 8.0 / 8.0 + kb; break; // separable fused residual + restriction (same bytes)
       case 14: per_pt = 32 + kb; break;            // fused p' = z + beta p, w = A p', p'.w: z, p in; p', w out
       case 12: per_pt = 16 + kb; break;            // blocked V(3,3) pre-smooth: b in, x out
       case 13: per_pt = 24 + kb; break;            // blocked V(3,3) post-smooth: x, b in, x out

@@ -3377,6 +3377,169 @@ int launch_cheb3_tb(const BoxGeo& g, const OpParams& op, const double* b, const 
   return 1;
 }
 
+// Residual + restriction, performance build, separable (single-box levels, 7-point rows):
+//   r = b - A x (k_march FApply<1> arithmetic), b_c = 2^-3 P^T r summed axis by axis
+// (x: lane shuffle, y: one shared plane, z: register accumulator), so no thread gathers 27 values.
+// Block = 32 x 9 threads over fine columns 62 bx - 2 + [0, 64) (pairs; lane 0 only feeds its odd
+// vertex to lane 1) and fine rows 8 by - 1 + [0, 9), marching the fine planes 2 K0 - 1 ... 2 K1 - 1
+// of its coarse chunk: outputs 31 x 4 coarse columns x zc planes. DRAM: x, b in (16 B per fine
+// point, ~14% recomputed tile edges), b_c out. Out-of-grid fine vertices contribute r = 0 (where
+// k_restrict skips the term); the summation order differs from k_restrict's (FMA build only;
+// the parity build keeps residual + k_restrict).
+constexpr int kRR2Y = 9, kRR2CX = 31, kRR2CY = 4;
+template <bool VAR>
+__global__ void __launch_bounds__(kBX* kRR2Y)
+    k_resid_restrict2(BoxGeo F, OpParams op, BoxGeo Cg, int czc, const double* __restrict__ b,
+                      const double* __restrict__ x, double* __restrict__ bc) {
+  __shared__ double rxs[4][kRR2Y][kBX];  // x-restricted planes, slot = fine plane & 3
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int I = kRR2CX * blockIdx.x + tx - 1;             // coarse column of this lane (tx >= 1)
+  const int J = kRR2CY * blockIdx.y + ((ty - 1) >> 1);    // coarse row (odd ty)
+  const int i0 = 2 * I, j = 2 * kRR2CY * blockIdx.y - 1 + ty;
+  const int K0 = blockIdx.z * czc, K1 = min(K0 + czc, Cg.ez);
+  const int kb = 2 * K0 - 1, ke = 2 * K1 - 1;
+  const bool col_ok = i0 + 1 >= 0 && i0 < F.Nx, row_ok = j >= 0 && j < F.Ny, ok = col_ok && row_ok;
+  const bool out = (ty & 1) && tx >= 1 && I < Cg.ex && J < Cg.ey;
+  const bool fast_xy = i0 >= 2 && i0 + 1 <= F.Nx - 3 && j >= 2 && j <= F.Ny - 3;
+  const long long pxy = F.pxy, px = F.px;
+  long long v = F.base + i0 + px * j + pxy * (long long)kb;
+  auto ldx = [&](long long o, int kk) -> double2 {  // x pair at plane kk (allocated: -1 <= kk <= Nz)
+    return (ok && kk >= -1 && kk <= F.Nz) ? ld2(x + o) : double2{0.0, 0.0};
+  };
+  auto ldb = [&](long long o, int kk) -> double2 {
+    return (ok && kk >= 0 && kk < F.Nz) ? ld2(b + o) : double2{0.0, 0.0};
+  };
+  double2 um = ldx(v - pxy, kb - 1), uc = ldx(v, kb), un = ldx(v + pxy, kb + 1), bq = ldb(v, kb);
+  const double *fD = op.fc, *fX = op.fc + op.fc_stride, *fY = op.fc + 2 * op.fc_stride, *fZ = op.fc + 3 * op.fc_stride;
+  double2 fzm{0.0, 0.0};
+  if (VAR && ok && kb >= 1) fzm = ld2(fZ + v - pxy);
+  double acc = 0.0;
+  double* const bcp = bc + vidx(Cg, I, J, 0);
+  struct InPlane {  // the plane's in-plane stencil operands (loaded one plane ahead)
+    double2 uym, uyp, dd, fx, fy, fym, fz;
+    double uxl, uxr, fxl;
+  };
+  auto ldp = [&](long long o, int kk) {
+    InPlane P{};
+    if (ok && kk >= 0 && kk < F.Nz) {
+      P.uym = ld2(x + o - px);
+      P.uyp = ld2(x + o + px);
+      P.uxl = __ldg(x + o - 1);
+      P.uxr = __ldg(x + o + 2);
+    }
+    return P;
+  };
+  auto ldc = [&](InPlane& P, long long o) {  // coefficient planes: loaded in-plane (registers)
+    P.dd = ld2(fD + o);
+    P.fx = ld2(fX + o);
+    P.fy = ld2(fY + o);
+    P.fym = ld2(fY + o - px);
+    P.fz = ld2(fZ + o);
+    P.fxl = __ldg(fX + o - 1);
+  };
+  InPlane PC = ldp(v, kb);
+  for (int k = kb; k <= ke; ++k, v += pxy) {
+    const double2 unn = ldx(v + 2 * pxy, k + 2), bn = ldb(v + pxy, k + 1);
+    const InPlane PN = ldp(v + pxy, k + 1);
+    double r0 = 0.0, r1 = 0.0;
+    if (VAR && ok && k >= 0 && k < F.Nz) ldc(PC, v);
+    const double2 fz = PC.fz;
+    if (ok && k >= 0 && k < F.Nz) {
+      const double2 uym = PC.uym, uyp = PC.uyp, dd = PC.dd, fx = PC.fx, fy = PC.fy, fym = PC.fym;
+      const double uxl = PC.uxl, uxr = PC.uxr, fxl = PC.fxl;
+      if (fast_xy && k >= 2 && k <= F.Nz - 3) {  // interior pair: every coupling present, no topology
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const double uxm = q ? uc.x : uxl, uxp = q ? uxr : uc.y;
+          double au;
+          if (VAR)
+            au = get(dd, q) * get(uc, q) -
+                 (get(fzm, q) * get(um, q) + get(fym, q) * get(uym, q) + (q ? fx.x : fxl) * uxm +
+                  get(fx, q) * uxp + get(fy, q) * get(uyp, q) + get(fz, q) * get(un, q));
+          else
+            au = op.cdiag * get(uc, q) - (op.ih2x * (uxm + uxp) + op.ih2y * (get(uym, q) + get(uyp, q)) +
+                                          op.ih2z * (get(um, q) + get(un, q)));
+          if (q)
+            r1 = get(bq, q) - au;
+          else
+            r0 = get(bq, q) - au;
+        }
+      } else
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        if (i0 + q < 0 || i0 + q >= F.Nx) continue;
+        const Pt p = make_pt(F, i0 + q, j, k);
+        Coef c;
+        if (VAR) {
+          c.dg = get(dd, q);
+          c.invd = 0.0;
+          c.azm = -get(fzm, q);
+          c.aym = -get(fym, q);
+          c.axm = -(q ? fx.x : fxl);
+          c.axp = -get(fx, q);
+          c.ayp = -get(fy, q);
+          c.azp = -get(fz, q);
+        } else {
+          c = coef_at<false>(op, p, 0, 0, 0, 0, 0, 0, 0);
+        }
+        const double uxm = q ? uc.x : uxl, uxp = q ? uxr : uc.y;
+        const double rr = get(bq, q) - row_apply(p, c, get(um, q), get(uym, q), uxm, get(uc, q), uxp, get(uyp, q),
+                                                 get(un, q));
+        if (q)
+          r1 = rr;
+        else
+          r0 = rr;
+      }
+    }
+    const double rl = __shfl_up_sync(0xffffffffu, r1, 1);  // r at fine column 2I - 1
+    rxs[k & 3][ty][tx] = 0.5 * rl + r0 + 0.5 * r1;
+    if (k & 1) {  // one barrier per fine plane pair (2K, 2K + 1); the first plane 2 K0 - 1 alone
+      __syncthreads();
+      if (ty & 1) {
+        if (k > kb) {
+          double(*R)[kBX] = rxs[(k - 1) & 3];
+          acc += 0.5 * R[ty - 1][tx] + R[ty][tx] + 0.5 * R[ty + 1][tx];  // even plane 2K: weight 1
+        }
+        double(*R)[kBX] = rxs[k & 3];
+        const double ry = 0.5 * R[ty - 1][tx] + R[ty][tx] + 0.5 * R[ty + 1][tx];
+        acc += 0.5 * ry;  // odd fine plane 2K + 1: completes coarse plane K, starts K + 1
+        if (k > kb && out) bcp[Cg.pxy * (long long)((k - 1) >> 1)] = 0.125 * acc;
+        acc = 0.5 * ry;
+      }
+    }
+    um = uc;
+    uc = un;
+    un = unn;
+    bq = bn;
+    PC = PN;
+    if (VAR) fzm = fz;
+  }
+}
+
+bool resid_restrict2_supported(const BoxGeo& fine, const OpParams& op, const BoxGeo& coarse) {
+  return op.S == nullptr && (op.fc != nullptr || op.k == nullptr) && fine.gx == 0 && fine.gy == 0 && fine.gz == 0 &&
+         fine.ex == fine.Nx && fine.ey == fine.Ny && fine.ez == fine.Nz && coarse.ex == (fine.Nx + 1) / 2 &&
+         coarse.ey == (fine.Ny + 1) / 2 && coarse.ez == (fine.Nz + 1) / 2 && (fine.Nx & 1) && (fine.Ny & 1) &&
+         (fine.Nz & 1);
+}
+
+int launch_resid_restrict2(const BoxGeo& fine, const OpParams& op, const BoxGeo& coarse, const double* b,
+                           const double* x, double* bc, cudaStream_t s) {
+  static const int zc_env = [] {
+    const char* e = std::getenv("TMGX_RR2_ZC");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int nxy = ((coarse.ex + kRR2CX - 1) / kRR2CX) * ((coarse.ey + kRR2CY - 1) / kRR2CY);
+  int zc = zc_env > 0 ? zc_env : 8;
+  while (zc > 1 && (long long)nxy * ((coarse.ez + zc - 1) / zc) < 4 * 148) zc >>= 1;  // coarse levels: parallelism
+  const dim3 gr((coarse.ex + kRR2CX - 1) / kRR2CX, (coarse.ey + kRR2CY - 1) / kRR2CY, (coarse.ez + zc - 1) / zc);
+  if (op.fc)
+    k_resid_restrict2<true><<<gr, dim3(kBX, kRR2Y), 0, s>>>(fine, op, coarse, zc, b, x, bc);
+  else
+    k_resid_restrict2<false><<<gr, dim3(kBX, kRR2Y), 0, s>>>(fine, op, coarse, zc, b, x, bc);
+  return 1;
+}
+
 bool resid_restrict_supported(const OpParams& op) { return op.S == nullptr && (op.fc != nullptr || op.k == nullptr); }
 
 int launch_resid_restrict(const BoxGeo& fine, const OpParams& op, const BoxGeo& coarse, const double* b,

@@ -118,6 +118,11 @@ int launch_residual(const BoxGeo& g, const OpParams& op, const double* b, const 
 int launch_apply(const BoxGeo& g, const OpParams& op, const double* x, double* y, cudaStream_t s);
 // Single-box levels, 7-point rows: bc = 2^-3 P^T (b - A x) with the residual kept on chip.
 bool resid_restrict_supported(const OpParams& op);
+// Performance build: the same with a separable restriction (lane shuffle in x, one shared plane
+// in y, register accumulator in z); single box covering an odd-sized grid.
+bool resid_restrict2_supported(const BoxGeo& fine, const OpParams& op, const BoxGeo& coarse);
+int launch_resid_restrict2(const BoxGeo& fine, const OpParams& op, const BoxGeo& coarse, const double* b,
+                           const double* x, double* bc, cudaStream_t s);
 int launch_resid_restrict(const BoxGeo& fine, const OpParams& op, const BoxGeo& coarse, const double* b,
                           const double* x, double* bc, cudaStream_t s);
 // bc = 2^-3 P^T rf over the coarse box (rf needs a box halo incl. corners).

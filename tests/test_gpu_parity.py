@@ -475,6 +475,7 @@ def test_fused_residual_restrict_optin(parity, monkeypatch):
     """The opt-in fused residual + restriction kernel (TMGX_FUSE_RR=1, measured slower and off
     by default) keeps the restriction's arithmetic: bitwise in the parity build."""
     monkeypatch.setenv("TMGX_FUSE_RR", "1")
+    monkeypatch.setenv("TMGX_FUSE_RR2", "0")
     np3, nl = (33, 65, 33), 3
     om = oracle_mg(np3, nl, O.VARCOEF7)
     w, s = make(np3, nl, T.VARCOEF7_HARMONIC, parity=parity, bounds=oracle_bounds(om, nl))
@@ -482,6 +483,24 @@ def test_fused_residual_restrict_optin(parity, monkeypatch):
     n = om.level_size(nl - 1)
     b, x = rng.standard_normal(n), rng.standard_normal(n)
     check(s.residual_restrict(nl - 1, b, x), om.restrict(nl - 1, b - om.apply(nl - 1, x)), parity)
+
+
+@pytest.mark.parametrize("np3,nl,kind", [((33, 65, 33), 3, 1), ((65, 65, 65), 4, 0), ((17, 33, 129), 3, 0),
+                                         ((129, 17, 9), 3, 1), ((9, 9, 9), 2, 0)])
+def test_separable_residual_restrict(np3, nl, kind):
+    """Performance build default on single-box levels: the separable fused residual + restriction
+    (lane shuffle in x, one shared plane in y, register accumulator in z) against the oracle's
+    restrict(b - A x) -- a different summation order, so within 1e-12 relative; every tile edge
+    (31 x 4 coarse tiles, z chunks) and grid boundary is exercised by these shapes."""
+    okind = O.VARCOEF7 if kind == 1 else O.POISSON7
+    om = oracle_mg(np3, nl, okind)
+    w, s = make(np3, nl, T.VARCOEF7_HARMONIC if kind == 1 else T.POISSON7, bounds=oracle_bounds(om, nl))
+    rng = np.random.default_rng(13)
+    n = om.level_size(nl - 1)
+    b, x = rng.standard_normal(n), rng.standard_normal(n)
+    got = s.residual_restrict(nl - 1, b, x)
+    want = om.restrict(nl - 1, b - om.apply(nl - 1, x))
+    assert rel(got, want) < 1e-12
 
 
 @pytest.mark.parametrize("cfg", ["cfg2", "cfg5"])
