@@ -57,6 +57,10 @@ def resolve(config, world):
 # algorithm needs ~500 CG iterations at 513^3).
 GALERKIN = {"cfg3": True}
 SEED_F = 1234
+# CPU legs (cpu_baseline, --impl reference): problems above CPU_SAMPLE_MAX_DOF are timed on a
+# bounded sample of at most CPU_SAMPLE_DOF vertices (cpu_reference_sample)
+CPU_SAMPLE_MAX_DOF = 40_000_000
+CPU_SAMPLE_DOF = 3_000_000
 SEED_K = 7
 
 
@@ -155,6 +159,17 @@ def cpu_reference_sample(config="cfg2", steps=1, warmup=0, galerkin=False, budge
     mean over `steps` complete solves. Returns (dof_per_s, seconds_per_solve, kind, description,
     iterations)."""
     np3, nlevels, m, kind_p, _, rtol, _ = resolve(config, world)
+    sample_note = "same problem as the GPU arm"
+    if np3[0] * np3[1] * np3[2] > CPU_SAMPLE_MAX_DOF and os.environ.get("TMGX_REF_FULL", "0") != "1":
+        # bounded sample (contract: the CPU leg must end within minutes): one complete solve of the
+        # 513^3 / 8-level problem takes ~45 min on one core, so the same algorithm (operator kind,
+        # V(m,m), coarse operators, rtol) runs at 129^3 with two levels fewer (the same 5^3 coarse
+        # grid). DOF/s of the reference is size-independent to ~10% between 129^3 and 257^3 (cfg2).
+        full = np3
+        while np3[0] * np3[1] * np3[2] > CPU_SAMPLE_DOF and nlevels > 2:
+            np3, nlevels = tuple((v - 1) // 2 + 1 for v in np3), nlevels - 1
+        sample_note = (f"BOUNDED SAMPLE of the GPU arm's {full[0]}x{full[1]}x{full[2]} problem (TMGX_REF_FULL=1 "
+                       f"times the full size): same operator and solver at")
     ref_bin = os.path.join(ROOT, "oracle", "_ref", "tmg_ref_bench")
     n = np3[0] * np3[1] * np3[2]
     if os.path.exists(ref_bin) and np3[0] == np3[1] == np3[2]:
@@ -188,7 +203,7 @@ def cpu_reference_sample(config="cfg2", steps=1, warmup=0, galerkin=False, budge
         t, its, kind = sum(ts) / len(ts), rep["iterations"], "port"
     impl = ("reference translation units + SPEC glue (oracle/_ref/tmg_ref_bench)" if kind == "reference"
             else "oracle C restatement (oracle/liboracle.so)")
-    desc = (f"same problem as the GPU arm: {np3[0]}x{np3[1]}x{np3[2]}, {nlevels}-level MG V({m},{m}) CG rtol "
+    desc = (f"{sample_note}: {np3[0]}x{np3[1]}x{np3[2]}, {nlevels}-level MG V({m},{m}) CG rtol "
             f"{rtol:g}, {its} its; {steps} timed complete solve(s) after {warmup} untimed, setup ({setup:.1f} s) "
             f"excluded; 1 rank on 1 core; {impl}")
     return n / t, t, kind, desc, its, steps
