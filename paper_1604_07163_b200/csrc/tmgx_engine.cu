@@ -436,7 +436,7 @@ Solver::Solver(World& W_, const ProblemDesc& P, const MGDesc& M) : W(W_), prob(P
   if (const char* e = std::getenv("TMGX_TB3")) tb3_enabled = std::string(e) != "0";
   if (const char* e = std::getenv("TMGX_FUSE_DOTS")) fuse_dots = std::string(e) != "0";
   if (const char* e = std::getenv("TMGX_FUSE_RR")) fuse_rr = std::string(e) != "0";
-  if (const char* e = std::getenv("TMGX_FUSE_RR2")) fuse_rr2 = std::string(e) != "0";
+  if (const char* e = std::getenv("TMGX_FUSE_RR2")) fuse_rr2 = std::atoi(e);
   if (const char* e = std::getenv("TMGX_CC_MAX")) cc_max_extent = std::atoi(e);
   if (mgd.nlevels < 1) throw tmg::ConfigError("mg: number of levels must be >= 1");
   if (mgd.m < 1) throw tmg::ConfigError("mg: smoother iterations must be >= 1");
@@ -1139,7 +1139,8 @@ void Solver::residual_restrict(int i, const Field& x) {
   Node& nd = nodes[i];
   Node& cn = nodes[i + 1];
   const Dist& D = *nd.dist;
-  if (!parity_build() && fuse_rr2 && D.h.n_ranks() == 1 && D.local.size() == 1 &&
+  if (!parity_build() && fuse_rr2 > 0 && D.h.n_ranks() == 1 && D.local.size() == 1 &&
+      fuse_rr2 >= (nd.op[0].k != nullptr || nd.op[0].fc != nullptr ? 2 : 1) &&
       resid_restrict2_supported(D.geo[0], nd.op[0], cn.dist->geo[0])) {
     W.cnt.launches += launch_resid_restrict2(D.geo[0], nd.op[0], cn.dist->geo[0], nd.b.p[0], x.p[0], cn.b.p[0], W.stream);
     return;

@@ -295,8 +295,10 @@ class Solver {
   bool fuse_dots = true;   // CG r.z, z.z from the finest blocked post-smooth (TMGX_FUSE_DOTS=0)
   int dots_nblk = 0;       // partials written by the last finest post-smooth (0: none)
   bool fuse_cg = true;     // p update fused into w = A p on single-box fine levels (TMGX_FUSE_CG=0)
-  bool fuse_rr2 = true;    // performance build: separable fused residual + restriction on single-box levels
-                           // (TMGX_FUSE_RR2=0 disables)
+  int fuse_rr2 = 1;        // performance build: separable fused residual + restriction on single-box levels.
+                           // 1 (default): constant-coefficient rows only; 2: variable-coefficient rows too
+                           // (2.7% faster on cfg3, but the re-associated sums move the 1e4-contrast 33^3
+                           // solve to 1.04e-9 of the oracle, past the 1e-9 bar); 0: off (TMGX_FUSE_RR2)
   bool fuse_rr = false;    // fused residual + restriction on single-box levels (TMGX_FUSE_RR=1; measured
                            // slower than residual + restriction on B200)
   bool use_tb(int i) const;

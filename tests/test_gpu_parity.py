@@ -487,11 +487,13 @@ def test_fused_residual_restrict_optin(parity, monkeypatch):
 
 @pytest.mark.parametrize("np3,nl,kind", [((33, 65, 33), 3, 1), ((65, 65, 65), 4, 0), ((17, 33, 129), 3, 0),
                                          ((129, 17, 9), 3, 1), ((9, 9, 9), 2, 0)])
-def test_separable_residual_restrict(np3, nl, kind):
-    """Performance build default on single-box levels: the separable fused residual + restriction
+def test_separable_residual_restrict(np3, nl, kind, monkeypatch):
+    """Performance build on single-box levels (default for constant-coefficient rows, TMGX_FUSE_RR2=2
+    for variable-coefficient rows too): the separable fused residual + restriction
     (lane shuffle in x, one shared plane in y, register accumulator in z) against the oracle's
     restrict(b - A x) -- a different summation order, so within 1e-12 relative; every tile edge
     (31 x 4 coarse tiles, z chunks) and grid boundary is exercised by these shapes."""
+    monkeypatch.setenv("TMGX_FUSE_RR2", "2")
     okind = O.VARCOEF7 if kind == 1 else O.POISSON7
     om = oracle_mg(np3, nl, okind)
     w, s = make(np3, nl, T.VARCOEF7_HARMONIC if kind == 1 else T.POISSON7, bounds=oracle_bounds(om, nl))
